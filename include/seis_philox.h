@@ -21,8 +21,10 @@
  *   draw 1 : w0w1 / w2w3 -> the two scalar draws of the move (birth t and x
  *            uniforms; event / station / partner indices by Lemire reduction)
  *   draw 2 : w0w1 -> joint-pair station-pair index
- *   draw 16+i : i-th standard normal of the step (birth: i = station j;
- *            location: 0 = x, 1 = t; arrival: 0; joint: 0..3)
+ *   draw 16+(i>>1) : i-th standard normal of the step from words w0w1 (i
+ *            even) or w2w3 (i odd), so one Philox call feeds a station pair
+ *            (birth: i = station j; location: 0 = x, 1 = t; arrival: 0;
+ *            joint: 0..3)
  */
 #ifndef SEIS_PHILOX_H
 #define SEIS_PHILOX_H
@@ -198,8 +200,16 @@ SEIS_HD float seis_bm(uint32_t w0, uint32_t w1) {
 
 SEIS_HD float seis_normal(uint64_t seed, uint32_t sweep, uint32_t region, uint32_t step,
                           uint32_t i) {
-  const seis_u32x4 d = seis_draw(seed, sweep, region, step, SEIS_DRAW_NORMAL0 + i);
-  return seis_bm(d.w[0], d.w[1]);
+  const seis_u32x4 d = seis_draw(seed, sweep, region, step, SEIS_DRAW_NORMAL0 + (i >> 1));
+  return (i & 1u) ? seis_bm(d.w[2], d.w[3]) : seis_bm(d.w[0], d.w[1]);
+}
+
+/* normals 2i and 2i+1 of a step from one Philox call */
+SEIS_HD void seis_normal_pair(uint64_t seed, uint32_t sweep, uint32_t region, uint32_t step,
+                              uint32_t i2, float* z0, float* z1) {
+  const seis_u32x4 d = seis_draw(seed, sweep, region, step, SEIS_DRAW_NORMAL0 + i2);
+  *z0 = seis_bm(d.w[0], d.w[1]);
+  *z1 = seis_bm(d.w[2], d.w[3]);
 }
 
 #endif /* SEIS_PHILOX_H */

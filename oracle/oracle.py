@@ -263,7 +263,7 @@ class Oracle:
 
     # -- partition.hpp
     def partition(self, T, l, offset, tau):
-        cap = int(T / l) + 16
+        cap = int(T / l) + 16 if l > 0 else 16
         b = np.zeros(cap)
         col = np.zeros(cap, np.int32)
         nr = i64(0)
@@ -332,3 +332,72 @@ class Oracle:
 
 def have_ref() -> bool:
     return os.path.exists(REF_SO)
+
+
+def ref_run_sampler(world: World, sampler: Sampler, workers: int = 1, cap: int = 1 << 16):
+    """The reference's own run_sampler (chromatic static/dynamic from empty)."""
+    L = C.CDLL(REF_SO)
+    f = L.sr_run_sampler
+    f.argtypes = [P, P, P, i64, i64, P, P, P, P, P, P, P, P]
+    m = world.model.c()
+    s = sampler.c()
+    S = world.model.S
+    ids = np.zeros(cap, np.uint64)
+    x = np.zeros(cap)
+    t = np.zeros(cap)
+    arr = np.zeros((cap, S))
+    n = i64(0)
+    ts = i64(0)
+    ta = i64(0)
+    wall = f64(0)
+    sig = np.ascontiguousarray(world.signals, np.float64)
+    rc = f(C.byref(m), _p(sig), C.byref(s), workers, cap, C.byref(n), _p(ids), _p(x), _p(t),
+           _p(arr), C.byref(ts), C.byref(ta), C.byref(wall))
+    if rc:
+        L.sr_last_error.restype = C.c_char_p
+        raise RuntimeError(L.sr_last_error().decode())
+    k = n.value
+    return dict(final=Events(ids[:k], x[:k], t[:k], arr[:k]), total_steps=ts.value,
+                total_accepted=ta.value, wall=wall.value)
+
+
+def ref_bench_region_steps(world: World, truth: Events, sampler: Sampler, threads: int,
+                           seconds: float, max_steps: int):
+    """CPU baseline: reference run_region_steps per thread on the truth world."""
+    L = C.CDLL(REF_SO)
+    f = L.sr_bench_region_steps
+    f.argtypes = [P, P, i64, P, P, P, P, P, i64, f64, i64, P, P]
+    m = world.model.c()
+    s = sampler.c()
+    sig = np.ascontiguousarray(world.signals, np.float64)
+    ids = np.ascontiguousarray(truth.ids, np.uint64)
+    x = np.ascontiguousarray(truth.x, np.float64)
+    t = np.ascontiguousarray(truth.t, np.float64)
+    arr = np.ascontiguousarray(truth.arr, np.float64)
+    props = i64(0)
+    wall = f64(0)
+    rc = f(C.byref(m), _p(sig), truth.N, _p(ids), _p(x), _p(t), _p(arr), C.byref(s), threads,
+           seconds, max_steps, C.byref(props), C.byref(wall))
+    if rc:
+        L.sr_last_error.restype = C.c_char_p
+        raise RuntimeError(L.sr_last_error().decode())
+    return props.value, wall.value
+
+
+def philox(c, k):
+    L = C.CDLL(ORACLE_SO)
+    o = (C.c_uint32 * 4)()
+    L.so_philox(*[C.c_uint32(v) for v in (*c, *k)], o)
+    return list(o)
+
+
+def philox_normal(seed, sweep, region, step, i):
+    L = C.CDLL(ORACLE_SO)
+    L.so_philox_normal.restype = C.c_float
+    L.so_philox_normal.argtypes = [u64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32]
+    return L.so_philox_normal(seed, sweep, region, step, i)
+
+
+def stations_line(S: int, x_max: float) -> np.ndarray:
+    """SURVEY §8(d) mapping: S stations evenly spaced, s_j = x_max j / (S - 1)."""
+    return x_max * np.arange(S, dtype=np.float64) / (S - 1)

@@ -1179,3 +1179,17 @@ void so_run_free(so_run* r) {
   evl_free(&q->final);
   free(q);
 }
+
+/* ------------------------------------------------ philox stream spec v1 probes */
+void so_philox(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0, uint32_t k1,
+               uint32_t* out) {
+  const seis_u32x4 r = seis_philox4x32_10(c0, c1, c2, c3, k0, k1);
+  for (int i = 0; i < 4; ++i) out[i] = r.w[i];
+}
+
+float so_philox_normal(uint64_t seed, uint32_t sweep, uint32_t region, uint32_t step,
+                       uint32_t i) {
+  return seis_normal(seed, sweep, region, step, i);
+}
+
+float so_bm(uint32_t w0, uint32_t w1) { return seis_bm(w0, w1); }

@@ -116,6 +116,12 @@ void so_run_rows(const so_run* r, int64_t* step, double* log_joint, int64_t* eve
 void so_run_final(const so_run* r, uint64_t* ids, double* x, double* t, double* arr);
 void so_run_free(so_run* r);
 
+/* ---- philox stream spec v1 (include/seis_philox.h) probes ---- */
+void so_philox(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0, uint32_t k1,
+               uint32_t* out);
+float so_philox_normal(uint64_t seed, uint32_t sweep, uint32_t region, uint32_t step, uint32_t i);
+float so_bm(uint32_t w0, uint32_t w1);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,1958 @@
+// engine.cu — B200 chromatic region-sweep engine: kernels + C-ABI host.
+//
+// Replaces the reference's run_chromatic hot path (arXiv 1612.00595 reference,
+// proj/include/seismic/samplers.hpp:401-498, proposals.hpp:84-293,
+// density.hpp:214-305, partition.hpp:40-90) with one CTA per same-color
+// region on sm_100a. See DESIGN.md for the layout and the roofline.
+//
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a --fmad=false ... (the
+// reference's integer outputs come from fp64 expressions evaluated without
+// contraction; FMA is used only where written explicitly).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "engine.cuh"
+#include "kernels.cuh"
+
+namespace seis {
+
+// ----------------------------------------------------------------- device xoshiro
+// derive_stream / Rng::uniform (reference rng.hpp:21-51, 110-121) for the
+// partition offset stream; integer-exact on device.
+__device__ __host__ inline uint64_t d_splitmix(uint64_t& s) {
+  uint64_t z = (s += 0x9e3779b97f4a7c15ULL);
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+__device__ __host__ inline uint64_t d_rotl(uint64_t x, int k) { return (x << k) | (x >> (64 - k)); }
+__device__ __host__ inline double d_offset_uniform(uint64_t seed, uint64_t purpose, uint64_t i0,
+                                                   double lo, double hi) {
+  uint64_t key = seed;
+  uint64_t k = d_splitmix(key);
+  const uint64_t words[4] = {purpose, i0, 0, 0};
+  for (int i = 0; i < 4; ++i) {
+    uint64_t w = words[i];
+    k ^= d_splitmix(w);
+    k = d_splitmix(k);
+  }
+  uint64_t s[4];
+  for (int i = 0; i < 4; ++i) s[i] = d_splitmix(k);
+  if ((s[0] | s[1] | s[2] | s[3]) == 0) s[0] = 1;
+  const uint64_t result = d_rotl(s[0] + s[3], 23) + s[0];
+  const double u = (double)(result >> 11) * 0x1.0p-53;
+  return lo + (hi - lo) * u;
+}
+
+// ----------------------------------------------------------------- partition
+// build_partition + color_partition (partition.hpp:40-90), one thread per
+// epoch: boundaries by the reference's repeated fp64 addition, colors i % k,
+// separation invariant checked against the nearest same-colored region
+// (equivalent to the reference's all-pairs check since boundaries increase).
+__global__ void k_partition(double T, double l, double tau, int ncol, int mode, uint64_t seed,
+                            int epoch0, int n_ep, double u_explicit, int bcap, double* bnd,
+                            int* nreg, int* err, int* colors) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n_ep) return;
+  const int epoch = epoch0 + e;
+  // mode 0 static (u = 0), 1 dynamic (u redrawn after every epoch,
+  // samplers.hpp:488-493), 2 explicit offset
+  double u = 0.0;
+  if (mode == 1 && epoch > 0) u = d_offset_uniform(seed, 6, (uint64_t)epoch, 0.0, l);
+  if (mode == 2) u = u_explicit;
+  double* b = bnd + (size_t)e * bcap;
+  int nb = 0;
+  b[nb++] = 0.0;
+  double x = u > 0 ? u : l;
+  while (x < T - 1e-9) {
+    if (nb >= bcap - 1) {
+      atomicExch(err, 2);
+      return;
+    }
+    b[nb++] = x;
+    x += l;
+  }
+  b[nb++] = T;
+  const int n = nb - 1;
+  nreg[e] = n;
+  if (colors)
+    for (int i = 0; i < n; ++i) colors[(size_t)e * bcap + i] = i % ncol;  // partition.hpp:81-82
+  for (int i = 0; i + ncol < n; ++i)
+    if (b[i + ncol] - b[i + 1] < tau - 1e-9) atomicExch(err, 1);
+}
+
+__global__ void k_offsets(uint64_t seed, int64_t epoch, double l, double* out) {
+  *out = d_offset_uniform(seed, 6, (uint64_t)epoch, 0.0, l);
+}
+
+// Partition::region_of (partition.hpp:33-37): first i < n-1 with t < b[i+1],
+// else n-1; a binary search over the same boundary array.
+__device__ __forceinline__ int region_of(const double* b, int n, double t) {
+  int lo = 0, hi = n - 1;  // answer in [lo, hi]
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (t < b[mid + 1])
+      hi = mid;
+    else
+      lo = mid + 1;
+  }
+  return lo;
+}
+
+__global__ void k_region_of(const double* b, int n, int64_t m, const double* t, int64_t* out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < m) out[i] = region_of(b, n, t[i]);
+}
+
+// ----------------------------------------------------------------- signals
+template <typename YT>
+__global__ void k_transpose(const YT* __restrict__ src, YT* __restrict__ dst, int S, int S_pad,
+                            int n) {
+  __shared__ YT tile[32][33];
+  const int s0 = blockIdx.x * 32, j0 = blockIdx.y * 32;
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int j = j0 + k, s = s0 + threadIdx.x;
+    tile[k][threadIdx.x] = (j < S && s < n) ? src[(size_t)j * n + s] : YT(0);
+  }
+  __syncthreads();
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int s = s0 + k, j = j0 + threadIdx.x;
+    if (s < n && j < S_pad) dst[(size_t)s * S_pad + j] = tile[threadIdx.x][k];
+  }
+}
+
+// coverage of every event of the table (variance_profile, density.hpp:112-129)
+__global__ void k_build_cov(Dev d, Table tab, const Ctl* ctl) {
+  const int e = blockIdx.y;
+  if (e >= ctl->n_events) return;
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= d.P2) return;
+  const double2 a = reinterpret_cast<const double2*>(d.pool)[(size_t)tab.slot[e] * d.P2 + p];
+  const Win w0 = 2 * p < d.S ? make_win(d, a.x) : empty_win();
+  const Win w1 = 2 * p + 1 < d.S ? make_win(d, a.y) : empty_win();
+  const int lo = min(w0.lo < w0.hi ? w0.lo : INT_MAX, w1.lo < w1.hi ? w1.lo : INT_MAX);
+  const int hi = max(w0.hi > w0.lo ? w0.hi : INT_MIN, w1.hi > w1.lo ? w1.hi : INT_MIN);
+  for (int r = lo; r < hi; ++r) {
+    const unsigned inc = (unsigned)inw(r, w0) + ((unsigned)inw(r, w1) << 16);
+    if (inc) atomicAdd(d.cov + (size_t)r * d.P2 + p, inc);
+  }
+}
+
+// ----------------------------------------------------------------- station pass
+enum { SRC_NONE = 0, SRC_BIRTH = 1, SRC_SHIFT = 2, SRC_ROWS = 3 };
+
+struct PassIn {
+  int src;
+  const double* rows[2];
+  uint64_t seed;
+  uint32_t sweep, region, step;
+  int wlo, whi;
+};
+
+// Scores one proposal over all stations (density.hpp:239-301): arrival
+// densities of added/removed events and the per-sample terms where the
+// coverage changes. Called by all NT threads; results are per-thread partials.
+template <typename YT>
+__device__ void station_pass(const Dev& d, const Prop& P, const PassIn& in, int nd,
+                             const int* dslot, const int* dsign, const double* Ls,
+                             const double* Is, double (&acc)[5], int& cnt) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double2* pool2 = reinterpret_cast<const double2*>(d.pool);
+  const double2* st2 = reinterpret_cast<const double2*>(d.stations);
+  for (int base = warp * 32; base < d.P2; base += NT) {
+    const int p = base + lane;
+    const bool pv = p < d.P2;
+    const bool v0 = pv && 2 * p < d.S, v1 = pv && 2 * p + 1 < d.S;
+    Win A[2][2], R[2][2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) A[q][0] = A[q][1] = R[q][0] = R[q][1] = empty_win();
+    double s0 = 0.0, s1 = 0.0;
+    if (pv) {
+      const double2 s = st2[p];
+      s0 = s.x;
+      s1 = s.y;
+    }
+    double ra[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      if (q < P.nr && pv) {
+        const double2 v = pool2[(size_t)P.rslot[q] * d.P2 + p];
+        ra[q][0] = v.x;
+        ra[q][1] = v.y;
+        if (v0) {
+          R[q][0] = clampw(make_win(d, v.x), in.wlo, in.whi);
+          acc[3 + q] += arr_logpdf(d, v.x, arrival_mean(d, P.rx[q], P.rt[q], s0));
+        }
+        if (v1) {
+          R[q][1] = clampw(make_win(d, v.y), in.wlo, in.whi);
+          acc[3 + q] += arr_logpdf(d, v.y, arrival_mean(d, P.rx[q], P.rt[q], s1));
+        }
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+      if (a < P.na && pv) {
+        double a0 = 0.0, a1 = 0.0;
+        const double m0 = arrival_mean(d, P.ax[a], P.at[a], s0);
+        const double m1 = arrival_mean(d, P.ax[a], P.at[a], s1);
+        if (in.src == SRC_BIRTH) {
+          float z0, z1;
+          seis_normal_pair(in.seed, in.sweep, in.region, in.step, (uint32_t)p, &z0, &z1);
+          a0 = m0 + d.sigma * (double)z0;
+          a1 = m1 + d.sigma * (double)z1;
+        } else if (in.src == SRC_SHIFT) {
+          a0 = ra[a][0] + (m0 - arrival_mean(d, P.rx[a], P.rt[a], s0));
+          a1 = ra[a][1] + (m1 - arrival_mean(d, P.rx[a], P.rt[a], s1));
+        } else {
+          if (v0) a0 = in.rows[a][2 * p];
+          if (v1) a1 = in.rows[a][2 * p + 1];
+        }
+        if (v0) {
+          A[a][0] = clampw(make_win(d, a0), in.wlo, in.whi);
+          acc[1 + a] += arr_logpdf(d, a0, m0);
+        }
+        if (v1) {
+          A[a][1] = clampw(make_win(d, a1), in.wlo, in.whi);
+          acc[1 + a] += arr_logpdf(d, a1, m1);
+        }
+      }
+    }
+    // windows that do not move leave every count unchanged
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      bool same = false;
+      if (P.nr == 1 && P.na == 1) same = weq(A[0][s], R[0][s]);
+      if (P.nr == 2 && P.na == 2)
+        same = (weq(A[0][s], R[0][s]) && weq(A[1][s], R[1][s])) ||
+               (weq(A[0][s], R[1][s]) && weq(A[1][s], R[0][s]));
+      if (same) A[0][s] = A[1][s] = R[0][s] = R[1][s] = empty_win();
+    }
+    int lo = INT_MAX, hi = INT_MIN;
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        if (A[q][s].hi > A[q][s].lo) {
+          lo = min(lo, A[q][s].lo);
+          hi = max(hi, A[q][s].hi);
+        }
+        if (R[q][s].hi > R[q][s].lo) {
+          lo = min(lo, R[q][s].lo);
+          hi = max(hi, R[q][s].hi);
+        }
+      }
+    const int blo = __reduce_min_sync(0xffffffffu, lo);
+    const int bhi = __reduce_max_sync(0xffffffffu, hi);
+    if (blo >= bhi) continue;
+    if (nd == 0)
+      band_with_diff<0, YT>(d, p, v0, v1, blo, bhi, A, R, nd, dslot, dsign, Ls, Is, acc[0], cnt);
+    else if (nd <= 2)
+      band_with_diff<2, YT>(d, p, v0, v1, blo, bhi, A, R, nd, dslot, dsign, Ls, Is, acc[0], cnt);
+    else if (nd <= 4)
+      band_with_diff<4, YT>(d, p, v0, v1, blo, bhi, A, R, nd, dslot, dsign, Ls, Is, acc[0], cnt);
+    else if (nd <= 8)
+      band_with_diff<8, YT>(d, p, v0, v1, blo, bhi, A, R, nd, dslot, dsign, Ls, Is, acc[0], cnt);
+    else
+      band_rows_generic<YT>(d, p, blo, bhi, A, R, nd, dslot, dsign, Ls, Is, acc[0], cnt);
+  }
+}
+
+// Arrival move (proposals.hpp:161-174) in production: only station st moves.
+// Warp 0 scores it; lanes take rows.
+template <typename YT>
+__device__ void arrival_pass(const Dev& d, const Prop& P, int nd, const int* dslot,
+                             const int* dsign, const double* Ls, const double* Is,
+                             double (&acc)[5], int& cnt) {
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x >= 32) return;
+  const int st = P.arr_st;
+  const double old_a = d.pool[(size_t)P.rslot[0] * d.S_pad + st];
+  const double new_a = old_a + P.arr_da;
+  const double mean = arrival_mean(d, P.rx[0], P.rt[0], d.stations[st]);
+  if (lane == 0) {
+    acc[1] += arr_logpdf(d, new_a, mean);
+    acc[3] += arr_logpdf(d, old_a, mean);
+  }
+  const Win wo = make_win(d, old_a), wn = make_win(d, new_a);
+  if (weq(wo, wn)) return;
+  const int blo = min(wo.hi > wo.lo ? wo.lo : INT_MAX, wn.hi > wn.lo ? wn.lo : INT_MAX);
+  const int bhi = max(wo.hi > wo.lo ? wo.hi : INT_MIN, wn.hi > wn.lo ? wn.hi : INT_MIN);
+  const YT* y = reinterpret_cast<const YT*>(d.y);
+  const uint16_t* c16 = reinterpret_cast<const uint16_t*>(d.cov);
+  for (int r = blo + lane; r < bhi; r += 32) {
+    const int dc = inw(r, wn) - inw(r, wo);
+    if (!dc) continue;
+    int co = (int)c16[(size_t)r * d.S_pad + st];
+    for (int q = 0; q < nd; ++q) {
+      const Win w = make_win(d, d.pool[(size_t)dslot[q] * d.S_pad + st]);
+      co += dsign[q] * inw(r, w);
+    }
+    acc[0] += sample_term(d, Ls, Is, (double)y[(size_t)r * d.S_pad + st], co, co + dc);
+    ++cnt;
+  }
+}
+
+// ----------------------------------------------------------------- phase kernel
+template <int MODE>
+__device__ void gen_proposal(const Dev& d, const Samp& sp, const PhaseArgs& pa, Prop& P,
+                             const OwnEv* own, int nown, int region, double rlo, double rhi,
+                             bool rclosed, int step, long long tape_idx, unsigned long long id_next,
+                             int* err) {
+  P.skip = 0;
+  P.scored = 0;
+  P.nr = P.na = 0;
+  P.accept = 0;
+  P.u_drawn = 1;
+  P.tape_acc = 0;
+  P.logq_f = P.logq_r = 0.0;
+  P.tape_idx = tape_idx;
+  bool null_ = false;
+  const int k = nown;
+  if (MODE == 0) {
+    // philox stream spec v1 (include/seis_philox.h); control flow of
+    // MoveDistribution::sample + propose_move (proposals.hpp:33-41,236-253)
+    const seis_u32x4 d0 = seis_draw(sp.seed, (uint32_t)pa.epoch, (uint32_t)region, (uint32_t)step,
+                                    SEIS_DRAW_MOVE);
+    const double um = seis_u53(d0.w[0], d0.w[1]);
+    int type = 4;
+    for (int q = 0; q < 5; ++q)
+      if (um < sp.cumw[q]) {
+        type = q;
+        break;
+      }
+    P.type = type;
+    P.u = seis_u53(d0.w[2], d0.w[3]);
+    const seis_u32x4 d1 = seis_draw(sp.seed, (uint32_t)pa.epoch, (uint32_t)region,
+                                    (uint32_t)step, SEIS_DRAW_SCALAR);
+    switch (type) {
+      case 0: {  // birth, proposals.hpp:84-107
+        P.na = 1;
+        P.at[0] = rlo + (rhi - rlo) * seis_u53(d1.w[0], d1.w[1]);
+        P.ax[0] = 0.0 + (d.x_max - 0.0) * seis_u53(d1.w[2], d1.w[3]);
+        P.aid = id_next;
+        break;
+      }
+      case 1: {  // death, proposals.hpp:111-138
+        if (k == 0) {
+          null_ = true;
+          break;
+        }
+        const int pick = (int)seis_lemire(seis_u64(d1.w[0], d1.w[1]), (uint64_t)k);
+        P.nr = 1;
+        P.rown[0] = pick;
+        break;
+      }
+      case 2: {  // location, proposals.hpp:143-159
+        if (k == 0) {
+          null_ = true;
+          break;
+        }
+        const int pick = (int)seis_lemire(seis_u64(d1.w[0], d1.w[1]), (uint64_t)k);
+        float z0, z1;
+        seis_normal_pair(sp.seed, (uint32_t)pa.epoch, (uint32_t)region, (uint32_t)step, 0, &z0,
+                         &z1);
+        P.nr = P.na = 1;
+        P.rown[0] = pick;
+        P.ax[0] = own[pick].x + (0.0 + sp.step_lx * (double)z0);
+        P.at[0] = own[pick].t + (0.0 + sp.step_lt * (double)z1);
+        break;
+      }
+      case 3: {  // arrival, proposals.hpp:161-174
+        if (k == 0) {
+          null_ = true;
+          break;
+        }
+        const int pick = (int)seis_lemire(seis_u64(d1.w[0], d1.w[1]), (uint64_t)k);
+        P.arr_st = (int)seis_lemire(seis_u64(d1.w[2], d1.w[3]), (uint64_t)d.S);
+        const float z0 = seis_normal(sp.seed, (uint32_t)pa.epoch, (uint32_t)region,
+                                     (uint32_t)step, 0);
+        P.arr_da = 0.0 + sp.step_arr * (double)z0;
+        P.nr = P.na = 1;
+        P.rown[0] = pick;
+        P.ax[0] = own[pick].x;
+        P.at[0] = own[pick].t;
+        break;
+      }
+      default: {  // joint pair, proposals.hpp:182-234
+        if (k < 2) {
+          null_ = true;
+          break;
+        }
+        const int i1 = (int)seis_lemire(seis_u64(d1.w[0], d1.w[1]), (uint64_t)k);
+        int i2 = (int)seis_lemire(seis_u64(d1.w[2], d1.w[3]), (uint64_t)(k - 1));
+        if (i2 >= i1) ++i2;
+        const seis_u32x4 d2 = seis_draw(sp.seed, (uint32_t)pa.epoch, (uint32_t)region,
+                                        (uint32_t)step, SEIS_DRAW_PAIR);
+        const int pair = (int)seis_lemire(seis_u64(d2.w[0], d2.w[1]), (uint64_t)(d.S - 1));
+        const double xl = d.stations[pair], xr = d.stations[pair + 1], v = d.v;
+        const double x1 = own[i1].x, t1 = own[i1].t, x2 = own[i2].x, t2 = own[i2].t;
+        const double al1 = t1 + fabs(x1 - xl) / v;
+        const double ar1 = t1 + fabs(x1 - xr) / v;
+        const double al2 = t2 + fabs(x2 - xl) / v;
+        const double ar2 = t2 + fabs(x2 - xr) / v;
+        double n1x = 0.5 * (xl + xr) + 0.5 * v * (al1 - ar2);
+        double n1t = 0.5 * (al1 + ar2) - (xr - xl) / (2.0 * v);
+        double n2x = 0.5 * (xl + xr) + 0.5 * v * (al2 - ar1);
+        double n2t = 0.5 * (al2 + ar1) - (xr - xl) / (2.0 * v);
+        float z0, z1, z2, z3;
+        seis_normal_pair(sp.seed, (uint32_t)pa.epoch, (uint32_t)region, (uint32_t)step, 0, &z0,
+                         &z1);
+        seis_normal_pair(sp.seed, (uint32_t)pa.epoch, (uint32_t)region, (uint32_t)step, 1, &z2,
+                         &z3);
+        n1x += 0.0 + sp.step_joint * (double)z0;
+        n1t += 0.0 + sp.joint_t_sd * (double)z1;
+        n2x += 0.0 + sp.step_joint * (double)z2;
+        n2t += 0.0 + sp.joint_t_sd * (double)z3;
+        P.nr = P.na = 2;
+        P.rown[0] = i1;
+        P.rown[1] = i2;
+        P.ax[0] = n1x;
+        P.at[0] = n1t;
+        P.ax[1] = n2x;
+        P.at[1] = n2t;
+        break;
+      }
+    }
+  } else {
+    // replay: the proposal comes from the host tape (reference draws)
+    const seis_tape_step& ts = pa.tape[tape_idx];
+    P.type = (int)ts.type;
+    null_ = ts.is_null != 0;
+    P.u = ts.u;
+    P.u_drawn = (int)ts.u_drawn;
+    P.tape_acc = (int)ts.accepted;
+    P.logq_f = ts.logq_f;
+    P.logq_r = ts.logq_r;
+    P.tape_off = ts.added_arr_off;
+    if (!null_) {
+      P.nr = (int)ts.n_removed;
+      P.na = (int)ts.n_added;
+      for (int q = 0; q < P.nr; ++q) {
+        int f = -1;
+        for (int i = 0; i < nown; ++i)
+          if (own[i].id == ts.removed_id[q]) {
+            f = i;
+            break;
+          }
+        if (f < 0) {
+          atomicExch(err, ERR_TAPE_UNKNOWN_ID);
+          null_ = true;
+          break;
+        }
+        P.rown[q] = f;
+      }
+      for (int a = 0; a < P.na; ++a) {
+        P.ax[a] = ts.added_x[a];
+        P.at[a] = ts.added_t[a];
+      }
+      P.aid = P.type == 0 ? ts.added_id[0] : 0;
+    }
+  }
+  if (null_) {
+    P.skip = 1;
+    P.nr = P.na = 0;
+    P.u_drawn = 0;
+    return;
+  }
+  for (int q = 0; q < P.nr; ++q) {
+    const OwnEv& e = own[P.rown[q]];
+    P.rslot[q] = e.slot;
+    P.rsidx[q] = e.sidx;
+    P.rx[q] = e.x;
+    P.rt[q] = e.t;
+  }
+  // mh_step constraint (proposals.hpp:269-282), then delta_log_joint's
+  // support check (density.hpp:218-221)
+  for (int a = 0; a < P.na; ++a) {
+    const double t = P.at[a];
+    if (!(t >= rlo && (t < rhi || (rclosed && t == rhi)))) P.skip = 1;
+  }
+  if (P.skip) return;
+  P.scored = 1;
+  for (int a = 0; a < P.na; ++a) {
+    const double t = P.at[a], x = P.ax[a];
+    if (x < 0.0 || x > d.x_max || !(t >= 0.0 && t <= d.T)) P.skip = 1;
+  }
+}
+
+template <typename YT, int MODE>
+__global__ void __launch_bounds__(NT, 1)
+    k_phase(const Dev d, const Samp sp, const PhaseArgs pa, Ctl* ctl, int stamp) {
+  __shared__ double Ls[TBL], Is[TBL];
+  __shared__ OwnEv own[MAXOWN];
+  __shared__ StartEv st[MAXOWN];
+  __shared__ int dslot[MAXDIFF], dsign[MAXDIFF];
+  __shared__ int lfree[MAXOWN];
+  __shared__ Prop prop[2];
+  __shared__ double red[NW][5];
+  __shared__ int redc[NW];
+  __shared__ int s_w[NW];
+  __shared__ int s_nown, s_nd, s_abort, s_tmp;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int slot_idx = blockIdx.x;
+  const int region = pa.color + slot_idx * sp.ncol;
+  if (region >= pa.nreg) return;
+  const double rlo = pa.bnd[region], rhi = pa.bnd[region + 1];
+  const bool rclosed = region + 1 == pa.nreg;
+  const int N = ctl->n_events;
+
+  for (int i = tid; i < TBL; i += NT) {
+    Ls[i] = i < d.tab_n ? d.Lg[i] : 0.0;
+    Is[i] = i < d.tab_n ? d.Ig[i] : 0.0;
+  }
+  if (tid == 0) {
+    s_nown = 0;
+    s_abort = 0;
+  }
+  __syncthreads();
+  // own events: table entries (id order) inside the region
+  // (events_in_region, proposals.hpp:65-71, on the local copy of samplers.hpp:448)
+  for (int base = 0; base < N; base += NT) {
+    const int i = base + tid;
+    bool inr = false;
+    if (i < N) {
+      const double t = pa.tab.t[i];
+      inr = t >= rlo && (t < rhi || (rclosed && t == rhi));
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, inr);
+    if (lane == 0) s_w[warp] = __popc(bal);
+    __syncthreads();
+    if (tid == 0) {
+      int acc = s_nown;
+      for (int w = 0; w < NW; ++w) {
+        const int c = s_w[w];
+        s_w[w] = acc;
+        acc += c;
+      }
+      s_tmp = acc;
+    }
+    __syncthreads();
+    if (inr) {
+      const int pos = s_w[warp] + __popc(bal & ((1u << lane) - 1u));
+      if (pos < MAXOWN) {
+        own[pos].id = pa.tab.id[i];
+        own[pos].x = pa.tab.x[i];
+        own[pos].t = pa.tab.t[i];
+        own[pos].slot = pa.tab.slot[i];
+        own[pos].sidx = pos;
+        st[pos].id = pa.tab.id[i];
+        st[pos].slot = pa.tab.slot[i];
+        st[pos].tab = i;
+        st[pos].current = 1;
+      }
+    }
+    __syncthreads();
+    if (tid == 0) s_nown = s_tmp;
+    __syncthreads();
+  }
+  if (s_nown > MAXOWN) {
+    if (tid == 0) atomicExch(&ctl->err, ERR_OWN_OVERFLOW);
+    return;
+  }
+  const int nstart = s_nown;
+  // thread-0 chain state
+  int nown = nstart, nd = 0, nlfree = 0;
+  long long n_local = N;
+  unsigned long long births = 0, n_acc = 0, n_scored = 0, n_arr = 0;
+  const unsigned long long id_base = pa.next_base + (unsigned long long)slot_idx * sp.k;
+  if (tid == 0) s_nd = 0;
+  unsigned long long n_changed = 0;
+  int cnt_total = 0;
+
+  for (int step = 0; step < (int)sp.k; ++step) {
+    Prop& P = prop[step & 1];
+    const long long tape_idx = pa.tape_base + (long long)slot_idx * sp.k + step;
+    if (tid == 0) {
+      gen_proposal<MODE>(d, sp, pa, P, own, nown, region, rlo, rhi, rclosed, step, tape_idx,
+                         id_base + births, &ctl->err);
+      if (P.scored) ++n_scored;
+      if (P.skip) {
+        // null (no draw), constrained out, or out of support: log_r = -inf
+        // -> reject (proposals.hpp:268-291)
+        if (MODE == 1) {
+          seis_step_out o;
+          o.delta = -INFINITY;
+          o.log_r = -INFINITY;
+          o.scored = P.scored;
+          o.accepted = 0;
+          pa.out[tape_idx] = o;
+        }
+      }
+    }
+    __syncthreads();
+    if (P.skip) continue;
+    double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    int cnt = 0;
+    if (MODE == 0 && P.type == 3) {
+      arrival_pass<YT>(d, P, s_nd, dslot, dsign, Ls, Is, acc, cnt);
+    } else {
+      PassIn in;
+      in.src = P.na == 0 ? SRC_NONE
+                         : (MODE == 1 ? SRC_ROWS : (P.type == 0 ? SRC_BIRTH : SRC_SHIFT));
+      in.rows[0] = pa.tape_arr + (MODE == 1 ? P.tape_off : 0);
+      in.rows[1] = in.rows[0] + d.S;
+      in.seed = sp.seed;
+      in.sweep = (uint32_t)pa.epoch;
+      in.region = (uint32_t)region;
+      in.step = (uint32_t)step;
+      in.wlo = 0;
+      in.whi = d.n;
+      station_pass<YT>(d, P, in, s_nd, dslot, dsign, Ls, Is, acc, cnt);
+    }
+#pragma unroll
+    for (int q = 0; q < 5; ++q) acc[q] = warp_sum(acc[q]);
+    cnt = __reduce_add_sync(0xffffffffu, (unsigned)cnt);
+    if (lane == 0) {
+#pragma unroll
+      for (int q = 0; q < 5; ++q) red[warp][q] = acc[q];
+      redc[warp] = cnt;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double sig = 0.0, A[5];
+      for (int q = 1; q < 5; ++q) A[q] = 0.0;
+      int c = 0;
+      for (int w = 0; w < NW; ++w) {
+        sig += red[w][0];
+        for (int q = 1; q < 5; ++q) A[q] += red[w][q];
+        c += redc[w];
+      }
+      n_changed += (unsigned long long)c;
+      n_arr += (P.type == 3) ? 2ull : (unsigned long long)d.S * (P.nr + P.na);
+      // delta_log_joint (density.hpp:223-240): prior terms with n0 = local
+      // event count and area T, arrival densities, likelihood
+      const long long n0 = n_local, n1 = n0 - P.nr + P.na;
+      double delta = 0.0;
+      if (n1 > n0) {
+        for (long long i = n0 + 1; i <= n1; ++i) delta += d.log_lambda_T - d.logi[i];
+      } else if (n1 < n0) {
+        for (long long i = n1 + 1; i <= n0; ++i) delta -= d.log_lambda_T - d.logi[i];
+      }
+      delta += (double)(n1 - n0) * d.lxa;
+      if (P.na >= 1) delta += A[1];
+      if (P.na >= 2) delta += A[2];
+      if (P.nr >= 1) delta -= A[3];
+      if (P.nr >= 2) delta -= A[4];
+      delta += sig;
+      // proposal log densities (proposals.hpp:100-104,120-126)
+      if (MODE == 0) {
+        if (P.type == 0) {
+          P.logq_f = sp.logw[0] - log(rhi - rlo) - d.log_xmax + A[1];
+          P.logq_r = sp.logw[1] - d.logi[nown + 1];
+        } else if (P.type == 1) {
+          P.logq_f = sp.logw[1] - d.logi[nown];
+          P.logq_r = sp.logw[0] - log(rhi - rlo) - d.log_xmax + A[3];
+        }
+      }
+      const double log_r = delta + P.logq_r - P.logq_f;  // log_accept_ratio
+      // mh_step decision (proposals.hpp:283-291)
+      bool acc_gpu = log_r >= 0.0;
+      if (!acc_gpu) acc_gpu = log(P.u) < log_r;
+      bool apply = acc_gpu;
+      if (MODE == 1) {
+        seis_step_out o;
+        o.delta = delta;
+        o.log_r = log_r;
+        o.scored = 1;
+        o.accepted = acc_gpu ? 1 : 0;
+        pa.out[tape_idx] = o;
+        apply = P.tape_acc != 0;  // keep the state on the tape's trajectory
+      }
+      P.accept = 0;
+      if (apply) {
+        // allocate destination slots; modify this-phase versions in place
+        bool ok = true;
+        for (int a = 0; a < P.na; ++a) {
+          if (a < P.nr && P.rsidx[a] < 0) {
+            P.dslot[a] = P.rslot[a];
+            P.inplace[a] = 1;
+          } else {
+            P.inplace[a] = 0;
+            if (nlfree > 0) {
+              P.dslot[a] = lfree[--nlfree];
+            } else {
+              const int top = atomicSub(&ctl->free_top, 1) - 1;
+              if (top < 0) {
+                atomicExch(&ctl->err, ERR_POOL_EXHAUSTED);
+                ok = false;
+                break;
+              }
+              P.dslot[a] = pa.free_stack[top];
+            }
+          }
+        }
+        if (ok && P.na >= 1 && nown - P.nr + P.na > MAXOWN) {
+          atomicExch(&ctl->err, ERR_OWN_OVERFLOW);
+          ok = false;
+        }
+        if (!ok) {
+          s_abort = 1;
+        } else {
+          P.accept = 1;
+          ++n_acc;
+          if (P.type == 0) ++births;
+          // retire removed versions; deaths of this-phase versions free slots
+          for (int q = 0; q < P.nr; ++q) {
+            const int sidx = P.rsidx[q];
+            if (sidx >= 0)
+              st[sidx].current = 0;
+            else if (q >= P.na)
+              lfree[nlfree++] = P.rslot[q];
+          }
+          // apply_change (density.hpp:171-180): erase by id, push_back added
+          unsigned long long rid[2];
+          for (int q = 0; q < P.nr; ++q) rid[q] = own[P.rown[q]].id;
+          for (int q = 0; q < P.nr; ++q) {
+            int i = 0;
+            while (i < nown && own[i].id != rid[q]) ++i;
+            for (int j = i; j + 1 < nown; ++j) own[j] = own[j + 1];
+            --nown;
+          }
+          for (int a = 0; a < P.na; ++a) {
+            OwnEv e;
+            e.id = P.type == 0 ? P.aid : rid[a];
+            e.x = P.ax[a];
+            e.t = P.at[a];
+            e.slot = P.dslot[a];
+            e.sidx = -1;
+            own[nown++] = e;
+          }
+          n_local += P.na - P.nr;
+          // own diff vs the phase-start snapshot (frozen-snapshot view)
+          nd = 0;
+          for (int i = 0; i < nstart; ++i)
+            if (!st[i].current) {
+              dslot[nd] = st[i].slot;
+              dsign[nd++] = -1;
+            }
+          for (int i = 0; i < nown; ++i)
+            if (own[i].sidx < 0) {
+              dslot[nd] = own[i].slot;
+              dsign[nd++] = 1;
+            }
+          s_nd = nd;
+          if (MODE == 1 && P.type == 0 && P.aid != id_base + births - 1)
+            atomicAdd(&ctl->id_mismatch, 1ull);
+        }
+      }
+    }
+    __syncthreads();
+    if (s_abort) return;
+    if (P.accept) {
+      // write the accepted versions' arrivals (recomputed exactly as scored)
+      double2* pool2 = reinterpret_cast<double2*>(d.pool);
+      const double2* st2 = reinterpret_cast<const double2*>(d.stations);
+      if (MODE == 0 && P.type == 3) {
+        if (P.inplace[0]) {
+          if (tid == 0) {
+            double& a = d.pool[(size_t)P.dslot[0] * d.S_pad + P.arr_st];
+            a = a + P.arr_da;
+          }
+        } else {
+          for (int p = tid; p < d.P2; p += NT) {
+            double2 v = pool2[(size_t)P.rslot[0] * d.P2 + p];
+            if (2 * p == P.arr_st) v.x = v.x + P.arr_da;
+            if (2 * p + 1 == P.arr_st) v.y = v.y + P.arr_da;
+            pool2[(size_t)P.dslot[0] * d.P2 + p] = v;
+          }
+        }
+      } else {
+        for (int a = 0; a < P.na; ++a) {
+          for (int p = tid; p < d.P2; p += NT) {
+            const double2 s = st2[p];
+            const double m0 = arrival_mean(d, P.ax[a], P.at[a], s.x);
+            const double m1 = arrival_mean(d, P.ax[a], P.at[a], s.y);
+            double2 v;
+            if (MODE == 1) {
+              const double* row = pa.tape_arr + P.tape_off + (size_t)a * d.S;
+              v.x = 2 * p < d.S ? row[2 * p] : 0.0;
+              v.y = 2 * p + 1 < d.S ? row[2 * p + 1] : 0.0;
+            } else if (P.type == 0) {
+              float z0, z1;
+              seis_normal_pair(sp.seed, (uint32_t)pa.epoch, (uint32_t)region, (uint32_t)step,
+                               (uint32_t)p, &z0, &z1);
+              v.x = m0 + d.sigma * (double)z0;
+              v.y = m1 + d.sigma * (double)z1;
+            } else {
+              const double2 o = pool2[(size_t)P.rslot[a] * d.P2 + p];
+              v.x = o.x + (m0 - arrival_mean(d, P.rx[a], P.rt[a], s.x));
+              v.y = o.y + (m1 - arrival_mean(d, P.rx[a], P.rt[a], s.y));
+            }
+            pool2[(size_t)P.dslot[a] * d.P2 + p] = v;
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  // ---- phase outputs (the barrier merge, samplers.hpp:459-462,471-482)
+  const int nown_f = s_nown;  // unused; thread 0 state below
+  (void)nown_f;
+  (void)cnt_total;
+  if (tid == 0) {
+    // fates of the phase-start versions
+    for (int i = 0; i < nstart; ++i) {
+      const int tab = st[i].tab;
+      pa.fate_stamp[tab] = stamp;
+      int f = -1;
+      for (int j = 0; j < nown; ++j)
+        if (own[j].id == st[i].id) {
+          f = j;
+          break;
+        }
+      pa.fate_alive[tab] = f >= 0;
+      if (f >= 0) {
+        pa.fate_x[tab] = own[f].x;
+        pa.fate_t[tab] = own[f].t;
+        pa.fate_slot[tab] = own[f].slot;
+      }
+    }
+    // births alive at phase end, sorted by id
+    OutEv* bo = pa.births + (size_t)slot_idx * MAXOWN;
+    int nb = 0;
+    for (int j = 0; j < nown; ++j)
+      if (own[j].id >= pa.next_base) {
+        OutEv e;
+        e.id = own[j].id;
+        e.x = own[j].x;
+        e.t = own[j].t;
+        e.slot = own[j].slot;
+        e.pad = 0;
+        int q = nb++;
+        while (q > 0 && bo[q - 1].id > e.id) {
+          bo[q] = bo[q - 1];
+          --q;
+        }
+        bo[q] = e;
+      }
+    pa.births_cnt[slot_idx] = nb;
+    // coverage diff for the commit; this-phase versions that died were
+    // already recycled locally, return them to the pool now
+    DiffEnt* dout = pa.diff + (size_t)slot_idx * MAXDIFF;
+    for (int q = 0; q < nd; ++q) {
+      dout[q].slot = dslot[q];
+      dout[q].sign = dsign[q];
+    }
+    pa.diff_cnt[slot_idx] = nd;
+    for (int q = 0; q < nlfree; ++q) {
+      const int top = atomicAdd(&ctl->free_top, 1);
+      pa.free_stack[top] = lfree[q];
+    }
+    atomicAdd(&ctl->scored, n_scored);
+    atomicAdd(&ctl->changed, n_changed);
+    atomicAdd(&ctl->arrvals, n_arr);
+    atomicAdd(&ctl->accepted, n_acc);
+  }
+}
+
+// ----------------------------------------------------------------- barrier
+// Coverage commit: C += sum over regions of (own_now - own_start) windows;
+// same-color footprints overlap, so packed 32-bit atomics.
+__global__ void k_commit(Dev d, int color, int ncol, int nreg, const int* diff_cnt,
+                         const DiffEnt* diff, int* free_stack, Ctl* ctl) {
+  const int slot_idx = blockIdx.x;
+  const int region = color + slot_idx * ncol;
+  if (region >= nreg) return;
+  const int nd = diff_cnt[slot_idx];
+  const DiffEnt* de = diff + (size_t)slot_idx * MAXDIFF;
+  const double2* pool2 = reinterpret_cast<const double2*>(d.pool);
+  for (int q = 0; q < nd; ++q) {
+    const int slot = de[q].slot, sign = de[q].sign;
+    for (int p = threadIdx.x; p < d.P2; p += blockDim.x) {
+      const double2 a = pool2[(size_t)slot * d.P2 + p];
+      const Win w0 = 2 * p < d.S ? make_win(d, a.x) : empty_win();
+      const Win w1 = 2 * p + 1 < d.S ? make_win(d, a.y) : empty_win();
+      const int lo = min(w0.hi > w0.lo ? w0.lo : INT_MAX, w1.hi > w1.lo ? w1.lo : INT_MAX);
+      const int hi = max(w0.hi > w0.lo ? w0.hi : INT_MIN, w1.hi > w1.lo ? w1.hi : INT_MIN);
+      for (int r = lo; r < hi; ++r) {
+        const int inc = sign * inw(r, w0) + sign * inw(r, w1) * 65536;
+        if (inc) atomicAdd(d.cov + (size_t)r * d.P2 + p, (unsigned)inc);
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int q = 0; q < nd; ++q)
+      if (de[q].sign < 0) {
+        const int top = atomicAdd(&ctl->free_top, 1);
+        free_stack[top] = de[q].slot;
+      }
+}
+
+// block-wide exclusive scan of one int per thread (1024 threads)
+__device__ int block_scan_excl(int v, int* total) {
+  __shared__ int ws[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) ws[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    const int nw = blockDim.x >> 5;
+    int s = lane < nw ? ws[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    ws[lane] = s;
+  }
+  __syncthreads();
+  const int excl = x - v + (warp ? ws[warp - 1] : 0);
+  *total = ws[(blockDim.x >> 5) - 1];
+  __syncthreads();
+  return excl;
+}
+
+// Event-table rebuild (merge + sort_by_id, samplers.hpp:471-482) without a
+// sort: survivors keep their id order, births (ids above every old id,
+// increasing with region slot) are appended region by region.
+__global__ void __launch_bounds__(1024) k_rebuild(Table in, Table out, int cap, int stamp,
+                                                  const int* fate_stamp, const int* fate_alive,
+                                                  const double* fate_x, const double* fate_t,
+                                                  const int* fate_slot, int n_slots,
+                                                  const int* births_cnt, const OutEv* births,
+                                                  Ctl* ctl) {
+  const int N = ctl->n_events;
+  int base = 0;
+  for (int c0 = 0; c0 < N; c0 += blockDim.x) {
+    const int i = c0 + threadIdx.x;
+    int alive = 0;
+    bool touched = false;
+    if (i < N) {
+      touched = fate_stamp[i] == stamp;
+      alive = touched ? fate_alive[i] : 1;
+    }
+    int tot;
+    const int pos = base + block_scan_excl(alive, &tot);
+    if (alive) {
+      if (pos < cap) {
+        out.id[pos] = in.id[i];
+        out.x[pos] = touched ? fate_x[i] : in.x[i];
+        out.t[pos] = touched ? fate_t[i] : in.t[i];
+        out.slot[pos] = touched ? fate_slot[i] : in.slot[i];
+      }
+    }
+    base += tot;
+  }
+  for (int c0 = 0; c0 < n_slots; c0 += blockDim.x) {
+    const int s = c0 + threadIdx.x;
+    const int nb = s < n_slots ? births_cnt[s] : 0;
+    int tot;
+    const int pos = base + block_scan_excl(nb, &tot);
+    for (int b = 0; b < nb; ++b) {
+      const OutEv& e = births[(size_t)s * MAXOWN + b];
+      if (pos + b < cap) {
+        out.id[pos + b] = e.id;
+        out.x[pos + b] = e.x;
+        out.t[pos + b] = e.t;
+        out.slot[pos + b] = e.slot;
+      }
+    }
+    base += tot;
+  }
+  if (threadIdx.x == 0) {
+    if (base > cap) atomicExch(&ctl->err, ERR_TABLE_OVERFLOW);
+    ctl->n_events = min(base, cap);
+  }
+}
+
+// ----------------------------------------------------------------- score batch
+struct ChangeDev {
+  int nr, na;
+  unsigned long long rid[2];
+  double ax[2], at[2];
+  long long arow[2];
+  int wlo, whi;
+  double slo, shi;
+  int sclosed;
+  double prior;  // host-computed prior part (reference order)
+};
+
+template <typename YT>
+__global__ void __launch_bounds__(NT, 1)
+    k_score_batch(const Dev d, Table tab, const Ctl* ctl, const ChangeDev* ch,
+                  const double* rows, double* out) {
+  __shared__ double Ls[TBL], Is[TBL];
+  __shared__ Prop P;
+  __shared__ double red[NW][5];
+  __shared__ int s_bad;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const ChangeDev c = ch[blockIdx.x];
+  for (int i = tid; i < TBL; i += NT) {
+    Ls[i] = i < d.tab_n ? d.Lg[i] : 0.0;
+    Is[i] = i < d.tab_n ? d.Ig[i] : 0.0;
+  }
+  if (tid == 0) {
+    s_bad = 0;
+    P.nr = c.nr;
+    P.na = c.na;
+    const int N = ctl->n_events;
+    for (int q = 0; q < c.nr; ++q) {
+      int lo = 0, hi = N;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (tab.id[mid] < c.rid[q])
+          lo = mid + 1;
+        else
+          hi = mid;
+      }
+      if (lo >= N || tab.id[lo] != c.rid[q]) {
+        s_bad = 2;
+        break;
+      }
+      P.rslot[q] = tab.slot[lo];
+      P.rx[q] = tab.x[lo];
+      P.rt[q] = tab.t[lo];
+    }
+    for (int a = 0; a < c.na; ++a) {
+      P.ax[a] = c.ax[a];
+      P.at[a] = c.at[a];
+      const double t = c.at[a];
+      if (c.ax[a] < 0.0 || c.ax[a] > d.x_max ||
+          !(t >= c.slo && (t < c.shi || (c.sclosed && t == c.shi))))
+        s_bad = s_bad ? s_bad : 1;
+    }
+  }
+  __syncthreads();
+  if (s_bad) {
+    if (tid == 0) out[blockIdx.x] = s_bad == 1 ? -INFINITY : NAN;
+    return;
+  }
+  PassIn in;
+  in.src = SRC_ROWS;
+  in.rows[0] = rows + (size_t)c.arow[0] * d.S;
+  in.rows[1] = rows + (size_t)c.arow[1] * d.S;
+  in.wlo = c.wlo;
+  in.whi = c.whi;
+  in.seed = 0;
+  in.sweep = in.region = in.step = 0;
+  double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  int cnt = 0;
+  station_pass<YT>(d, P, in, 0, nullptr, nullptr, Ls, Is, acc, cnt);
+#pragma unroll
+  for (int q = 0; q < 5; ++q) acc[q] = warp_sum(acc[q]);
+  if (lane == 0)
+    for (int q = 0; q < 5; ++q) red[warp][q] = acc[q];
+  __syncthreads();
+  if (tid == 0) {
+    double sig = 0.0, A[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int w = 0; w < NW; ++w) {
+      sig += red[w][0];
+      for (int q = 1; q < 5; ++q) A[q] += red[w][q];
+    }
+    double delta = c.prior;
+    if (c.na >= 1) delta += A[1];
+    if (c.na >= 2) delta += A[2];
+    if (c.nr >= 1) delta -= A[3];
+    if (c.nr >= 2) delta -= A[4];
+    out[blockIdx.x] = delta + sig;
+  }
+}
+
+// ----------------------------------------------------------------- log_joint
+// log_joint (density.hpp:146-154): full-window likelihood over [n][S] plus
+// arrival densities; per-block partials reduced in a fixed order.
+template <typename YT>
+__global__ void k_lj_signal(const Dev d, double* part) {
+  __shared__ double sred[32];
+  using T2 = typename Y2<YT>::T;
+  const T2* y2 = reinterpret_cast<const T2*>(d.y);
+  const size_t total = (size_t)d.n * d.P2;
+  double acc = 0.0;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const int p = (int)(i % d.P2);
+    const uint32_t w = d.cov[i];
+    const T2 yy = y2[i];
+    if (2 * p < d.S) {
+      const int c = (int)(w & 0xffffu);
+      const double y = (double)yy.x;
+      acc += d.Lg[c] - y * y * d.Ig[c];
+    }
+    if (2 * p + 1 < d.S) {
+      const int c = (int)(w >> 16);
+      const double y = (double)yy.y;
+      acc += d.Lg[c] - y * y * d.Ig[c];
+    }
+  }
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) sred[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += sred[w];
+    part[blockIdx.x] = s;
+  }
+}
+
+__global__ void k_lj_arrivals(const Dev d, Table tab, const Ctl* ctl, double* part) {
+  __shared__ double sred[32];
+  const int N = ctl->n_events;
+  const size_t total = (size_t)N * d.S;
+  double acc = 0.0;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const int e = (int)(i / d.S), j = (int)(i % d.S);
+    const double a = d.pool[(size_t)tab.slot[e] * d.S_pad + j];
+    acc += arr_logpdf(d, a, arrival_mean(d, tab.x[e], tab.t[e], d.stations[j]));
+  }
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) sred[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += sred[w];
+    part[blockIdx.x] = s;
+  }
+}
+
+__global__ void k_lj_final(const Dev d, double lambdaT, const double* logfact, const Ctl* ctl,
+                           const double* psig, int nsig, const double* parr, int narr,
+                           double* out) {
+  if (threadIdx.x != 0) return;
+  const int N = ctl->n_events;
+  double sig = 0.0, arr = 0.0;
+  for (int i = 0; i < nsig; ++i) sig += psig[i];
+  for (int i = 0; i < narr; ++i) arr += parr[i];
+  // log_event_prior over [0, T] (density.hpp:45-61)
+  const double prior =
+      -lambdaT + (double)N * d.log_lambda_T - logfact[N] + (double)N * d.lxa;
+  *out = prior + arr + sig;
+}
+
+__global__ void k_max_id(Table tab, const Ctl* ctl, unsigned long long* out) {
+  const int N = ctl->n_events;
+  unsigned long long m = 0;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) m = max(m, tab.id[i] + 1);
+  for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  __shared__ unsigned long long s[32];
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = max(m, s[w]);
+    *out = m;
+  }
+}
+
+__global__ void k_record(const Ctl* ctl, long long* count_out) { *count_out = ctl->n_events; }
+
+__global__ void k_reset_counters(Ctl* ctl) {
+  ctl->scored = ctl->changed = ctl->arrvals = ctl->accepted = ctl->id_mismatch = 0ull;
+  ctl->err = 0;
+}
+
+}  // namespace seis
+
+// =================================================================== host side
+using namespace seis;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& m) {
+  g_err = m;
+  return code;
+}
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class T>
+T* dalloc(size_t n) {
+  void* p = nullptr;
+  if (n == 0) n = 1;
+  ck(cudaMalloc(&p, n * sizeof(T)), "cudaMalloc");
+  return static_cast<T*>(p);
+}
+
+struct ValidationError : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return SEIS_OK;
+  } catch (const std::invalid_argument& e) {
+    return fail(SEIS_EINVAL, e.what());
+  } catch (const std::exception& e) {
+    return fail(SEIS_ERUNTIME, e.what());
+  }
+}
+
+void check_device() {
+  int dev = 0, n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+    throw std::runtime_error("no CUDA device: the B200 engine has no CPU fallback");
+  ck(cudaGetDevice(&dev), "cudaGetDevice");
+  cudaDeviceProp prop;
+  ck(cudaGetDeviceProperties(&prop, dev), "cudaGetDeviceProperties");
+  if (prop.major != 10)
+    throw std::runtime_error("engine is built for sm_100a (B200); device is sm_" +
+                             std::to_string(prop.major) + std::to_string(prop.minor));
+}
+
+// ModelConfig::validate (model.hpp:79-103)
+void validate_model(const seis_model_cfg* c, const double* st, int64_t S) {
+  auto bad = [](const std::string& m) { throw std::invalid_argument("ModelConfig: " + m); };
+  if (!(c->lambda_rate > 0)) bad("lambda_rate must be > 0");
+  if (!(c->T > 0)) bad("T must be > 0");
+  if (!(c->x_max > 0)) bad("x_max must be > 0");
+  if (!(c->v > 0)) bad("v must be > 0");
+  if (!(c->sigma_arrival > 0)) bad("sigma_arrival must be > 0");
+  if (!(c->t_s > 0)) bad("t_s must be > 0");
+  if (!(c->var_noise > 0)) bad("var_noise must be > 0");
+  if (!(c->var_event > c->var_noise)) bad("var_event must exceed var_noise");
+  if (!(c->sample_rate > 0)) bad("sample_rate must be > 0");
+  const double n = c->sample_rate * c->T;
+  if (std::abs(n - std::llround(n)) > 1e-9) bad("sample_rate * T must be an integer sample count");
+  if (S < 2) bad("need at least 2 stations");
+  for (int64_t j = 0; j < S; ++j) {
+    if (st[j] < 0 || st[j] > c->x_max) bad("station " + std::to_string(j) + " outside [0, x_max]");
+    if (j > 0 && !(st[j - 1] < st[j])) bad("stations must be sorted strictly ascending");
+  }
+}
+
+}  // namespace
+
+struct seis_engine {
+  seis_model_cfg cfg{};
+  int S = 0, S_pad = 0, P2 = 0, n = 0, dtype = 0, cap = 0;
+  cudaStream_t stream = nullptr;
+  Dev d{};
+  double* stations = nullptr;
+  void* y = nullptr;
+  uint32_t* cov = nullptr;
+  double* pool = nullptr;
+  double* Lg = nullptr;
+  double* Ig = nullptr;
+  double* logi = nullptr;
+  double* logfact = nullptr;
+  std::vector<double> h_logi, h_logfact;
+  Table tab[2]{};
+  int cur = 0;
+  int* free_stack = nullptr;
+  Ctl* ctl = nullptr;
+  int* fate_stamp = nullptr;
+  int* fate_alive = nullptr;
+  double* fate_x = nullptr;
+  double* fate_t = nullptr;
+  int* fate_slot = nullptr;
+  int stamp = 0;
+
+  ~seis_engine() {
+    cudaFree(stations);
+    cudaFree(y);
+    cudaFree(cov);
+    cudaFree(pool);
+    cudaFree(Lg);
+    cudaFree(Ig);
+    cudaFree(logi);
+    cudaFree(logfact);
+    for (auto& t : tab) {
+      cudaFree(t.id);
+      cudaFree(t.x);
+      cudaFree(t.t);
+      cudaFree(t.slot);
+    }
+    cudaFree(free_stack);
+    cudaFree(ctl);
+    cudaFree(fate_stamp);
+    cudaFree(fate_alive);
+    cudaFree(fate_x);
+    cudaFree(fate_t);
+    cudaFree(fate_slot);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+namespace {
+
+void upload_signals(seis_engine* e, const void* signals) {
+  const size_t esz = e->dtype == SEIS_F64 ? 8 : 4;
+  void* tmp = nullptr;
+  ck(cudaMalloc(&tmp, (size_t)e->S * e->n * esz), "cudaMalloc");
+  ck(cudaMemcpyAsync(tmp, signals, (size_t)e->S * e->n * esz, cudaMemcpyHostToDevice, e->stream),
+     "H2D signals");
+  dim3 grid((e->n + 31) / 32, (e->S_pad + 31) / 32), block(32, 8);
+  if (e->dtype == SEIS_F64)
+    k_transpose<double><<<grid, block, 0, e->stream>>>(static_cast<const double*>(tmp),
+                                                       static_cast<double*>(e->y), e->S,
+                                                       e->S_pad, e->n);
+  else
+    k_transpose<float><<<grid, block, 0, e->stream>>>(static_cast<const float*>(tmp),
+                                                      static_cast<float*>(e->y), e->S, e->S_pad,
+                                                      e->n);
+  ck(cudaGetLastError(), "k_transpose");
+  ck(cudaStreamSynchronize(e->stream), "sync");
+  cudaFree(tmp);
+}
+
+Ctl read_ctl(seis_engine* e) {
+  Ctl c;
+  ck(cudaMemcpyAsync(&c, e->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, e->stream), "D2H ctl");
+  ck(cudaStreamSynchronize(e->stream), "sync");
+  return c;
+}
+
+const char* err_name(int e) {
+  switch (e) {
+    case ERR_OWN_OVERFLOW: return "a region exceeded the per-region event limit (128)";
+    case ERR_POOL_EXHAUSTED: return "event pool exhausted: raise event_capacity";
+    case ERR_TAPE_UNKNOWN_ID: return "replay tape names an event the region does not hold";
+    case ERR_TABLE_OVERFLOW: return "event table overflow: raise event_capacity";
+    default: return "device error";
+  }
+}
+
+template <typename YT>
+void launch_lj(seis_engine* e, double* out_dev, double* scratch) {
+  const int nb = 296;
+  k_lj_signal<YT><<<nb, 256, 0, e->stream>>>(e->d, scratch);
+  k_lj_arrivals<<<nb, 256, 0, e->stream>>>(e->d, e->tab[e->cur], e->ctl, scratch + nb);
+  k_lj_final<<<1, 32, 0, e->stream>>>(e->d, e->cfg.lambda_rate * e->cfg.T, e->logfact, e->ctl,
+                                       scratch, nb, scratch + nb, nb, out_dev);
+}
+
+void launch_lj_any(seis_engine* e, double* out_dev, double* scratch) {
+  if (e->dtype == SEIS_F64)
+    launch_lj<double>(e, out_dev, scratch);
+  else
+    launch_lj<float>(e, out_dev, scratch);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* seis_last_error(void) { return g_err.c_str(); }
+
+int seis_engine_create(const seis_model_cfg* cfg, const double* stations, int64_t n_stations,
+                       const void* signals, int32_t dtype, int64_t event_capacity,
+                       seis_engine** out) {
+  *out = nullptr;
+  seis_engine* e = nullptr;
+  const int rc = guarded([&] {
+    validate_model(cfg, stations, n_stations);
+    if (dtype != SEIS_F32 && dtype != SEIS_F64) throw std::invalid_argument("dtype must be F32 or F64");
+    if (event_capacity < 1 || event_capacity > 65000)
+      throw std::invalid_argument("event_capacity must be in [1, 65000] (uint16 coverage counts)");
+    check_device();
+    e = new seis_engine;
+    e->cfg = *cfg;
+    e->S = (int)n_stations;
+    e->S_pad = (int)((n_stations + 63) / 64 * 64);
+    e->P2 = e->S_pad / 2;
+    e->n = (int)std::llround(cfg->sample_rate * cfg->T);
+    e->dtype = dtype;
+    e->cap = (int)event_capacity;
+    ck(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking), "stream");
+    std::vector<double> st(e->S_pad, 0.0);
+    std::copy(stations, stations + n_stations, st.begin());
+    e->stations = dalloc<double>(e->S_pad);
+    ck(cudaMemcpy(e->stations, st.data(), st.size() * 8, cudaMemcpyHostToDevice), "H2D");
+    const size_t esz = dtype == SEIS_F64 ? 8 : 4;
+    ck(cudaMalloc(&e->y, (size_t)e->n * e->S_pad * esz), "cudaMalloc y");
+    e->cov = dalloc<uint32_t>((size_t)e->n * e->P2);
+    ck(cudaMemset(e->cov, 0, (size_t)e->n * e->P2 * 4), "memset");
+    e->pool = dalloc<double>((size_t)e->cap * e->S_pad);
+    // per-count terms with glibc log, exactly as density.hpp:288-297
+    const int tab_n = e->cap + 8;
+    std::vector<double> L(tab_n), I(tab_n);
+    for (int c = 0; c < tab_n; ++c) {
+      const double var = cfg->var_noise + c * cfg->var_event;
+      L[c] = -0.5 * (kLog2Pi + std::log(var));
+      I[c] = 0.5 / var;
+    }
+    e->Lg = dalloc<double>(tab_n);
+    e->Ig = dalloc<double>(tab_n);
+    ck(cudaMemcpy(e->Lg, L.data(), tab_n * 8, cudaMemcpyHostToDevice), "H2D");
+    ck(cudaMemcpy(e->Ig, I.data(), tab_n * 8, cudaMemcpyHostToDevice), "H2D");
+    e->h_logi.resize(tab_n);
+    e->h_logfact.resize(tab_n);
+    double acc = 0.0;
+    for (int i = 0; i < tab_n; ++i) {
+      e->h_logi[i] = i > 0 ? std::log(static_cast<double>(i)) : -INFINITY;
+      if (i >= 2) acc += std::log(static_cast<double>(i));  // log_factorial, density.hpp:21-25
+      e->h_logfact[i] = acc;
+    }
+    e->logi = dalloc<double>(tab_n);
+    e->logfact = dalloc<double>(tab_n);
+    ck(cudaMemcpy(e->logi, e->h_logi.data(), tab_n * 8, cudaMemcpyHostToDevice), "H2D");
+    ck(cudaMemcpy(e->logfact, e->h_logfact.data(), tab_n * 8, cudaMemcpyHostToDevice), "H2D");
+    for (auto& t : e->tab) {
+      t.id = dalloc<unsigned long long>(e->cap);
+      t.x = dalloc<double>(e->cap);
+      t.t = dalloc<double>(e->cap);
+      t.slot = dalloc<int>(e->cap);
+    }
+    e->free_stack = dalloc<int>(e->cap);
+    e->ctl = dalloc<Ctl>(1);
+    e->fate_stamp = dalloc<int>(e->cap);
+    ck(cudaMemset(e->fate_stamp, 0, e->cap * 4), "memset");
+    e->fate_alive = dalloc<int>(e->cap);
+    e->fate_x = dalloc<double>(e->cap);
+    e->fate_t = dalloc<double>(e->cap);
+    e->fate_slot = dalloc<int>(e->cap);
+    Dev& d = e->d;
+    d.S = e->S;
+    d.S_pad = e->S_pad;
+    d.P2 = e->P2;
+    d.n = e->n;
+    d.rate = cfg->sample_rate;
+    d.t_s = cfg->t_s;
+    d.v = cfg->v;
+    d.sigma = cfg->sigma_arrival;
+    d.x_max = cfg->x_max;
+    d.T = cfg->T;
+    const double var_a = cfg->sigma_arrival * cfg->sigma_arrival;
+    d.c0_arr = -0.5 * (kLog2Pi + std::log(var_a));
+    d.twovar_arr = 2.0 * var_a;
+    d.log_lambda_T = std::log(cfg->lambda_rate * cfg->T);
+    d.lxa = -std::log(cfg->x_max) - std::log(cfg->T);
+    d.log_xmax = std::log(cfg->x_max);
+    d.stations = e->stations;
+    d.y = e->y;
+    d.cov = e->cov;
+    d.pool = e->pool;
+    d.Lg = e->Lg;
+    d.Ig = e->Ig;
+    d.tab_n = tab_n;
+    d.logi = e->logi;
+    d.logi_n = tab_n;
+    d.pool_cap = e->cap;
+    upload_signals(e, signals);
+  });
+  if (rc) {
+    delete e;
+    return rc;
+  }
+  // start from the empty hypothesis (samplers.hpp:409)
+  const int rc2 = seis_set_hypothesis(e, 0, nullptr, nullptr, nullptr, nullptr);
+  if (rc2) {
+    delete e;
+    return rc2;
+  }
+  *out = e;
+  return SEIS_OK;
+}
+
+void seis_engine_destroy(seis_engine* eng) { delete eng; }
+
+int seis_upload_signals(seis_engine* e, const void* signals) {
+  return guarded([&] { upload_signals(e, signals); });
+}
+
+int seis_set_hypothesis(seis_engine* e, int64_t N, const uint64_t* ids, const double* x,
+                        const double* t, const double* arrivals) {
+  return guarded([&] {
+    if (N < 0 || N > e->cap) throw std::invalid_argument("hypothesis larger than event_capacity");
+    std::vector<int64_t> order(N);
+    for (int64_t i = 0; i < N; ++i) order[i] = i;
+    std::sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return ids[a] < ids[b]; });
+    for (int64_t i = 1; i < N; ++i)
+      if (ids[order[i]] == ids[order[i - 1]]) throw std::invalid_argument("duplicate event id");
+    std::vector<unsigned long long> hid(N);
+    std::vector<double> hx(N), ht(N), ha((size_t)N * e->S_pad, 0.0);
+    std::vector<int> hs(N), fs(e->cap);
+    for (int64_t i = 0; i < N; ++i) {
+      const int64_t k = order[i];
+      hid[i] = ids[k];
+      hx[i] = x[k];
+      ht[i] = t[k];
+      hs[i] = (int)i;
+      std::copy(arrivals + k * e->S, arrivals + (k + 1) * e->S, ha.begin() + i * e->S_pad);
+    }
+    // free stack: slots N..cap-1 (top of stack = lowest)
+    int nf = 0;
+    for (int s = e->cap - 1; s >= (int)N; --s) fs[nf++] = s;
+    e->cur = 0;
+    Table& tb = e->tab[0];
+    if (N) {
+      ck(cudaMemcpy(tb.id, hid.data(), N * 8, cudaMemcpyHostToDevice), "H2D");
+      ck(cudaMemcpy(tb.x, hx.data(), N * 8, cudaMemcpyHostToDevice), "H2D");
+      ck(cudaMemcpy(tb.t, ht.data(), N * 8, cudaMemcpyHostToDevice), "H2D");
+      ck(cudaMemcpy(tb.slot, hs.data(), N * 4, cudaMemcpyHostToDevice), "H2D");
+      ck(cudaMemcpy(e->pool, ha.data(), ha.size() * 8, cudaMemcpyHostToDevice), "H2D");
+    }
+    ck(cudaMemcpy(e->free_stack, fs.data(), (size_t)nf * 4 + 4, cudaMemcpyHostToDevice), "H2D");
+    Ctl c{};
+    c.n_events = (int)N;
+    c.free_top = nf;
+    ck(cudaMemcpy(e->ctl, &c, sizeof c, cudaMemcpyHostToDevice), "H2D");
+    ck(cudaMemsetAsync(e->cov, 0, (size_t)e->n * e->P2 * 4, e->stream), "memset");
+    if (N) {
+      dim3 grid((e->P2 + 127) / 128, (unsigned)N);
+      k_build_cov<<<grid, 128, 0, e->stream>>>(e->d, tb, e->ctl);
+      ck(cudaGetLastError(), "k_build_cov");
+    }
+    ck(cudaStreamSynchronize(e->stream), "sync");
+  });
+}
+
+int seis_get_hypothesis(seis_engine* e, int64_t cap, int64_t* n, uint64_t* ids, double* x,
+                        double* t, double* arrivals) {
+  return guarded([&] {
+    const Ctl c = read_ctl(e);
+    *n = c.n_events;
+    const int64_t m = std::min<int64_t>(cap, c.n_events);
+    if (m <= 0) return;
+    const Table& tb = e->tab[e->cur];
+    ck(cudaMemcpy(ids, tb.id, m * 8, cudaMemcpyDeviceToHost), "D2H");
+    ck(cudaMemcpy(x, tb.x, m * 8, cudaMemcpyDeviceToHost), "D2H");
+    ck(cudaMemcpy(t, tb.t, m * 8, cudaMemcpyDeviceToHost), "D2H");
+    if (arrivals) {
+      std::vector<int> sl(m);
+      ck(cudaMemcpy(sl.data(), tb.slot, m * 4, cudaMemcpyDeviceToHost), "D2H");
+      for (int64_t i = 0; i < m; ++i)
+        ck(cudaMemcpy(arrivals + i * e->S, e->pool + (size_t)sl[i] * e->S_pad, e->S * 8,
+                      cudaMemcpyDeviceToHost),
+           "D2H");
+    }
+  });
+}
+
+int seis_partition(double T, double l, double offset, double tau, int64_t cap,
+                   int64_t* n_regions, double* boundaries, int32_t* colors, int32_t* n_colors) {
+  return guarded([&] {
+    // argument validation of build_partition / color_partition (partition.hpp:41-46,67-78)
+    if (!(T > 0)) throw std::invalid_argument("build_partition: T must be > 0");
+    if (!(l > 0) || l > T) throw std::invalid_argument("build_partition: need 0 < l <= T");
+    if (offset < 0 || offset >= l)
+      throw std::invalid_argument("build_partition: need 0 <= offset < l");
+    if (!(tau >= 0)) throw std::invalid_argument("color_partition: tau_max must be >= 0");
+    int k;
+    if (l >= tau)
+      k = 2;
+    else if (l >= tau / 2)
+      k = 3;
+    else
+      throw std::invalid_argument("color_partition: region length is below tau_max/2");
+    check_device();
+    const int bcap = (int)std::min<int64_t>(cap, (int64_t)(T / l) + 8);
+    double* b = dalloc<double>(bcap);
+    int* nr = dalloc<int>(1);
+    int* err = dalloc<int>(1);
+    ck(cudaMemset(err, 0, 4), "memset");
+    // offset passed explicitly: epoch-0 static path with the given u
+    int* col = dalloc<int>(bcap);
+    k_partition<<<1, 1>>>(T, l, tau, k, 2, 0, 0, 1, offset, bcap, b, nr, err, col);
+    ck(cudaGetLastError(), "k_partition");
+    int h_nr = 0, h_err = 0;
+    ck(cudaMemcpy(&h_nr, nr, 4, cudaMemcpyDeviceToHost), "D2H");
+    ck(cudaMemcpy(&h_err, err, 4, cudaMemcpyDeviceToHost), "D2H");
+    if (h_err == 2) throw std::runtime_error("partition capacity");
+    *n_regions = h_nr;
+    if (h_nr + 1 > cap) throw std::runtime_error("partition capacity");
+    ck(cudaMemcpy(boundaries, b, (size_t)(h_nr + 1) * 8, cudaMemcpyDeviceToHost), "D2H");
+    std::vector<int> hc(h_nr);
+    ck(cudaMemcpy(hc.data(), col, (size_t)h_nr * 4, cudaMemcpyDeviceToHost), "D2H");
+    for (int i = 0; i < h_nr; ++i) colors[i] = hc[i];
+    *n_colors = k;
+    cudaFree(col);
+    cudaFree(b);
+    cudaFree(nr);
+    cudaFree(err);
+    if (h_err == 1) throw std::logic_error("color_partition: separation invariant violated");
+  });
+}
+
+int seis_assign_regions(const double* boundaries, int64_t n_regions, int64_t m, const double* t,
+                        int64_t* region_out) {
+  return guarded([&] {
+    check_device();
+    if (n_regions < 1) throw std::invalid_argument("need at least one region");
+    double* b = dalloc<double>(n_regions + 1);
+    double* dt = dalloc<double>(m);
+    int64_t* o = dalloc<int64_t>(m);
+    ck(cudaMemcpy(b, boundaries, (n_regions + 1) * 8, cudaMemcpyHostToDevice), "H2D");
+    if (m) ck(cudaMemcpy(dt, t, m * 8, cudaMemcpyHostToDevice), "H2D");
+    if (m) k_region_of<<<(unsigned)((m + 255) / 256), 256>>>(b, (int)n_regions, m, dt, o);
+    ck(cudaGetLastError(), "k_region_of");
+    if (m) ck(cudaMemcpy(region_out, o, m * 8, cudaMemcpyDeviceToHost), "D2H");
+    cudaFree(b);
+    cudaFree(dt);
+    cudaFree(o);
+  });
+}
+
+int seis_partition_offset(uint64_t seed, int64_t epoch, double l, double* u_out) {
+  return guarded([&] {
+    check_device();
+    double* o = dalloc<double>(1);
+    k_offsets<<<1, 1>>>(seed, epoch, l, o);
+    ck(cudaGetLastError(), "k_offsets");
+    ck(cudaMemcpy(u_out, o, 8, cudaMemcpyDeviceToHost), "D2H");
+    cudaFree(o);
+  });
+}
+
+int seis_score_batch(seis_engine* e, int64_t n_changes, const seis_change* changes,
+                     const double* added_arrivals, int64_t n_rows, double* delta_out) {
+  return guarded([&] {
+    if (n_changes == 0) return;
+    const Ctl c = read_ctl(e);
+    const int64_t N = c.n_events;
+    std::vector<ChangeDev> hc(n_changes);
+    for (int64_t i = 0; i < n_changes; ++i) {
+      const seis_change& s = changes[i];
+      if (s.n_removed < 0 || s.n_removed > 2 || s.n_added < 0 || s.n_added > 2)
+        throw std::invalid_argument("a change holds at most 2 removed and 2 added events");
+      ChangeDev& h = hc[i];
+      h.nr = s.n_removed;
+      h.na = s.n_added;
+      for (int q = 0; q < 2; ++q) {
+        h.rid[q] = s.removed_id[q];
+        h.ax[q] = s.added_x[q];
+        h.at[q] = s.added_t[q];
+        h.arow[q] = q < s.n_added ? s.added_row[q] : 0;
+        if (q < s.n_added && (s.added_row[q] < 0 || s.added_row[q] >= n_rows))
+          throw std::invalid_argument("added_row out of range");
+      }
+      h.wlo = (int)std::max<int64_t>(0, s.window_lo);
+      h.whi = (int)std::min<int64_t>(e->n, s.window_hi);
+      h.slo = s.support_lo;
+      h.shi = s.support_hi;
+      h.sclosed = s.support_closed;
+      // prior part of delta_log_joint (density.hpp:223-237), glibc log
+      const int64_t n0 = N, n1 = n0 - s.n_removed + s.n_added;
+      const double area = s.support_hi - s.support_lo;
+      const double lla = std::log(e->cfg.lambda_rate * area);
+      double delta = 0.0;
+      if (n1 > n0) {
+        for (int64_t k = n0 + 1; k <= n1; ++k) delta += lla - std::log(static_cast<double>(k));
+      } else if (n1 < n0) {
+        for (int64_t k = n1 + 1; k <= n0; ++k) delta -= lla - std::log(static_cast<double>(k));
+      }
+      delta += static_cast<double>(n1 - n0) * (-std::log(e->cfg.x_max) - std::log(area));
+      h.prior = delta;
+    }
+    ChangeDev* dc = dalloc<ChangeDev>(n_changes);
+    double* rows = dalloc<double>(std::max<int64_t>(n_rows, 1) * e->S);
+    double* o = dalloc<double>(n_changes);
+    ck(cudaMemcpyAsync(dc, hc.data(), n_changes * sizeof(ChangeDev), cudaMemcpyHostToDevice,
+                       e->stream),
+       "H2D");
+    if (n_rows)
+      ck(cudaMemcpyAsync(rows, added_arrivals, (size_t)n_rows * e->S * 8,
+                         cudaMemcpyHostToDevice, e->stream),
+         "H2D");
+    if (e->dtype == SEIS_F64)
+      k_score_batch<double><<<(unsigned)n_changes, NT, 0, e->stream>>>(e->d, e->tab[e->cur],
+                                                                       e->ctl, dc, rows, o);
+    else
+      k_score_batch<float><<<(unsigned)n_changes, NT, 0, e->stream>>>(e->d, e->tab[e->cur],
+                                                                      e->ctl, dc, rows, o);
+    ck(cudaGetLastError(), "k_score_batch");
+    ck(cudaMemcpyAsync(delta_out, o, n_changes * 8, cudaMemcpyDeviceToHost, e->stream), "D2H");
+    ck(cudaStreamSynchronize(e->stream), "sync");
+    cudaFree(dc);
+    cudaFree(rows);
+    cudaFree(o);
+    for (int64_t i = 0; i < n_changes; ++i)
+      if (std::isnan(delta_out[i]))
+        throw std::invalid_argument("removed event id not in the hypothesis");
+  });
+}
+
+int seis_log_joint(seis_engine* e, double* out) {
+  return guarded([&] {
+    double* scratch = dalloc<double>(2 * 296 + 1);
+    launch_lj_any(e, scratch + 2 * 296, scratch);
+    ck(cudaGetLastError(), "log_joint");
+    ck(cudaMemcpyAsync(out, scratch + 2 * 296, 8, cudaMemcpyDeviceToHost, e->stream), "D2H");
+    ck(cudaStreamSynchronize(e->stream), "sync");
+    cudaFree(scratch);
+  });
+}
+
+}  // extern "C"
+
+extern "C" int seis_run_chromatic(seis_engine* e, const seis_sampler_cfg* sc, int32_t mode,
+                                  const seis_tape_step* tape, int64_t n_tape,
+                                  const double* tape_arr, int64_t n_tape_arr,
+                                  seis_step_out* step_out, int64_t row_cap, int64_t* row_step,
+                                  double* row_log_joint, int64_t* row_count,
+                                  seis_run_stats* stats) {
+  std::vector<void*> tmp;
+  std::vector<cudaEvent_t> evs;
+  auto alloc = [&](size_t bytes) {
+    void* p = nullptr;
+    ck(cudaMalloc(&p, bytes ? bytes : 1), "cudaMalloc");
+    tmp.push_back(p);
+    return p;
+  };
+  const int rc = guarded([&] {
+    // SamplerConfig::validate + MoveDistribution::validate (samplers.hpp:59-70,
+    // proposals.hpp:23-31)
+    if (sc->steps_per_epoch < 1)
+      throw std::invalid_argument("SamplerConfig: steps_per_epoch must be >= 1");
+    if (sc->epochs < 1) throw std::invalid_argument("SamplerConfig: epochs must be >= 1");
+    if (sc->n_regions < 1) throw std::invalid_argument("SamplerConfig: n_regions must be >= 1");
+    if (sc->burn_in_fraction < 0 || sc->burn_in_fraction >= 1)
+      throw std::invalid_argument("SamplerConfig: burn_in_fraction must be in [0, 1)");
+    if (sc->record_every < 1)
+      throw std::invalid_argument("SamplerConfig: record_every must be >= 1");
+    double wsum = 0.0;
+    for (double w : sc->weights) {
+      if (w < 0) throw std::invalid_argument("MoveDistribution: negative weight");
+      wsum += w;
+    }
+    if (std::abs(wsum - 1.0) > 1e-12)
+      throw std::invalid_argument("MoveDistribution: weights must sum to 1");
+    if (mode != 0 && mode != 1) throw std::invalid_argument("mode must be 0 or 1");
+    if (mode == 1 && (!tape || !step_out)) throw std::invalid_argument("replay needs a tape");
+    // run_chromatic setup (samplers.hpp:405-407)
+    const double tau = e->cfg.x_max / e->cfg.v;
+    const double l = e->cfg.T / (double)sc->n_regions;
+    if (l > e->cfg.T) throw std::invalid_argument("build_partition: need 0 < l <= T");
+    int ncol;
+    if (l >= tau)
+      ncol = 2;
+    else if (l >= tau / 2)
+      ncol = 3;
+    else
+      throw std::invalid_argument("color_partition: region length " + std::to_string(l) +
+                                  " is below tau_max/2 = " + std::to_string(tau / 2) +
+                                  "; would need more than 3 colors");
+    Samp sp{};
+    sp.k = sc->steps_per_epoch;
+    sp.seed = sc->seed;
+    double cum = 0.0;
+    for (int q = 0; q < 5; ++q) {
+      cum += sc->weights[q];
+      sp.cumw[q] = cum;
+      sp.logw[q] = std::log(sc->weights[q]);
+    }
+    sp.step_lx = sc->step_location_x;
+    sp.step_lt = sc->step_location_t;
+    sp.step_arr = sc->step_arrival;
+    sp.step_joint = sc->step_joint;
+    sp.joint_t_sd = sc->step_joint / e->cfg.v;
+    sp.ncol = ncol;
+    const int bcap = (int)sc->n_regions + 4;
+    const int CH = (int)std::min<int64_t>(sc->epochs, 64);
+    double* bnd = static_cast<double*>(alloc((size_t)CH * bcap * 8));
+    int* nreg_d = static_cast<int*>(alloc((size_t)CH * 4));
+    int* perr = static_cast<int*>(alloc(4));
+    const int n_slots = (int)((sc->n_regions + 1 + ncol - 1) / ncol) + 1;
+    int* births_cnt = static_cast<int*>(alloc((size_t)n_slots * 4));
+    OutEv* births = static_cast<OutEv*>(alloc((size_t)n_slots * MAXOWN * sizeof(OutEv)));
+    int* diff_cnt = static_cast<int*>(alloc((size_t)n_slots * 4));
+    DiffEnt* diff = static_cast<DiffEnt*>(alloc((size_t)n_slots * MAXDIFF * sizeof(DiffEnt)));
+    seis_tape_step* d_tape = nullptr;
+    double* d_tarr = nullptr;
+    seis_step_out* d_out = nullptr;
+    if (mode == 1) {
+      d_tape = static_cast<seis_tape_step*>(alloc((size_t)n_tape * sizeof(seis_tape_step)));
+      d_tarr = static_cast<double*>(alloc((size_t)std::max<int64_t>(n_tape_arr, 1) * 8));
+      d_out = static_cast<seis_step_out*>(alloc((size_t)n_tape * sizeof(seis_step_out)));
+      ck(cudaMemcpyAsync(d_tape, tape, (size_t)n_tape * sizeof(seis_tape_step),
+                         cudaMemcpyHostToDevice, e->stream),
+         "H2D tape");
+      if (n_tape_arr)
+        ck(cudaMemcpyAsync(d_tarr, tape_arr, (size_t)n_tape_arr * 8, cudaMemcpyHostToDevice,
+                           e->stream),
+           "H2D tape arrivals");
+    }
+    const int64_t rcap = std::max<int64_t>(row_cap, 1);
+    double* lj_dev = static_cast<double*>(alloc((size_t)rcap * 8));
+    long long* cnt_dev = static_cast<long long*>(alloc((size_t)rcap * 8));
+    double* lj_scratch = static_cast<double*>(alloc((2 * 296 + 1) * 8));
+    unsigned long long* maxid = static_cast<unsigned long long*>(alloc(8));
+    // next_base: above every id already present (reference starts empty at 0)
+    k_max_id<<<1, 1024, 0, e->stream>>>(e->tab[e->cur], e->ctl, maxid);
+    k_reset_counters<<<1, 1, 0, e->stream>>>(e->ctl);
+    unsigned long long next_base = 0;
+    ck(cudaMemcpyAsync(&next_base, maxid, 8, cudaMemcpyDeviceToHost, e->stream), "D2H");
+    ck(cudaStreamSynchronize(e->stream), "sync");
+    int64_t launches = 2;
+    cudaEvent_t ev_start, ev_stop;
+    ck(cudaEventCreate(&ev_start), "event");
+    ck(cudaEventCreate(&ev_stop), "event");
+    evs.push_back(ev_start);
+    evs.push_back(ev_stop);
+    const bool timing = stats != nullptr;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> phase_ev;
+    int64_t n_rows = 0;
+    std::vector<int64_t> h_row_step;
+    auto record_row = [&](int64_t executed) {
+      if (n_rows < row_cap) {
+        if (sc->record_log_joint) {
+          launch_lj_any(e, lj_dev + n_rows, lj_scratch);
+          launches += 3;
+        }
+        k_record<<<1, 1, 0, e->stream>>>(e->ctl, cnt_dev + n_rows);
+        ++launches;
+        h_row_step.push_back(executed);
+      }
+      ++n_rows;
+    };
+    ck(cudaEventRecord(ev_start, e->stream), "event");
+    record_row(0);
+    int64_t executed = 0, last_recorded = 0;
+    long long tape_base = 0;
+    const int64_t k = sc->steps_per_epoch;
+    std::vector<int> h_nreg(CH);
+    for (int64_t e0 = 0; e0 < sc->epochs; e0 += CH) {
+      const int nep = (int)std::min<int64_t>(CH, sc->epochs - e0);
+      ck(cudaMemsetAsync(perr, 0, 4, e->stream), "memset");
+      k_partition<<<(nep + 63) / 64, 64, 0, e->stream>>>(
+          e->cfg.T, l, tau, ncol, sc->dynamic ? 1 : 0, sc->seed, (int)e0, nep, 0.0, bcap, bnd,
+          nreg_d, perr, nullptr);
+      ++launches;
+      int herr = 0;
+      ck(cudaMemcpyAsync(h_nreg.data(), nreg_d, (size_t)nep * 4, cudaMemcpyDeviceToHost,
+                         e->stream),
+         "D2H nreg");
+      ck(cudaMemcpyAsync(&herr, perr, 4, cudaMemcpyDeviceToHost, e->stream), "D2H");
+      ck(cudaStreamSynchronize(e->stream), "sync");
+      if (herr == 1) throw std::logic_error("color_partition: separation invariant violated");
+      if (herr == 2) throw std::runtime_error("partition capacity");
+      for (int i = 0; i < nep; ++i) {
+        const int epoch = (int)(e0 + i);
+        const int nreg = h_nreg[i];
+        for (int color = 0; color < ncol; ++color) {
+          const int ncr = nreg > color ? (nreg - color + ncol - 1) / ncol : 0;
+          if (ncr == 0) continue;
+          PhaseArgs pa{};
+          pa.epoch = epoch;
+          pa.color = color;
+          pa.nreg = nreg;
+          pa.n_slots = ncr;
+          pa.bnd = bnd + (size_t)i * bcap;
+          pa.next_base = next_base;
+          pa.tape_base = tape_base;
+          pa.tab = e->tab[e->cur];
+          pa.fate_stamp = e->fate_stamp;
+          pa.fate_alive = e->fate_alive;
+          pa.fate_x = e->fate_x;
+          pa.fate_t = e->fate_t;
+          pa.fate_slot = e->fate_slot;
+          pa.births_cnt = births_cnt;
+          pa.births = births;
+          pa.diff_cnt = diff_cnt;
+          pa.diff = diff;
+          pa.free_stack = e->free_stack;
+          pa.tape = d_tape;
+          pa.tape_arr = d_tarr;
+          pa.out = d_out;
+          const int stamp = ++e->stamp;
+          if (mode == 1 && tape_base + (long long)ncr * k > n_tape)
+            throw std::invalid_argument("replay tape shorter than the run");
+          cudaEvent_t a = nullptr, b = nullptr;
+          if (timing) {
+            ck(cudaEventCreate(&a), "event");
+            ck(cudaEventCreate(&b), "event");
+            evs.push_back(a);
+            evs.push_back(b);
+            ck(cudaEventRecord(a, e->stream), "event");
+          }
+          if (e->dtype == SEIS_F64) {
+            if (mode == 0)
+              k_phase<double, 0><<<ncr, NT, 0, e->stream>>>(e->d, sp, pa, e->ctl, stamp);
+            else
+              k_phase<double, 1><<<ncr, NT, 0, e->stream>>>(e->d, sp, pa, e->ctl, stamp);
+          } else {
+            if (mode == 0)
+              k_phase<float, 0><<<ncr, NT, 0, e->stream>>>(e->d, sp, pa, e->ctl, stamp);
+            else
+              k_phase<float, 1><<<ncr, NT, 0, e->stream>>>(e->d, sp, pa, e->ctl, stamp);
+          }
+          if (timing) {
+            ck(cudaEventRecord(b, e->stream), "event");
+            phase_ev.emplace_back(a, b);
+          }
+          ck(cudaGetLastError(), "k_phase");
+          k_commit<<<ncr, 256, 0, e->stream>>>(e->d, color, ncol, nreg, diff_cnt, diff,
+                                                 e->free_stack, e->ctl);
+          ck(cudaGetLastError(), "k_commit");
+          const int nxt = e->cur ^ 1;
+          k_rebuild<<<1, 1024, 0, e->stream>>>(e->tab[e->cur], e->tab[nxt], e->cap, stamp,
+                                                e->fate_stamp, e->fate_alive, e->fate_x,
+                                                e->fate_t, e->fate_slot, ncr, births_cnt,
+                                                births, e->ctl);
+          ck(cudaGetLastError(), "k_rebuild");
+          launches += 3;
+          e->cur = nxt;
+          next_base += (unsigned long long)ncr * (unsigned long long)k;
+          tape_base += (long long)ncr * k;
+          executed += (int64_t)ncr * k;
+          // record(false), samplers.hpp:424-434
+          if (executed - last_recorded >= sc->record_every) {
+            last_recorded = executed;
+            record_row(executed);
+          }
+        }
+      }
+    }
+    if (last_recorded != executed) record_row(executed);
+    ck(cudaEventRecord(ev_stop, e->stream), "event");
+    ck(cudaStreamSynchronize(e->stream), "run");
+    const Ctl c = read_ctl(e);
+    if (c.err) throw std::runtime_error(std::string("device: ") + err_name(c.err));
+    if (mode == 1 && tape_base != n_tape)
+      throw std::invalid_argument("replay tape longer than the run");
+    const int64_t nr_out = std::min<int64_t>(n_rows, row_cap);
+    if (nr_out > 0) {
+      std::vector<double> lj(nr_out);
+      std::vector<long long> cn(nr_out);
+      ck(cudaMemcpy(lj.data(), lj_dev, nr_out * 8, cudaMemcpyDeviceToHost), "D2H");
+      ck(cudaMemcpy(cn.data(), cnt_dev, nr_out * 8, cudaMemcpyDeviceToHost), "D2H");
+      for (int64_t i = 0; i < nr_out; ++i) {
+        if (row_step) row_step[i] = h_row_step[i];
+        if (row_log_joint) row_log_joint[i] = sc->record_log_joint ? lj[i] : 0.0;
+        if (row_count) row_count[i] = cn[i];
+      }
+    }
+    if (mode == 1)
+      ck(cudaMemcpy(step_out, d_out, (size_t)n_tape * sizeof(seis_step_out),
+                    cudaMemcpyDeviceToHost),
+         "D2H out");
+    if (stats) {
+      std::memset(stats, 0, sizeof *stats);
+      stats->total_steps = executed;
+      stats->total_accepted = (int64_t)c.accepted;
+      stats->scored_proposals = (int64_t)c.scored;
+      stats->changed_samples = (int64_t)c.changed;
+      stats->arrival_values = (int64_t)c.arrvals;
+      const double by = e->dtype == SEIS_F64 ? 8.0 : 4.0;
+      stats->algorithmic_bytes = (double)c.changed * (by + 2.0) + 8.0 * (double)c.arrvals;
+      float ms = 0.f;
+      double tot = 0.0;
+      for (auto& pr : phase_ev) {
+        ck(cudaEventElapsedTime(&ms, pr.first, pr.second), "elapsed");
+        tot += ms;
+      }
+      stats->sweep_kernel_ms = tot;
+      ck(cudaEventElapsedTime(&ms, ev_start, ev_stop), "elapsed");
+      stats->total_ms = ms;
+      stats->kernel_launches = launches;
+      stats->n_rows = n_rows;
+      stats->final_events = c.n_events;
+    }
+  });
+  for (auto ev : evs) cudaEventDestroy(ev);
+  for (void* p : tmp) cudaFree(p);
+  return rc;
+}

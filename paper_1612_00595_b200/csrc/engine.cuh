@@ -1,0 +1,145 @@
+// engine.cuh — device data layout and helpers of the B200 region-sweep engine.
+//
+// HBM layout:
+//   y     [n][S_pad]   observed signals, time-major (fp32 for configs 1-4, fp64
+//                      for config 0), so the ~20-sample arrival windows of a
+//                      proposal at neighbouring stations fall in the same rows
+//   cov   [n][S_pad/2] uint32 words packing two uint16 coverage counts
+//                      (stations 2p, 2p+1): the reference's per-sample signal
+//                      count, rebuilt there from all N events per proposal
+//                      (density.hpp:263-278), kept resident here
+//   pool  [P][S_pad]   fp64 arrival times, one slot per event version
+//   table sorted-by-id event list {id, x, t, slot} (the reference's
+//                      World::events after sort_by_id, samplers.hpp:481)
+#pragma once
+
+#include <cstdint>
+
+#include "../../include/seis_b200.h"
+#include "../../include/seis_philox.h"
+
+namespace seis {
+
+constexpr int NT = 512;          // threads per region CTA
+constexpr int NW = NT / 32;
+constexpr int MAXOWN = 128;      // events a region may hold during a phase
+constexpr int MAXDIFF = 2 * MAXOWN;
+constexpr int TBL = 1024;        // per-count log/inverse-variance entries kept in smem
+constexpr int BANDMAX = 256;     // rows of the generic diff-correction scratch
+constexpr double kLog2Pi = 1.8378770664093454835606594728112;
+
+struct Win {
+  int lo, hi;
+};
+
+struct Dev {
+  int S, S_pad, P2, n;
+  double rate, t_s, v, sigma, x_max, T;
+  double c0_arr, twovar_arr;       // log_gaussian constants for sigma_arrival
+  double log_lambda_T, lxa;        // log(lambda T), -log(x_max) - log(T)
+  double log_xmax;
+  const double* stations;          // [S_pad]
+  const void* y;                   // [n][S_pad]
+  uint32_t* cov;                   // [n][P2]
+  double* pool;                    // [P][S_pad]
+  const double* Lg;                // [tab_n] -0.5 (log 2pi + log var_c)
+  const double* Ig;                // [tab_n] 0.5 / var_c
+  int tab_n;
+  const double* logi;              // [logi_n] log((double) i)
+  int logi_n;
+  int pool_cap;
+};
+
+struct Samp {
+  int64_t k;
+  uint64_t seed;
+  double cumw[5];
+  double logw[5];
+  double step_lx, step_lt, step_arr, step_joint, joint_t_sd;
+  int ncol;
+};
+
+struct Table {
+  unsigned long long* id;
+  double* x;
+  double* t;
+  int* slot;
+};
+
+struct OutEv {
+  unsigned long long id;
+  double x, t;
+  int slot, pad;
+};
+
+struct DiffEnt {
+  int slot, sign;
+};
+
+struct Ctl {
+  int n_events;
+  int free_top;
+  int err;
+  int phase_stamp;
+  unsigned long long scored, changed, arrvals, accepted, id_mismatch;
+};
+
+struct PhaseArgs {
+  int epoch, color, nreg, n_slots;
+  const double* bnd;               // [nreg + 1]
+  unsigned long long next_base;
+  long long tape_base;
+  Table tab;                       // phase-start table (sorted by id)
+  int* fate_stamp;
+  int* fate_alive;
+  double* fate_x;
+  double* fate_t;
+  int* fate_slot;
+  int* births_cnt;                 // [n_slots]
+  OutEv* births;                   // [n_slots][MAXOWN]
+  int* diff_cnt;                   // [n_slots]
+  DiffEnt* diff;                   // [n_slots][MAXDIFF]
+  int* free_stack;
+  const seis_tape_step* tape;
+  const double* tape_arr;
+  seis_step_out* out;
+};
+
+enum : int {
+  ERR_NONE = 0,
+  ERR_OWN_OVERFLOW = 1,
+  ERR_POOL_EXHAUSTED = 2,
+  ERR_TAPE_UNKNOWN_ID = 3,
+  ERR_TABLE_OVERFLOW = 4,
+  ERR_COUNT_OVERFLOW = 5,
+};
+
+__device__ __forceinline__ Win make_win(const Dev& d, double a) {
+  // arrival_sample_range, density.hpp:29-36 (fp64, no contraction: --fmad=false)
+  const double n = (double)d.n;
+  double lo = ceil(a * d.rate);
+  double hi = ceil((a + d.t_s) * d.rate);
+  lo = fmin(fmax(lo, 0.0), n);
+  hi = fmin(fmax(hi, 0.0), n);
+  Win w;
+  w.lo = (int)lo;
+  w.hi = (int)hi;
+  return w;
+}
+
+__device__ __forceinline__ int inw(int r, Win w) {
+  return (unsigned)(r - w.lo) < (unsigned)(w.hi - w.lo) ? 1 : 0;
+}
+
+__device__ __forceinline__ double arrival_mean(const Dev& d, double x, double t, double s) {
+  return t + fabs(x - s) / d.v;  // model.hpp:73-75
+}
+
+__device__ __forceinline__ double arr_logpdf(const Dev& d, double a, double mean) {
+  // log_gaussian(a, mean, sigma^2), density.hpp:15-18 with host-computed
+  // -0.5 (log 2pi + log sigma^2) and 2 sigma^2
+  const double dd = a - mean;
+  return d.c0_arr - dd * dd / d.twovar_arr;
+}
+
+}  // namespace seis

@@ -1,0 +1,438 @@
+"""Python mirror of the reference sampler/model API over the engine's C-ABI.
+
+Names follow the reference (proj/include/seismic/): ``ModelConfig``
+(model.hpp:55-104), ``SamplerConfig`` (samplers.hpp:47-71), ``run_chromatic`` /
+``run_sampler`` (samplers.hpp:401-509), ``delta_log_joint`` (density.hpp:214-305,
+batched here), ``log_joint`` (density.hpp:146-154), ``build_partition`` +
+``color_partition`` (partition.hpp:40-90) and ``Partition.region_of``
+(partition.hpp:33-37). Validation errors raise ``ValueError`` (the reference's
+std::invalid_argument, CLI exit 2), runtime errors ``RuntimeError`` (exit 3).
+
+Everything computes in libseis_b200.so on the GPU; there is no CPU fallback.
+Loading fails loudly if the library is missing or no sm_100 device is present.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import build as _build
+
+i32, i64, u64, f64, P = C.c_int32, C.c_int64, C.c_uint64, C.c_double, C.c_void_p
+
+F32, F64 = 0, 1
+
+
+class _ModelC(C.Structure):
+    _fields_ = [(n, f64) for n in ("lambda_rate", "T", "x_max", "v", "sigma_arrival", "t_s",
+                                   "var_noise", "var_event", "sample_rate")]
+
+
+class _SamplerC(C.Structure):
+    _fields_ = [("steps_per_epoch", i64), ("epochs", i64), ("n_regions", i64), ("seed", u64),
+                ("burn_in_fraction", f64), ("record_every", i64), ("weights", f64 * 5),
+                ("step_location_x", f64), ("step_location_t", f64), ("step_arrival", f64),
+                ("step_joint", f64), ("dynamic", i32), ("record_log_joint", i32)]
+
+
+class _ChangeC(C.Structure):
+    _fields_ = [("n_removed", i32), ("n_added", i32), ("removed_id", u64 * 2),
+                ("added_x", f64 * 2), ("added_t", f64 * 2), ("added_row", i64 * 2),
+                ("window_lo", i64), ("window_hi", i64), ("support_lo", f64),
+                ("support_hi", f64), ("support_closed", i32), ("pad_", i32)]
+
+
+class _StatsC(C.Structure):
+    _fields_ = [("total_steps", i64), ("total_accepted", i64), ("scored_proposals", i64),
+                ("changed_samples", i64), ("arrival_values", i64), ("algorithmic_bytes", f64),
+                ("sweep_kernel_ms", f64), ("total_ms", f64), ("kernel_launches", i64),
+                ("n_rows", i64), ("final_events", i64)]
+
+
+TAPE_DTYPE = np.dtype([
+    ("epoch", "<i8"), ("color", "<i8"), ("region", "<i8"), ("slot", "<i8"), ("step", "<i8"),
+    ("type", "<i8"), ("is_null", "<i8"), ("n_removed", "<i8"), ("n_added", "<i8"),
+    ("u_drawn", "<i8"), ("scored", "<i8"), ("accepted", "<i8"), ("constrained_out", "<i8"),
+    ("removed_id", "<u8", (2,)), ("added_id", "<u8", (2,)), ("added_x", "<f8", (2,)),
+    ("added_t", "<f8", (2,)), ("logq_f", "<f8"), ("logq_r", "<f8"), ("u", "<f8"),
+    ("delta", "<f8"), ("log_r", "<f8"), ("added_arr_off", "<i8")])
+STEP_OUT_DTYPE = np.dtype([("delta", "<f8"), ("log_r", "<f8"), ("scored", "<i4"),
+                           ("accepted", "<i4")])
+
+EXPORTS = ("seis_last_error", "seis_engine_create", "seis_engine_destroy", "seis_upload_signals",
+           "seis_set_hypothesis", "seis_get_hypothesis", "seis_partition", "seis_assign_regions",
+           "seis_partition_offset", "seis_score_batch", "seis_log_joint", "seis_run_chromatic",
+           "seis_world_last_error", "seis_world_generate", "seis_world_with_events",
+           "seis_thomas_events")
+
+_LIB = None
+
+
+def load_library(path: str | None = None) -> C.CDLL:
+    """dlopen libseis_b200.so (in-tree). Raises if it is absent: no fallback."""
+    global _LIB
+    if _LIB is not None and path is None:
+        return _LIB
+    path = path or _build.LIB
+    if not os.path.exists(path):
+        raise ImportError(f"{path} missing: run `python -m paper_1612_00595_b200.build` "
+                          "(the engine has no CPU fallback)")
+    L = C.CDLL(path)
+    L.seis_last_error.restype = C.c_char_p
+    L.seis_world_last_error.restype = C.c_char_p
+    L.seis_engine_create.argtypes = [P, P, i64, P, i32, i64, P]
+    L.seis_engine_destroy.argtypes = [P]
+    L.seis_upload_signals.argtypes = [P, P]
+    L.seis_set_hypothesis.argtypes = [P, i64, P, P, P, P]
+    L.seis_get_hypothesis.argtypes = [P, i64, P, P, P, P, P]
+    L.seis_partition.argtypes = [f64, f64, f64, f64, i64, P, P, P, P]
+    L.seis_assign_regions.argtypes = [P, i64, i64, P, P]
+    L.seis_partition_offset.argtypes = [u64, i64, f64, P]
+    L.seis_score_batch.argtypes = [P, i64, P, P, i64, P]
+    L.seis_log_joint.argtypes = [P, P]
+    L.seis_run_chromatic.argtypes = [P, P, i32, P, i64, P, i64, P, i64, P, P, P, P]
+    L.seis_world_generate.argtypes = [P, P, i64, u64, i64, P, P, P, P, P, P, i32, i32]
+    L.seis_world_with_events.argtypes = [P, P, i64, i64, P, P, u64, P, P, i32, i32]
+    L.seis_thomas_events.argtypes = [u64, f64, f64, f64, f64, f64, f64, i64, P, P, P]
+    if path == _build.LIB:
+        _LIB = L
+    return L
+
+
+def _p(a):
+    return a.ctypes.data_as(P) if a is not None and a.size else None
+
+
+def _check(rc: int, L=None):
+    if rc == 0:
+        return
+    msg = (L or load_library()).seis_last_error().decode()
+    if rc == 2:
+        raise ValueError(msg)
+    raise RuntimeError(msg)
+
+
+@dataclass
+class ModelConfig:
+    """reference ModelConfig (model.hpp:55-65); defaults are the reference's."""
+    lambda_rate: float = 0.02
+    T: float = 240.0
+    x_max: float = 100.0
+    v: float = 2.0
+    sigma_arrival: float = 2.0
+    t_s: float = 20.0
+    var_noise: float = 1.0
+    var_event: float = 4.0
+    sample_rate: float = 1.0
+    stations: np.ndarray = field(default_factory=lambda: np.array([0.0, 33.0, 66.0, 100.0]))
+
+    def n_samples(self) -> int:
+        return int(round(self.sample_rate * self.T))
+
+    def n_stations(self) -> int:
+        return len(self.stations)
+
+    def tau_max(self) -> float:
+        return self.x_max / self.v
+
+    def _c(self):
+        return _ModelC(self.lambda_rate, self.T, self.x_max, self.v, self.sigma_arrival,
+                       self.t_s, self.var_noise, self.var_event, self.sample_rate)
+
+
+@dataclass
+class SamplerConfig:
+    """reference SamplerConfig (samplers.hpp:47-58) for the chromatic drivers."""
+    algorithm: str = "chromatic-static"
+    steps_per_epoch: int = 500
+    epochs: int = 100
+    n_regions: int = 4
+    seed: int = 1
+    burn_in_fraction: float = 0.5
+    record_every: int = 1000
+    weights: tuple = (0.2, 0.2, 0.3, 0.2, 0.1)
+    step_location_x: float = 4.0
+    step_location_t: float = 4.0
+    step_arrival: float = 1.0
+    step_joint: float = 1.0
+    record_log_joint: bool = False
+
+    def _c(self):
+        if self.algorithm not in ("chromatic-static", "chromatic-dynamic"):
+            raise ValueError(f"unknown sampler '{self.algorithm}' (this engine runs "
+                             "chromatic-static or chromatic-dynamic)")
+        return _SamplerC(self.steps_per_epoch, self.epochs, self.n_regions, self.seed,
+                         self.burn_in_fraction, self.record_every, (f64 * 5)(*self.weights),
+                         self.step_location_x, self.step_location_t, self.step_arrival,
+                         self.step_joint, int(self.algorithm == "chromatic-dynamic"),
+                         int(self.record_log_joint))
+
+
+@dataclass
+class Events:
+    """an event set (reference Event, model.hpp:44-53) as arrays."""
+    ids: np.ndarray
+    x: np.ndarray
+    t: np.ndarray
+    arrivals: np.ndarray | None  # [N, S]
+
+    @property
+    def N(self) -> int:
+        return len(self.ids)
+
+
+@dataclass
+class Trace:
+    """reference Trace (samplers.hpp:97-103) + engine measurement counters."""
+    row_step: np.ndarray
+    row_log_joint: np.ndarray
+    row_count: np.ndarray
+    total_steps: int
+    total_accepted: int
+    stats: dict
+    final: Events | None = None
+    step_out: np.ndarray | None = None
+
+
+@dataclass
+class Partition:
+    """reference Partition after color_partition (partition.hpp:16-38)."""
+    boundaries: np.ndarray
+    colors: np.ndarray
+    n_colors: int
+
+    def n_regions(self) -> int:
+        return len(self.boundaries) - 1
+
+    def region_of(self, t):
+        return assign_regions(self.boundaries, t)
+
+
+def partition(T: float, l: float, offset: float, tau: float) -> Partition:
+    """build_partition(T, l, offset) + color_partition(., tau), on the GPU."""
+    L = load_library()
+    cap = int(T / l) + 16
+    b = np.zeros(cap)
+    c = np.zeros(cap, np.int32)
+    nr = i64(0)
+    nc = i32(0)
+    _check(L.seis_partition(T, l, offset, tau, cap, C.byref(nr), _p(b), _p(c), C.byref(nc)), L)
+    k = nr.value
+    return Partition(b[:k + 1].copy(), c[:k].copy(), nc.value)
+
+
+def assign_regions(boundaries, t) -> np.ndarray:
+    """Partition::region_of for every t, on the GPU."""
+    L = load_library()
+    b = np.ascontiguousarray(boundaries, np.float64)
+    t = np.ascontiguousarray(np.atleast_1d(t), np.float64)
+    out = np.zeros(len(t), np.int64)
+    _check(L.seis_assign_regions(_p(b), len(b) - 1, len(t), _p(t), _p(out)), L)
+    return out
+
+
+def partition_offset(seed: int, epoch: int, l: float) -> float:
+    """dynamic-partition offset of `epoch` (samplers.hpp:488-491), on the GPU."""
+    L = load_library()
+    u = f64(0)
+    _check(L.seis_partition_offset(seed, epoch, l, C.byref(u)), L)
+    return u.value
+
+
+def sample_world(config: ModelConfig, seed: int, dtype=F64, threads: int = 0,
+                 cap: int = 1 << 20):
+    """reference sample_world (worldgen.hpp:20-53): (Events, signals [S][n])."""
+    L = load_library()
+    threads = threads or os.cpu_count() or 1
+    S, n = config.n_stations(), config.n_samples()
+    lam = config.lambda_rate * config.T
+    cap = int(min(cap, lam + 20 * np.sqrt(lam) + 64))
+    st = np.ascontiguousarray(config.stations, np.float64)
+    ids = np.zeros(cap, np.uint64)
+    x = np.zeros(cap)
+    t = np.zeros(cap)
+    arr = np.zeros((cap, S))
+    sig = np.zeros((S, n), np.float64 if dtype == F64 else np.float32)
+    N = i64(0)
+    m = config._c()
+    rc = L.seis_world_generate(C.byref(m), _p(st), S, seed, cap, C.byref(N), _p(ids), _p(x),
+                               _p(t), _p(arr), _p(sig), dtype, threads)
+    if rc:
+        raise RuntimeError(L.seis_world_last_error().decode())
+    k = N.value
+    return Events(ids[:k].copy(), x[:k].copy(), t[:k].copy(), arr[:k].copy()), sig
+
+
+def make_world_with_events(config: ModelConfig, cx, ct, seed: int, dtype=F64, threads: int = 0):
+    """reference make_world_with_events (worldgen.hpp:57-86)."""
+    L = load_library()
+    threads = threads or os.cpu_count() or 1
+    S, n = config.n_stations(), config.n_samples()
+    cx = np.ascontiguousarray(cx, np.float64)
+    ct = np.ascontiguousarray(ct, np.float64)
+    N = len(cx)
+    st = np.ascontiguousarray(config.stations, np.float64)
+    arr = np.zeros((max(N, 1), S))
+    sig = np.zeros((S, n), np.float64 if dtype == F64 else np.float32)
+    m = config._c()
+    rc = L.seis_world_with_events(C.byref(m), _p(st), S, N, _p(cx), _p(ct), seed, _p(arr),
+                                  _p(sig), dtype, threads)
+    if rc:
+        raise RuntimeError(L.seis_world_last_error().decode())
+    return Events(np.arange(N, dtype=np.uint64), cx.copy(), ct.copy(), arr[:N].copy()), sig
+
+
+def thomas_events(seed, x_max, T, parent_mean, child_mean, sx, st, cap=1 << 22):
+    L = load_library()
+    cx = np.zeros(cap)
+    ct = np.zeros(cap)
+    n = i64(0)
+    rc = L.seis_thomas_events(seed, x_max, T, parent_mean, child_mean, sx, st, cap, C.byref(n),
+                              _p(cx), _p(ct))
+    if rc:
+        raise RuntimeError(L.seis_world_last_error().decode())
+    return cx[:n.value].copy(), ct[:n.value].copy()
+
+
+class Engine:
+    """World{config, events, signals} resident on one B200 (seis_engine)."""
+
+    def __init__(self, config: ModelConfig, signals: np.ndarray, event_capacity: int = 4096):
+        self.L = load_library()
+        self.config = config
+        sig = np.ascontiguousarray(signals)
+        if sig.dtype == np.float64:
+            self.dtype = F64
+        elif sig.dtype == np.float32:
+            self.dtype = F32
+        else:
+            raise ValueError("signals must be float32 or float64")
+        if sig.shape != (config.n_stations(), config.n_samples()):
+            raise ValueError(f"signals must be [S={config.n_stations()}][n={config.n_samples()}]")
+        st = np.ascontiguousarray(config.stations, np.float64)
+        h = P()
+        m = config._c()
+        _check(self.L.seis_engine_create(C.byref(m), _p(st), len(st), _p(sig), self.dtype,
+                                         event_capacity, C.byref(h)), self.L)
+        self.h = h
+        self.capacity = event_capacity
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.seis_engine_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+    def upload_signals(self, signals: np.ndarray):
+        sig = np.ascontiguousarray(signals, np.float64 if self.dtype == F64 else np.float32)
+        _check(self.L.seis_upload_signals(self.h, _p(sig)), self.L)
+
+    def set_hypothesis(self, ev: Events):
+        S = self.config.n_stations()
+        ids = np.ascontiguousarray(ev.ids, np.uint64)
+        x = np.ascontiguousarray(ev.x, np.float64)
+        t = np.ascontiguousarray(ev.t, np.float64)
+        a = np.ascontiguousarray(ev.arrivals, np.float64).reshape(len(ids), S)
+        _check(self.L.seis_set_hypothesis(self.h, len(ids), _p(ids), _p(x), _p(t), _p(a)),
+               self.L)
+
+    def get_hypothesis(self, arrivals: bool = True) -> Events:
+        n = i64(0)
+        _check(self.L.seis_get_hypothesis(self.h, 0, C.byref(n), None, None, None, None), self.L)
+        N = n.value
+        S = self.config.n_stations()
+        ids = np.zeros(max(N, 1), np.uint64)
+        x = np.zeros(max(N, 1))
+        t = np.zeros(max(N, 1))
+        a = np.zeros((max(N, 1), S)) if arrivals else None
+        _check(self.L.seis_get_hypothesis(self.h, N, C.byref(n), _p(ids), _p(x), _p(t),
+                                          _p(a) if arrivals else None), self.L)
+        return Events(ids[:N], x[:N], t[:N], a[:N] if arrivals else None)
+
+    def log_joint(self) -> float:
+        out = f64(0)
+        _check(self.L.seis_log_joint(self.h, C.byref(out)), self.L)
+        return out.value
+
+    def delta_log_joint(self, changes: list, window=None, support=None) -> np.ndarray:
+        """Batched delta_log_joint against the resident hypothesis.
+
+        Each change is (removed_ids, added) with added a list of
+        (x, t, arrivals[S]) tuples.
+        """
+        S = self.config.n_stations()
+        n = self.config.n_samples()
+        wlo, whi = window if window is not None else (0, n)
+        slo, shi, sc = support if support is not None else (0.0, self.config.T, 1)
+        arr_rows = []
+        cs = (_ChangeC * max(len(changes), 1))()
+        for i, (rem, add) in enumerate(changes):
+            c = cs[i]
+            c.n_removed = len(rem)
+            c.n_added = len(add)
+            for q, rid in enumerate(rem):
+                c.removed_id[q] = int(rid)
+            for q, (ax, at, aa) in enumerate(add):
+                c.added_x[q] = ax
+                c.added_t[q] = at
+                c.added_row[q] = len(arr_rows)
+                arr_rows.append(np.asarray(aa, np.float64).reshape(S))
+            c.window_lo, c.window_hi = wlo, whi
+            c.support_lo, c.support_hi, c.support_closed = slo, shi, sc
+        rows = np.ascontiguousarray(np.stack(arr_rows) if arr_rows else np.zeros((0, S)))
+        out = np.zeros(len(changes))
+        _check(self.L.seis_score_batch(self.h, len(changes), C.cast(cs, P), _p(rows),
+                                       len(arr_rows), _p(out)), self.L)
+        return out
+
+    def run_chromatic(self, sc: SamplerConfig, tape: np.ndarray | None = None,
+                      tape_arrivals: np.ndarray | None = None, row_cap: int = 1 << 16,
+                      final: bool = True) -> Trace:
+        """run_chromatic (samplers.hpp:401-498) from the resident hypothesis.
+
+        Without `tape`: production mode (philox stream spec v1). With `tape`
+        (oracle TAPE_DTYPE records in driver order): replay mode, returning the
+        engine's per-step delta / log_r / decision in Trace.step_out.
+        """
+        s = sc._c()
+        mode = 0
+        n_tape = 0
+        tarr = None
+        out = None
+        if tape is not None:
+            mode = 1
+            tape = np.ascontiguousarray(tape, TAPE_DTYPE)
+            n_tape = len(tape)
+            tarr = np.ascontiguousarray(tape_arrivals if tape_arrivals is not None
+                                        else np.zeros(1), np.float64)
+            out = np.zeros(n_tape, STEP_OUT_DTYPE)
+        rs = np.zeros(row_cap, np.int64)
+        rl = np.zeros(row_cap)
+        rc = np.zeros(row_cap, np.int64)
+        st = _StatsC()
+        _check(self.L.seis_run_chromatic(self.h, C.byref(s), mode, _p(tape), n_tape, _p(tarr),
+                                         0 if tarr is None else len(tarr), _p(out), row_cap,
+                                         _p(rs), _p(rl), _p(rc), C.byref(st)), self.L)
+        nr = min(st.n_rows, row_cap)
+        stats = {f: getattr(st, f) for f, _ in _StatsC._fields_}
+        tr = Trace(rs[:nr], rl[:nr], rc[:nr], st.total_steps, st.total_accepted, stats,
+                   step_out=out)
+        if final:
+            tr.final = self.get_hypothesis()
+        return tr
+
+
+def run_sampler(config: ModelConfig, signals: np.ndarray, sc: SamplerConfig,
+                event_capacity: int = 4096) -> Trace:
+    """reference run_sampler (samplers.hpp:500-509) for the chromatic algorithms:
+    from the empty hypothesis, through the C-ABI with host buffers."""
+    eng = Engine(config, signals, event_capacity)
+    try:
+        return eng.run_chromatic(sc)
+    finally:
+        eng.close()

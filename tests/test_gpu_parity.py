@@ -1,0 +1,260 @@
+"""GPU parity: the B200 engine (through its C-ABI) against the reference's
+golden vectors and the CPU oracle on the same seeded inputs.
+
+Bars (BASELINE.json north_star): region assignment, coloring and replay
+accept/reject decisions bit-exact except where |log alpha - log u| < 1e-9;
+per-proposal deltas within 1e-5 relative (asserted here much tighter, 1e-9);
+production trajectories identical to the oracle's philox-spec replay.
+"""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from tests.helpers import (default_model, engine_model, engine_sampler, golden, golden_world,
+                           tape_sampler, wide_model)
+
+pytestmark = pytest.mark.gpu
+
+TIE = 1e-9
+DTOL = 1e-9
+
+
+@pytest.fixture(scope="module")
+def E(built):
+    import paper_1612_00595_b200 as E
+    return E
+
+
+@pytest.fixture(scope="module")
+def oc(built):
+    return O.Oracle("c")
+
+
+def close(a, b, tol=DTOL):
+    if np.isinf(a) or np.isinf(b):
+        return a == b
+    return abs(a - b) <= tol * max(1.0, abs(b))
+
+
+# ------------------------------------------------------------------ partition
+def test_partition_bit_exact(E):
+    g = golden("partition.npz")
+    for i, (T, l, u, tau) in enumerate(g["cases"]):
+        if g["rc"][i]:
+            with pytest.raises(ValueError):
+                E.partition(T, l, u, tau)
+            continue
+        p = E.partition(T, l, u, tau)
+        assert np.array_equal(p.boundaries, g[f"b{i}"]), i
+        assert np.array_equal(p.colors, g[f"c{i}"]) and p.n_colors == g["k"][i]
+
+
+def test_region_of_bit_exact(E):
+    g = golden("partition.npz")
+    for i in range(len(g["rc"])):
+        if g["rc"][i] or len(g[f"probe{i}"]) == 0:
+            continue
+        got = E.assign_regions(g[f"b{i}"], g[f"probe{i}"])
+        assert np.array_equal(got, g[f"reg{i}"]), i
+
+
+def test_partition_offsets(E):
+    g = golden("rng.npz")
+    for r, (seed, l) in enumerate([(0, 60.0), (1, 14.0625), (123456789, 0.87890625)]):
+        got = [E.partition_offset(seed, ep, l) for ep in range(1, 20)]
+        assert np.array_equal(got, g["offsets"][r])
+
+
+# ------------------------------------------------------------------ delta
+def _golden_changes(m):
+    g = golden("deltas.npz")
+    w = golden_world("wide", m)
+    out = []
+    for i in range(len(g["delta"])):
+        rem = [int(w.events.ids[g["rem"][i]])] if g["n_rem"][i] else []
+        add = [(g["add_x"][i], g["add_t"][i], g["add_arr"][i])] if g["n_add"][i] else []
+        out.append((rem, add))
+    return w, out, g["delta"]
+
+
+def test_score_batch_matches_reference_fp64(E):
+    m = wide_model()
+    w, changes, ref = _golden_changes(m)
+    eng = E.Engine(engine_model(m), w.signals, event_capacity=256)
+    eng.set_hypothesis(E.Events(w.events.ids, w.events.x, w.events.t, w.events.arr))
+    got = eng.delta_log_joint(changes)
+    bad = [(i, got[i], ref[i]) for i in range(len(ref)) if not close(got[i], ref[i])]
+    assert not bad, bad[:5]
+    assert close(eng.log_joint(), golden("deltas.npz")["log_joint"][0], 1e-12)
+
+
+def test_score_batch_fp32_signals_vs_oracle(E, oc):
+    m = wide_model()
+    w, changes, _ = _golden_changes(m)
+    sig32 = w.signals.astype(np.float32)
+    eng = E.Engine(engine_model(m), sig32, event_capacity=256)
+    eng.set_hypothesis(E.Events(w.events.ids, w.events.x, w.events.t, w.events.arr))
+    got = eng.delta_log_joint(changes)
+    sig = sig32.astype(np.float64)  # identical inputs: the widened fp32 values
+    idx = {int(v): i for i, v in enumerate(w.events.ids)}
+    for i, (rem, add) in enumerate(changes):
+        a = None
+        if add:
+            a = O.Events(np.array([7], np.uint64), np.array([add[0][0]]), np.array([add[0][1]]),
+                         np.array(add[0][2])[None, :])
+        ref = oc.delta(m, sig, w.events, [idx[r] for r in rem], a)
+        assert close(got[i], ref), (i, got[i], ref)
+
+
+def test_score_batch_restricted_window_and_support(E, oc):
+    m = wide_model()
+    w, changes, _ = _golden_changes(m)
+    eng = E.Engine(engine_model(m), w.signals, event_capacity=256)
+    eng.set_hypothesis(E.Events(w.events.ids, w.events.x, w.events.t, w.events.arr))
+    idx = {int(v): i for i, v in enumerate(w.events.ids)}
+    win, sup = (100, 500), (50.0, 400.0, 0)  # naive-mode style ScoreOptions
+    got = eng.delta_log_joint(changes[:80], window=win, support=sup)
+    for i, (rem, add) in enumerate(changes[:80]):
+        a = None
+        if add:
+            a = O.Events(np.array([7], np.uint64), np.array([add[0][0]]), np.array([add[0][1]]),
+                         np.array(add[0][2])[None, :])
+        ref = oc.delta(m, w.signals, w.events, [idx[r] for r in rem], a, window=win, support=sup)
+        assert close(got[i], ref), (i, got[i], ref)
+
+
+def test_score_batch_empty_world_and_unknown_id(E):
+    m = default_model()
+    g = golden_world("w0", m)
+    eng = E.Engine(engine_model(m), g.signals)
+    d = eng.delta_log_joint([([], [(10.0, 30.0, 30.0 + np.abs(10.0 - m.stations) / m.v)])])
+    assert np.isfinite(d[0])
+    with pytest.raises(ValueError):
+        eng.delta_log_joint([([12345], [])])
+
+
+# ------------------------------------------------------------------ replay
+def _replay_check(E, world, model, tape, tape_arr, sampler, final, dtype=np.float64):
+    eng = E.Engine(engine_model(model), world.signals.astype(dtype), event_capacity=512)
+    tr = eng.run_chromatic(engine_sampler(sampler), tape=tape, tape_arrivals=tape_arr)
+    out = tr.step_out
+    scored = tape["scored"] == 1
+    assert np.array_equal(out["scored"], tape["scored"])
+    # decisions: bit-exact except near ties |log alpha - log u| < 1e-9
+    lr = tape["log_r"]
+    tie = np.zeros(len(tape), bool)
+    drawn = tape["u_drawn"] == 1
+    tie[drawn] = np.abs(lr[drawn] - np.log(tape["u"][drawn])) < TIE
+    tie |= scored & (np.abs(lr) < TIE)
+    mism = (out["accepted"] != tape["accepted"]) & ~tie
+    assert not mism.any(), np.where(mism)[0][:10]
+    for i in np.where(scored)[0]:
+        assert close(out["delta"][i], tape["delta"][i]), (i, out["delta"][i], tape["delta"][i])
+        assert close(out["log_r"][i], tape["log_r"][i]), i
+    fin = tr.final
+    assert np.array_equal(fin.ids, final["ids"])
+    assert np.array_equal(fin.x, final["x"]) and np.array_equal(fin.t, final["t"])
+    assert np.array_equal(fin.arrivals, final["arr"])
+    return tr
+
+
+@pytest.mark.parametrize("name", ["default_static", "default_dynamic", "wide_dynamic"])
+def test_replay_golden_tapes(E, name):
+    g = golden(f"tape_{name}.npz")
+    s = tape_sampler(g["sampler"])
+    if name.startswith("default"):
+        m = default_model()
+        w = golden_world("w1" if "static" in name else "w2", m)
+    else:
+        m = wide_model()
+        w = golden_world("wide", m)
+    _replay_check(E, w, m, g["tape"], g["tape_arr"], s,
+                  dict(ids=g["final_ids"], x=g["final_x"], t=g["final_t"], arr=g["final_arr"]))
+
+
+def _mapped_model(S, T, n_regions, x_max, lam_events):
+    # SURVEY §8(d) mapping: l / tau = 1.2
+    v = 1.2 * x_max * n_regions / T
+    return O.Model(lambda_rate=lam_events / T, T=T, x_max=x_max, v=v,
+                   stations=O.stations_line(S, x_max))
+
+
+def test_replay_fp32_mapped_world(E, oc):
+    # a config[1]-shaped slice small enough for the O(S N) oracle: fp32 signals,
+    # overlapping same-color windows (tau + t_s > l) exercise the frozen snapshot
+    m = _mapped_model(S=96, T=600.0, n_regions=40, x_max=4000.0, lam_events=60)
+    w = oc.sample_world(m, 3)
+    w32 = O.World(m, w.events, w.signals.astype(np.float32).astype(np.float64))
+    s = O.Sampler(steps_per_epoch=16, epochs=3, n_regions=40, seed=9, dynamic=1)
+    r = oc.run_chromatic(w32, s, init=w.events, tape=True)
+    eng = E.Engine(engine_model(m), w32.signals.astype(np.float32), event_capacity=1024)
+    eng.set_hypothesis(E.Events(w.events.ids, w.events.x, w.events.t, w.events.arr))
+    tr = eng.run_chromatic(engine_sampler(s), tape=r["tape"], tape_arrivals=r["tape_arr"])
+    t = r["tape"]
+    drawn = t["u_drawn"] == 1
+    tie = np.zeros(len(t), bool)
+    tie[drawn] = np.abs(t["log_r"][drawn] - np.log(t["u"][drawn])) < TIE
+    assert not ((tr.step_out["accepted"] != t["accepted"]) & ~tie).any()
+    sc = t["scored"] == 1
+    assert np.allclose(tr.step_out["delta"][sc], t["delta"][sc], rtol=1e-11, atol=1e-9)
+    assert np.array_equal(tr.final.ids, r["final"].ids)
+    assert np.array_equal(tr.final.arrivals, r["final"].arr)
+
+
+# ------------------------------------------------------------------ production
+def _prod_vs_oracle(E, oc, m, w, s, init=None, dtype=np.float64, rowlj=False):
+    ro = oc.run_chromatic(w, s, init=init, tape=False, rowlj=rowlj)
+    eng = E.Engine(engine_model(m), w.signals.astype(dtype), event_capacity=2048)
+    if init is not None:
+        eng.set_hypothesis(E.Events(init.ids, init.x, init.t, init.arr))
+    tr = eng.run_chromatic(engine_sampler(s, record_log_joint=rowlj))
+    assert tr.total_steps == ro["total_steps"]
+    assert tr.total_accepted == ro["total_accepted"]
+    assert np.array_equal(tr.final.ids, ro["final"].ids)
+    assert np.array_equal(tr.final.x, ro["final"].x)
+    assert np.array_equal(tr.final.t, ro["final"].t)
+    assert np.array_equal(tr.final.arrivals, ro["final"].arr)
+    assert np.array_equal(tr.row_step, ro["row_step"])
+    assert np.array_equal(tr.row_count, ro["row_count"])
+    if rowlj:
+        assert np.allclose(tr.row_log_joint, ro["row_lj"], rtol=1e-12, atol=1e-8)
+    return tr, ro
+
+
+@pytest.mark.parametrize("dyn", [0, 1])
+def test_production_matches_oracle_philox_default(E, oc, dyn):
+    m = default_model()
+    w = golden_world("w3", m)
+    s = O.Sampler(steps_per_epoch=100, epochs=12, n_regions=4, seed=17, dynamic=dyn,
+                  rng_mode=1, record_every=400)
+    _prod_vs_oracle(E, oc, m, w, s, rowlj=True)
+
+
+def test_production_matches_oracle_philox_mapped_fp32(E, oc):
+    m = _mapped_model(S=96, T=600.0, n_regions=40, x_max=4000.0, lam_events=60)
+    w = oc.sample_world(m, 4)
+    w32 = O.World(m, w.events, w.signals.astype(np.float32).astype(np.float64))
+    s = O.Sampler(steps_per_epoch=16, epochs=4, n_regions=40, seed=3, dynamic=1, rng_mode=1)
+    _prod_vs_oracle(E, oc, m, w32, s, init=w.events, dtype=np.float32)
+
+
+def test_production_from_empty_three_colors(E, oc):
+    # l in [tau/2, tau): three colors (partition.hpp:68-71)
+    m = O.Model(lambda_rate=0.03, T=300.0, x_max=100.0, v=2.0 * 1.5, stations=O.stations_line(8, 100.0))
+    w = oc.sample_world(m, 8)
+    s = O.Sampler(steps_per_epoch=60, epochs=6, n_regions=12, seed=5, dynamic=1, rng_mode=1)
+    _prod_vs_oracle(E, oc, m, w, s)
+
+
+def test_sampler_validation_errors(E):
+    m = default_model()
+    g = golden_world("w0", m)
+    eng = E.Engine(engine_model(m), g.signals)
+    with pytest.raises(ValueError):
+        eng.run_chromatic(E.SamplerConfig(steps_per_epoch=0))
+    with pytest.raises(ValueError):
+        eng.run_chromatic(E.SamplerConfig(weights=(0.5, 0.5, 0.5, 0.0, 0.0)))
+    with pytest.raises(ValueError):  # l < tau / 2
+        eng.run_chromatic(E.SamplerConfig(n_regions=12))
+    with pytest.raises(ValueError):
+        E.Engine(engine_model(O.Model(var_event=0.5)), g.signals)

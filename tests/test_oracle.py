@@ -1,0 +1,172 @@
+"""CPU: the plain-C oracle restatement against the reference's golden vectors
+(tests/golden/, generated from the reference compiled in place) and, when the
+reference tree is present, against oracle/_ref directly."""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from tests.helpers import default_model, golden, golden_world, tape_sampler, wide_model
+
+
+@pytest.fixture(scope="module")
+def oc(built):
+    return O.Oracle("c")
+
+
+def test_partition_kats_and_grid(oc):
+    g = golden("partition.npz")
+    for i, (T, l, u, tau) in enumerate(g["cases"]):
+        rc, msg, b, c, k = oc.partition(T, l, u, tau)
+        assert rc == g["rc"][i], (i, msg)
+        if rc:
+            continue
+        assert np.array_equal(b, g[f"b{i}"])  # bit-exact boundaries (b += l recurrence)
+        assert np.array_equal(c, g[f"c{i}"]) and k == g["k"][i]
+        regs = [oc.region_of(b, p) for p in g[f"probe{i}"]]
+        assert np.array_equal(regs, g[f"reg{i}"])
+
+
+def test_partition_reference_kats(oc):
+    # proj/tests/test_partition.cpp:11-59
+    rc, _, b, c, k = oc.partition(240, 60, 0, 50)
+    assert list(b) == [0, 60, 120, 180, 240] and list(c) == [0, 1, 0, 1] and k == 2
+    rc, _, b, c, k = oc.partition(240, 60, 25, 50)
+    assert np.allclose(b, [0, 25, 85, 145, 205, 240])
+    rc, _, b, c, k = oc.partition(240, 30, 0, 50)
+    assert k == 3 and list(c) == [i % 3 for i in range(8)]
+    assert oc.partition(240, 20, 0, 50)[0] == 2
+    for bad in [(240, 0, 0, 50), (240, 300, 0, 50), (240, 60, 60, 50), (240, 60, -1, 50)]:
+        assert oc.partition(*bad)[0] == 2
+
+
+def test_offsets(oc):
+    g = golden("rng.npz")
+    for r, (seed, l) in enumerate([(0, 60.0), (1, 14.0625), (123456789, 0.87890625)]):
+        got = [oc.partition_offset(seed, ep, l) for ep in range(1, 20)]
+        assert np.array_equal(got, g["offsets"][r])
+
+
+def test_worldgen_bit_exact(oc):
+    m = default_model()
+    for seed in range(4):
+        w = oc.sample_world(m, seed)
+        gw = golden_world(f"w{seed}", m)
+        assert np.array_equal(w.signals, gw.signals)
+        assert np.array_equal(w.events.arr, gw.events.arr)
+        assert np.array_equal(w.events.x, gw.events.x) and np.array_equal(w.events.t, gw.events.t)
+    mw = wide_model()
+    w = oc.sample_world(mw, 5)
+    gw = golden_world("wide", mw)
+    assert np.array_equal(w.signals, gw.signals)
+    p = oc.make_world_with_events(m, [20.0, 80.0, 50.0], [30.0, 100.0, 190.0], 9)
+    gp = golden_world("planted", m)
+    assert np.array_equal(p.signals, gp.signals) and np.array_equal(p.events.arr, gp.events.arr)
+
+
+def _golden_changes():
+    g = golden("deltas.npz")
+    for i in range(len(g["delta"])):
+        rem = [int(g["rem"][i])] if g["n_rem"][i] else []
+        add = None
+        if g["n_add"][i]:
+            add = O.Events(np.array([g["add_id"][i]], np.uint64), np.array([g["add_x"][i]]),
+                           np.array([g["add_t"][i]]), g["add_arr"][i][None, :])
+        yield rem, add, g["delta"][i]
+
+
+def test_delta_matches_reference_bits(oc):
+    mw = wide_model()
+    w = golden_world("wide", mw)
+    for rem, add, d in _golden_changes():
+        got = oc.delta(mw, w.signals, w.events, rem, add)
+        assert got == d or (np.isinf(got) and np.isinf(d))
+    assert oc.log_joint(mw, w.signals, w.events) == golden("deltas.npz")["log_joint"][0]
+
+
+def test_delta_equals_full_recompute(oc):
+    # proj/tests/test_model.cpp:309-348: delta vs log_joint(after) - log_joint(before)
+    mw = wide_model()
+    w = golden_world("wide", mw)
+    base = oc.log_joint(mw, w.signals, w.events)
+    n = 0
+    for rem, add, d in _golden_changes():
+        keep = [i for i in range(w.events.N) if i not in rem]
+        ev = w.events
+        ids = np.concatenate([ev.ids[keep], add.ids if add else np.zeros(0, np.uint64)])
+        x = np.concatenate([ev.x[keep], add.x if add else []])
+        t = np.concatenate([ev.t[keep], add.t if add else []])
+        arr = np.concatenate([ev.arr[keep], add.arr if add else np.zeros((0, mw.S))])
+        after = oc.log_joint(mw, w.signals, O.Events(ids, x, t, arr))
+        if np.isinf(d):
+            assert np.isinf(after)
+        else:
+            assert abs((after - base) - d) < 1e-8
+        n += 1
+        if n >= 60:
+            break
+
+
+@pytest.mark.parametrize("name", ["default_static", "default_dynamic", "wide_dynamic"])
+def test_chromatic_tape_matches_reference(oc, name):
+    g = golden(f"tape_{name}.npz")
+    s = tape_sampler(g["sampler"])
+    if name.startswith("default"):
+        m = default_model()
+        w = golden_world("w1" if "static" in name else "w2", m)
+    else:
+        m = wide_model()
+        w = golden_world("wide", m)
+    r = oc.run_chromatic(w, s, tape=True, rowlj=True)
+    assert r["tape"].tobytes() == g["tape"].tobytes()
+    assert np.array_equal(r["tape_arr"], g["tape_arr"])
+    assert np.array_equal(r["final"].ids, g["final_ids"])
+    assert np.array_equal(r["final"].arr, g["final_arr"])
+    assert np.array_equal(r["row_lj"], g["row_lj"])
+    assert r["total_accepted"] == int(g["total_accepted"])
+
+
+@pytest.mark.skipif(not O.have_ref(), reason="reference tree absent")
+def test_composed_driver_equals_reference_run_sampler(built):
+    # the shim's tape driver == the reference's own run_sampler (workers 1 and 4)
+    R = O.Oracle("ref")
+    m = default_model()
+    w = R.sample_world(m, 11)
+    for dyn in (0, 1):
+        s = O.Sampler(steps_per_epoch=50, epochs=8, n_regions=4, seed=21, dynamic=dyn,
+                      burn_in_fraction=0.0)
+        a = R.run_chromatic(w, s, tape=False)
+        for workers in (1, 4):
+            b = O.ref_run_sampler(w, s, workers=workers)
+            assert np.array_equal(a["final"].ids, b["final"].ids)
+            assert np.array_equal(a["final"].arr, b["final"].arr)
+            assert a["total_accepted"] == b["total_accepted"]
+
+
+@pytest.mark.skipif(not O.have_ref(), reason="reference tree absent")
+def test_oracle_vs_reference_random_worlds(built, oc):
+    R = O.Oracle("ref")
+    for seed in range(3):
+        m = O.Model(lambda_rate=0.05, T=120.0, stations=O.stations_line(6, 100.0))
+        a = oc.sample_world(m, 100 + seed)
+        b = R.sample_world(m, 100 + seed)
+        assert np.array_equal(a.signals, b.signals)
+        s = O.Sampler(steps_per_epoch=40, epochs=5, n_regions=2, seed=seed, dynamic=seed % 2)
+        ra = oc.run_chromatic(a, s)
+        rb = R.run_chromatic(b, s)
+        assert ra["tape"].tobytes() == rb["tape"].tobytes()
+
+
+def test_philox_known_answers(built):
+    # Random123 kat_vectors for philox4x32_10
+    assert O.philox((0, 0, 0, 0), (0, 0)) == [0x6627E8D5, 0xE169C58D, 0xBC57AC4C, 0x9B00DBD8]
+    f = 0xFFFFFFFF
+    assert O.philox((f, f, f, f), (f, f)) == [0x408F276D, 0x41C83B0E, 0xA20BC7C6, 0x6D5451FD]
+    assert O.philox((0x243F6A88, 0x85A308D3, 0x13198A2E, 0x03707344),
+                    (0xA4093822, 0x299F31D0)) == [0xD16CFE09, 0x94FDCCEB, 0x5001E420, 0x24126EA1]
+
+
+def test_philox_normals_are_standard(built):
+    z = np.array([O.philox_normal(7, 3, r, s, i) for r in range(10) for s in range(20)
+                  for i in range(25)])
+    assert abs(z.mean()) < 0.05 and abs(z.std() - 1) < 0.05
+    assert abs(np.mean(z ** 4) - 3) < 0.3
