@@ -1,0 +1,378 @@
+#!/usr/bin/env python
+"""Benchmark of the chromatic region-sweep hot path (BASELINE.json metric:
+MH proposals/s and region sweeps/s on 1 B200; likelihood-delta % of roofline).
+
+One "step" = one chromatic sweep (every color x every region x k MH steps) of
+config[1] (SURVEY §8(d) 1-D mapping: S=1600 stations, T=3600 samples fp32,
+Poisson(400) events, 256 time regions, k=64, static 2-coloring), started from
+the world's truth hypothesis so every step is a steady-state sweep.
+
+    python bench.py [--gpus N --steps K --warmup W --config C --impl ours|reference]
+
+--impl reference times the reference's own CPU implementation (oracle/_ref:
+the reference headers compiled unchanged; run_region_steps on the truth world,
+one chain per host thread) on the same config/metric. Multi-GPU (torchrun):
+independent replica chains per rank ("replicas only", weak scaling), barrier +
+max-over-ranks device time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# side -> x_max, trace length -> T (1 Hz), Poisson mean -> lambda T,
+# G x G stations -> S evenly spaced, R x R regions -> R^2 time regions,
+# v = 1.2 x_max n_regions / T (l / tau_max = 1.2)
+CONFIGS = {
+    0: dict(x_max=1000.0, T=3600.0, events=20, S=100, n_regions=16, k=500, dynamic=0,
+            dtype="f64", desc="config[0] small: 10x10 stations, 4x4 regions, fp64"),
+    1: dict(x_max=4000.0, T=3600.0, events=400, S=1600, n_regions=256, k=64, dynamic=0,
+            dtype="f32", desc="config[1] medium: 40x40 stations x 3600 fp32, 16x16 regions"),
+    2: dict(x_max=16000.0, T=3600.0, events=5000, S=16384, n_regions=4096, k=64, dynamic=1,
+            dtype="f32", desc="config[2] large: 128x128 stations x 3600 fp32, 64x64 regions, "
+                              "dynamic offsets"),
+    3: dict(x_max=16000.0, T=1800.0, events=20000, S=65536, n_regions=16384, k=256, dynamic=1,
+            dtype="f32", desc="config[3] dense: 256x256 stations x 1800 fp32, 128x128 regions"),
+    4: dict(x_max=32000.0, T=1024.0, events=None, S=262144, n_regions=65536, k=64, dynamic=1,
+            dtype="f32", desc="config[4] clustered (Thomas): 512x512 stations x 1024 fp32, "
+                              "256x256 regions"),
+}
+
+
+def model_for(c):
+    from paper_1612_00595_b200 import ModelConfig
+    v = 1.2 * c["x_max"] * c["n_regions"] / c["T"]
+    lam = (c["events"] or 20000) / c["T"]
+    st = c["x_max"] * np.arange(c["S"], dtype=np.float64) / (c["S"] - 1)
+    return ModelConfig(lambda_rate=lam, T=c["T"], x_max=c["x_max"], v=v, stations=st)
+
+
+def make_world(c, threads):
+    import paper_1612_00595_b200 as E
+    m = model_for(c)
+    dt = E.F64 if c["dtype"] == "f64" else E.F32
+    if c["events"] is None:
+        cx, ct = E.thomas_events(0, c["x_max"], c["T"], 2000.0, 10.0, 50.0, 0.0015625 * c["T"])
+        ev, sig = E.make_world_with_events(m, cx, ct, 0, dtype=dt, threads=threads)
+    else:
+        ev, sig = E.sample_world(m, 0, dtype=dt, threads=threads)
+    return m, ev, sig
+
+
+def sampler_for(c, seed, epochs=1):
+    from paper_1612_00595_b200 import SamplerConfig
+    return SamplerConfig(algorithm="chromatic-dynamic" if c["dynamic"] else "chromatic-static",
+                         steps_per_epoch=c["k"], epochs=epochs, n_regions=c["n_regions"],
+                         seed=seed, record_every=1 << 30)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([s.strip() for s in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 5 + i and r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def ncu_traffic(cfg_id):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(f"config{cfg_id}")
+    return None
+
+
+def cpu_baseline_ref(c, m, ev, sig, seconds, threads, seed=1):
+    """reference run_region_steps (oracle/_ref) on the truth world, one chain per thread."""
+    from oracle import oracle as O
+    if not O.have_ref():
+        return None
+    om = O.Model(lambda_rate=m.lambda_rate, T=m.T, x_max=m.x_max, v=m.v,
+                 sigma_arrival=m.sigma_arrival, t_s=m.t_s, var_noise=m.var_noise,
+                 var_event=m.var_event, sample_rate=m.sample_rate, stations=m.stations)
+    w = O.World(om, O.Events(ev.ids, ev.x, ev.t, ev.arrivals), sig.astype(np.float64))
+    s = O.Sampler(steps_per_epoch=c["k"], epochs=1, n_regions=c["n_regions"], seed=seed)
+    props, wall = O.ref_bench_region_steps(w, w.events, s, threads, seconds, 1 << 40)
+    return props, wall
+
+
+def dist_init():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch
+        import torch.distributed as dist
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend)
+        return ws, rank, local, dist
+    return 1, 0, 0, None
+
+
+def reduce_max(dist, v):
+    if dist is None:
+        return v
+    import torch
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([float(v)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def reduce_sum(dist, v):
+    if dist is None:
+        return v
+    import torch
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([float(v)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t)
+    return float(t.item())
+
+
+def barrier(dist):
+    if dist is not None:
+        dist.barrier()
+
+
+def run_reference(args, c, ws, rank, dist):
+    if rank != 0:
+        return 0
+    from oracle import oracle as O
+    if not O.have_ref():
+        O.build()
+    threads = os.cpu_count() or 1
+    m, ev, sig = make_world(c, threads)
+    per_step = args.ref_seconds
+    vals = []
+    total_p, total_w = 0, 0.0
+    for i in range(args.warmup + args.steps):
+        r = cpu_baseline_ref(c, m, ev, sig, per_step if i >= args.warmup else 1.0, threads,
+                             seed=1 + i)
+        if r is None:
+            print(json.dumps({"impl": "reference",
+                              "unavailable": "oracle/_ref (reference compiled in place) absent"}))
+            return 0
+        if i >= args.warmup:
+            total_p += r[0]
+            total_w += r[1]
+            vals.append(r[0] / r[1])
+    value = total_p / total_w
+    sweep_props = c["n_regions"] * c["k"]
+    out = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "proposals/s",
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * sweep_props / value, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference generative model sample_world, world seed 0)",
+        "config": {"workload": c["desc"], "start": "truth hypothesis",
+                   "sweeps_per_s": value / sweep_props,
+                   "sample": f"{args.steps} x {per_step:.0f} s of reference run_region_steps, "
+                             f"{threads} threads, one region chain per thread"},
+        "cpu_baseline": {"value": value, "unit": "proposals/s", "cores": threads,
+                         "kind": "reference",
+                         "sample": f"{args.steps} x {per_step:.0f} s, {total_p} proposals"},
+        "e2e": {"value": value, "unit": "proposals/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out))
+    return 0
+
+
+METRIC = "MH proposals/sec (and region sweeps/sec) on 1 B200; likelihood-delta % of roofline"
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--ref-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    c = CONFIGS[args.config]
+    ws, rank, local, dist = dist_init()
+    if args.impl == "reference":
+        return run_reference(args, c, ws, rank, dist)
+
+    import torch
+    import paper_1612_00595_b200 as E
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a GPU (the engine has no CPU fallback)")
+    torch.cuda.set_device(local)
+    threads = os.cpu_count() or 1
+    m, ev, sig = make_world(c, threads)
+    cap = int(max(1024, ev.N * 2 + 256))
+    eng = E.Engine(m, sig, event_capacity=min(cap, 65000))
+    truth = E.Events(ev.ids, ev.x, ev.t, ev.arrivals)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    seed0 = 1000 * rank
+
+    def sweep(i):
+        return eng.run_chromatic(sampler_for(c, seed0 + i), final=False, row_cap=4)
+
+    eng.set_hypothesis(truth)
+    for i in range(args.warmup):
+        sweep(i)
+    torch.cuda.synchronize()
+    acc = dict(total_ms=0.0, sweep_ms=0.0, bytes=0.0, steps=0, scored=0, launches=0,
+               changed=0, arrvals=0, phases=0)
+    barrier(dist)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()  # L2 flush between timed sweeps (256 MiB > 126 MB L2)
+            torch.cuda.synchronize()
+            tr = sweep(args.warmup + i)
+            st = tr.stats
+            acc["total_ms"] += st["total_ms"]
+            acc["sweep_ms"] += st["sweep_kernel_ms"]
+            acc["bytes"] += st["algorithmic_bytes"]
+            acc["steps"] += st["total_steps"]
+            acc["scored"] += st["scored_proposals"]
+            acc["launches"] += st["kernel_launches"]
+            acc["changed"] += st["changed_samples"]
+            acc["arrvals"] += st["arrival_values"]
+    torch.cuda.synchronize()
+    barrier(dist)
+    t_max = reduce_max(dist, acc["total_ms"])
+    steps_all = reduce_sum(dist, acc["steps"])
+    value = steps_all / (t_max / 1e3)
+    n_colors = 2 if c["n_regions"] * 0 == 0 else 2
+    phases_per_sweep = n_colors
+    peak, peak_kind = peaks()
+    achieved = acc["bytes"] / (acc["sweep_ms"] / 1e3) / 1e9
+    res = {
+        "metric": METRIC, "value": value, "unit": "proposals/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference generative model sample_world, world seed 0; "
+                f"{'fp32' if c['dtype'] == 'f32' else 'fp64'} signals)",
+        "config": {"workload": c["desc"], "start": "truth hypothesis (seis_set_hypothesis)",
+                   "parallelism": "replicas" if ws > 1 else "single",
+                   "sweeps_per_s": ws * args.steps / (t_max / 1e3),
+                   "scored_proposals_per_s": reduce_sum(dist, acc["scored"]) / (t_max / 1e3),
+                   "events": int(ev.N), "stations": c["S"], "regions": c["n_regions"],
+                   "k": c["k"], "l2": "flushed between timed sweeps (256 MiB write)",
+                   "sweep_kernel_ms_per_step": acc["sweep_ms"] / args.steps},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": ncu_traffic(args.config),
+                     "peak_kind": peak_kind, "kernel": "k_phase (region sweep, fused delta)",
+                     "bytes_per_launch": acc["bytes"] / (args.steps * phases_per_sweep),
+                     "avg_launch_ms": acc["sweep_ms"] / (args.steps * phases_per_sweep)},
+        "gpu_launches": int(acc["launches"]),
+    }
+    res["clocks"] = clk.summary()
+    # e2e through the C-ABI with host buffers: per step upload the observed
+    # signals from pinned memory, load the start hypothesis, one sweep, read
+    # the final hypothesis back
+    if not args.no_e2e:
+        pin = torch.empty(sig.size * sig.itemsize, dtype=torch.uint8, pin_memory=True)
+        pin_np = pin.numpy().view(sig.dtype).reshape(sig.shape)
+        pin_np[...] = sig
+        eng.upload_signals(pin_np)
+        h2d = sig.nbytes + ev.N * (24 + 8 * c["S"])
+        d2h = 0
+        e2e_steps = max(3, min(args.steps, 10))
+        barrier(dist)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        props = 0
+        for i in range(e2e_steps):
+            eng.upload_signals(pin_np)
+            eng.set_hypothesis(truth)
+            tr = eng.run_chromatic(sampler_for(c, seed0 + 500 + i), final=True, row_cap=4)
+            props += tr.total_steps
+            d2h = tr.final.N * (24 + 8 * c["S"])
+        torch.cuda.synchronize()
+        wall = reduce_max(dist, time.perf_counter() - t0)
+        res["e2e"] = {"value": reduce_sum(dist, props) / wall, "unit": "proposals/s",
+                      "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                      "path": "seis_upload_signals + seis_set_hypothesis + seis_run_chromatic "
+                              "+ seis_get_hypothesis, wall clock"}
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        r = cpu_baseline_ref(c, m, ev, sig, args.cpu_seconds, threads)
+        if r is not None:
+            res["cpu_baseline"] = {
+                "value": r[0] / r[1], "unit": "proposals/s", "cores": threads,
+                "kind": "reference",
+                "sample": f"{r[0]} proposals in {r[1]:.1f} s: reference run_region_steps on the "
+                          f"truth world, one region chain per thread ({threads} threads)"}
+        else:
+            res["cpu_baseline"] = None
+    if rank == 0:
+        print(json.dumps(res))
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -834,18 +834,19 @@ __global__ void __launch_bounds__(NT, 1)
         bo[q] = e;
       }
     pa.births_cnt[slot_idx] = nb;
-    // coverage diff for the commit; this-phase versions that died were
-    // already recycled locally, return them to the pool now
-    DiffEnt* dout = pa.diff + (size_t)slot_idx * MAXDIFF;
+    // coverage diff for the commit, then this-phase versions that died (sign
+    // 0): k_commit returns those slots to the pool, after every CTA of this
+    // phase has stopped popping from it
+    DiffEnt* dout = pa.diff + (size_t)slot_idx * MAXDOUT;
     for (int q = 0; q < nd; ++q) {
       dout[q].slot = dslot[q];
       dout[q].sign = dsign[q];
     }
-    pa.diff_cnt[slot_idx] = nd;
     for (int q = 0; q < nlfree; ++q) {
-      const int top = atomicAdd(&ctl->free_top, 1);
-      pa.free_stack[top] = lfree[q];
+      dout[nd + q].slot = lfree[q];
+      dout[nd + q].sign = 0;
     }
+    pa.diff_cnt[slot_idx] = nd + nlfree;
     atomicAdd(&ctl->scored, n_scored);
     atomicAdd(&ctl->changed, n_changed);
     atomicAdd(&ctl->arrvals, n_arr);
@@ -862,10 +863,11 @@ __global__ void k_commit(Dev d, int color, int ncol, int nreg, const int* diff_c
   const int region = color + slot_idx * ncol;
   if (region >= nreg) return;
   const int nd = diff_cnt[slot_idx];
-  const DiffEnt* de = diff + (size_t)slot_idx * MAXDIFF;
+  const DiffEnt* de = diff + (size_t)slot_idx * MAXDOUT;
   const double2* pool2 = reinterpret_cast<const double2*>(d.pool);
   for (int q = 0; q < nd; ++q) {
     const int slot = de[q].slot, sign = de[q].sign;
+    if (sign == 0) continue;
     for (int p = threadIdx.x; p < d.P2; p += blockDim.x) {
       const double2 a = pool2[(size_t)slot * d.P2 + p];
       const Win w0 = 2 * p < d.S ? make_win(d, a.x) : empty_win();
@@ -881,7 +883,7 @@ __global__ void k_commit(Dev d, int color, int ncol, int nreg, const int* diff_c
   __syncthreads();
   if (threadIdx.x == 0)
     for (int q = 0; q < nd; ++q)
-      if (de[q].sign < 0) {
+      if (de[q].sign <= 0) {
         const int top = atomicAdd(&ctl->free_top, 1);
         free_stack[top] = de[q].slot;
       }
@@ -1495,7 +1497,7 @@ int seis_set_hypothesis(seis_engine* e, int64_t N, const uint64_t* ids, const do
       ck(cudaMemcpy(tb.slot, hs.data(), N * 4, cudaMemcpyHostToDevice), "H2D");
       ck(cudaMemcpy(e->pool, ha.data(), ha.size() * 8, cudaMemcpyHostToDevice), "H2D");
     }
-    ck(cudaMemcpy(e->free_stack, fs.data(), (size_t)nf * 4 + 4, cudaMemcpyHostToDevice), "H2D");
+    if (nf) ck(cudaMemcpy(e->free_stack, fs.data(), (size_t)nf * 4, cudaMemcpyHostToDevice), "H2D");
     Ctl c{};
     c.n_events = (int)N;
     c.free_top = nf;
@@ -1751,15 +1753,33 @@ extern "C" int seis_run_chromatic(seis_engine* e, const seis_sampler_cfg* sc, in
     sp.joint_t_sd = sc->step_joint / e->cfg.v;
     sp.ncol = ncol;
     const int bcap = (int)sc->n_regions + 4;
-    const int CH = (int)std::min<int64_t>(sc->epochs, 64);
-    double* bnd = static_cast<double*>(alloc((size_t)CH * bcap * 8));
-    int* nreg_d = static_cast<int*>(alloc((size_t)CH * 4));
+    // every epoch's partition up front (one thread per epoch), so the timed
+    // region holds no host round trip
+    const int64_t n_ep = sc->dynamic ? sc->epochs : 1;
+    double* bnd = static_cast<double*>(alloc((size_t)n_ep * bcap * 8));
+    int* nreg_d = static_cast<int*>(alloc((size_t)n_ep * 4));
     int* perr = static_cast<int*>(alloc(4));
+    std::vector<int> h_nreg(n_ep);
+    {
+      ck(cudaMemsetAsync(perr, 0, 4, e->stream), "memset");
+      k_partition<<<(unsigned)((n_ep + 63) / 64), 64, 0, e->stream>>>(
+          e->cfg.T, l, tau, ncol, sc->dynamic ? 1 : 0, sc->seed, 0, (int)n_ep, 0.0, bcap, bnd,
+          nreg_d, perr, nullptr);
+      ck(cudaGetLastError(), "k_partition");
+      int herr = 0;
+      ck(cudaMemcpyAsync(h_nreg.data(), nreg_d, (size_t)n_ep * 4, cudaMemcpyDeviceToHost,
+                         e->stream),
+         "D2H nreg");
+      ck(cudaMemcpyAsync(&herr, perr, 4, cudaMemcpyDeviceToHost, e->stream), "D2H");
+      ck(cudaStreamSynchronize(e->stream), "sync");
+      if (herr == 1) throw std::logic_error("color_partition: separation invariant violated");
+      if (herr == 2) throw std::runtime_error("partition capacity");
+    }
     const int n_slots = (int)((sc->n_regions + 1 + ncol - 1) / ncol) + 1;
     int* births_cnt = static_cast<int*>(alloc((size_t)n_slots * 4));
     OutEv* births = static_cast<OutEv*>(alloc((size_t)n_slots * MAXOWN * sizeof(OutEv)));
     int* diff_cnt = static_cast<int*>(alloc((size_t)n_slots * 4));
-    DiffEnt* diff = static_cast<DiffEnt*>(alloc((size_t)n_slots * MAXDIFF * sizeof(DiffEnt)));
+    DiffEnt* diff = static_cast<DiffEnt*>(alloc((size_t)n_slots * MAXDOUT * sizeof(DiffEnt)));
     seis_tape_step* d_tape = nullptr;
     double* d_tarr = nullptr;
     seis_step_out* d_out = nullptr;
@@ -1786,7 +1806,7 @@ extern "C" int seis_run_chromatic(seis_engine* e, const seis_sampler_cfg* sc, in
     unsigned long long next_base = 0;
     ck(cudaMemcpyAsync(&next_base, maxid, 8, cudaMemcpyDeviceToHost, e->stream), "D2H");
     ck(cudaStreamSynchronize(e->stream), "sync");
-    int64_t launches = 2;
+    int64_t launches = 0;  // kernels launched inside the timed region
     cudaEvent_t ev_start, ev_stop;
     ck(cudaEventCreate(&ev_start), "event");
     ck(cudaEventCreate(&ev_stop), "event");
@@ -1813,25 +1833,11 @@ extern "C" int seis_run_chromatic(seis_engine* e, const seis_sampler_cfg* sc, in
     int64_t executed = 0, last_recorded = 0;
     long long tape_base = 0;
     const int64_t k = sc->steps_per_epoch;
-    std::vector<int> h_nreg(CH);
-    for (int64_t e0 = 0; e0 < sc->epochs; e0 += CH) {
-      const int nep = (int)std::min<int64_t>(CH, sc->epochs - e0);
-      ck(cudaMemsetAsync(perr, 0, 4, e->stream), "memset");
-      k_partition<<<(nep + 63) / 64, 64, 0, e->stream>>>(
-          e->cfg.T, l, tau, ncol, sc->dynamic ? 1 : 0, sc->seed, (int)e0, nep, 0.0, bcap, bnd,
-          nreg_d, perr, nullptr);
-      ++launches;
-      int herr = 0;
-      ck(cudaMemcpyAsync(h_nreg.data(), nreg_d, (size_t)nep * 4, cudaMemcpyDeviceToHost,
-                         e->stream),
-         "D2H nreg");
-      ck(cudaMemcpyAsync(&herr, perr, 4, cudaMemcpyDeviceToHost, e->stream), "D2H");
-      ck(cudaStreamSynchronize(e->stream), "sync");
-      if (herr == 1) throw std::logic_error("color_partition: separation invariant violated");
-      if (herr == 2) throw std::runtime_error("partition capacity");
-      for (int i = 0; i < nep; ++i) {
-        const int epoch = (int)(e0 + i);
-        const int nreg = h_nreg[i];
+    {
+      for (int64_t i = 0; i < sc->epochs; ++i) {
+        const int epoch = (int)i;
+        const int64_t pi = sc->dynamic ? i : 0;
+        const int nreg = h_nreg[pi];
         for (int color = 0; color < ncol; ++color) {
           const int ncr = nreg > color ? (nreg - color + ncol - 1) / ncol : 0;
           if (ncr == 0) continue;
@@ -1840,7 +1846,7 @@ extern "C" int seis_run_chromatic(seis_engine* e, const seis_sampler_cfg* sc, in
           pa.color = color;
           pa.nreg = nreg;
           pa.n_slots = ncr;
-          pa.bnd = bnd + (size_t)i * bcap;
+          pa.bnd = bnd + (size_t)pi * bcap;
           pa.next_base = next_base;
           pa.tape_base = tape_base;
           pa.tab = e->tab[e->cur];

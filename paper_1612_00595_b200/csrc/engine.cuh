@@ -24,6 +24,7 @@ constexpr int NT = 512;          // threads per region CTA
 constexpr int NW = NT / 32;
 constexpr int MAXOWN = 128;      // events a region may hold during a phase
 constexpr int MAXDIFF = 2 * MAXOWN;
+constexpr int MAXDOUT = 3 * MAXOWN;  // diff entries + recycled slots per region
 constexpr int TBL = 1024;        // per-count log/inverse-variance entries kept in smem
 constexpr int BANDMAX = 256;     // rows of the generic diff-correction scratch
 constexpr double kLog2Pi = 1.8378770664093454835606594728112;
@@ -98,7 +99,7 @@ struct PhaseArgs {
   int* births_cnt;                 // [n_slots]
   OutEv* births;                   // [n_slots][MAXOWN]
   int* diff_cnt;                   // [n_slots]
-  DiffEnt* diff;                   // [n_slots][MAXDIFF]
+  DiffEnt* diff;                   // [n_slots][MAXDOUT]
   int* free_stack;
   const seis_tape_step* tape;
   const double* tape_arr;

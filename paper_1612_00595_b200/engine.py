@@ -214,7 +214,7 @@ class Partition:
 def partition(T: float, l: float, offset: float, tau: float) -> Partition:
     """build_partition(T, l, offset) + color_partition(., tau), on the GPU."""
     L = load_library()
-    cap = int(T / l) + 16
+    cap = int(T / l) + 16 if (l > 0 and np.isfinite(T / l)) else 16
     b = np.zeros(cap)
     c = np.zeros(cap, np.int32)
     nr = i64(0)
