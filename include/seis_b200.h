@@ -118,6 +118,7 @@ typedef struct {
   int64_t kernel_launches;              /* kernels launched by the run */
   int64_t n_rows;                       /* trace rows produced */
   int64_t final_events;
+  int64_t speculative_discarded;        /* proposals evaluated ahead of an accept, then dropped */
 } seis_run_stats;
 
 const char* seis_last_error(void);

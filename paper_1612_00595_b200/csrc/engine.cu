@@ -145,160 +145,6 @@ __global__ void k_build_cov(Dev d, Table tab, const Ctl* ctl) {
   }
 }
 
-// ----------------------------------------------------------------- station pass
-enum { SRC_NONE = 0, SRC_BIRTH = 1, SRC_SHIFT = 2, SRC_ROWS = 3 };
-
-struct PassIn {
-  int src;
-  const double* rows[2];
-  uint64_t seed;
-  uint32_t sweep, region, step;
-  int wlo, whi;
-};
-
-// Scores one proposal over all stations (density.hpp:239-301): arrival
-// densities of added/removed events and the per-sample terms where the
-// coverage changes. Called by all NT threads; results are per-thread partials.
-template <typename YT>
-__device__ void station_pass(const Dev& d, const Prop& P, const PassIn& in, int nd,
-                             const int* dslot, const int* dsign, const double* Ls,
-                             const double* Is, double (&acc)[5], int& cnt) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const double2* pool2 = reinterpret_cast<const double2*>(d.pool);
-  const double2* st2 = reinterpret_cast<const double2*>(d.stations);
-  for (int base = warp * 32; base < d.P2; base += NT) {
-    const int p = base + lane;
-    const bool pv = p < d.P2;
-    const bool v0 = pv && 2 * p < d.S, v1 = pv && 2 * p + 1 < d.S;
-    Win A[2][2], R[2][2];
-#pragma unroll
-    for (int q = 0; q < 2; ++q) A[q][0] = A[q][1] = R[q][0] = R[q][1] = empty_win();
-    double s0 = 0.0, s1 = 0.0;
-    if (pv) {
-      const double2 s = st2[p];
-      s0 = s.x;
-      s1 = s.y;
-    }
-    double ra[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      if (q < P.nr && pv) {
-        const double2 v = pool2[(size_t)P.rslot[q] * d.P2 + p];
-        ra[q][0] = v.x;
-        ra[q][1] = v.y;
-        if (v0) {
-          R[q][0] = clampw(make_win(d, v.x), in.wlo, in.whi);
-          acc[3 + q] += arr_logpdf(d, v.x, arrival_mean(d, P.rx[q], P.rt[q], s0));
-        }
-        if (v1) {
-          R[q][1] = clampw(make_win(d, v.y), in.wlo, in.whi);
-          acc[3 + q] += arr_logpdf(d, v.y, arrival_mean(d, P.rx[q], P.rt[q], s1));
-        }
-      }
-    }
-#pragma unroll
-    for (int a = 0; a < 2; ++a) {
-      if (a < P.na && pv) {
-        double a0 = 0.0, a1 = 0.0;
-        const double m0 = arrival_mean(d, P.ax[a], P.at[a], s0);
-        const double m1 = arrival_mean(d, P.ax[a], P.at[a], s1);
-        if (in.src == SRC_BIRTH) {
-          float z0, z1;
-          seis_normal_pair(in.seed, in.sweep, in.region, in.step, (uint32_t)p, &z0, &z1);
-          a0 = m0 + d.sigma * (double)z0;
-          a1 = m1 + d.sigma * (double)z1;
-        } else if (in.src == SRC_SHIFT) {
-          a0 = ra[a][0] + (m0 - arrival_mean(d, P.rx[a], P.rt[a], s0));
-          a1 = ra[a][1] + (m1 - arrival_mean(d, P.rx[a], P.rt[a], s1));
-        } else {
-          if (v0) a0 = in.rows[a][2 * p];
-          if (v1) a1 = in.rows[a][2 * p + 1];
-        }
-        if (v0) {
-          A[a][0] = clampw(make_win(d, a0), in.wlo, in.whi);
-          acc[1 + a] += arr_logpdf(d, a0, m0);
-        }
-        if (v1) {
-          A[a][1] = clampw(make_win(d, a1), in.wlo, in.whi);
-          acc[1 + a] += arr_logpdf(d, a1, m1);
-        }
-      }
-    }
-    // windows that do not move leave every count unchanged
-#pragma unroll
-    for (int s = 0; s < 2; ++s) {
-      bool same = false;
-      if (P.nr == 1 && P.na == 1) same = weq(A[0][s], R[0][s]);
-      if (P.nr == 2 && P.na == 2)
-        same = (weq(A[0][s], R[0][s]) && weq(A[1][s], R[1][s])) ||
-               (weq(A[0][s], R[1][s]) && weq(A[1][s], R[0][s]));
-      if (same) A[0][s] = A[1][s] = R[0][s] = R[1][s] = empty_win();
-    }
-    int lo = INT_MAX, hi = INT_MIN;
-#pragma unroll
-    for (int q = 0; q < 2; ++q)
-#pragma unroll
-      for (int s = 0; s < 2; ++s) {
-        if (A[q][s].hi > A[q][s].lo) {
-          lo = min(lo, A[q][s].lo);
-          hi = max(hi, A[q][s].hi);
-        }
-        if (R[q][s].hi > R[q][s].lo) {
-          lo = min(lo, R[q][s].lo);
-          hi = max(hi, R[q][s].hi);
-        }
-      }
-    const int blo = __reduce_min_sync(0xffffffffu, lo);
-    const int bhi = __reduce_max_sync(0xffffffffu, hi);
-    if (blo >= bhi) continue;
-    if (nd == 0)
-      band_with_diff<0, YT>(d, p, v0, v1, blo, bhi, A, R, nd, dslot, dsign, Ls, Is, acc[0], cnt);
-    else if (nd <= 2)
-      band_with_diff<2, YT>(d, p, v0, v1, blo, bhi, A, R, nd, dslot, dsign, Ls, Is, acc[0], cnt);
-    else if (nd <= 4)
-      band_with_diff<4, YT>(d, p, v0, v1, blo, bhi, A, R, nd, dslot, dsign, Ls, Is, acc[0], cnt);
-    else if (nd <= 8)
-      band_with_diff<8, YT>(d, p, v0, v1, blo, bhi, A, R, nd, dslot, dsign, Ls, Is, acc[0], cnt);
-    else
-      band_rows_generic<YT>(d, p, blo, bhi, A, R, nd, dslot, dsign, Ls, Is, acc[0], cnt);
-  }
-}
-
-// Arrival move (proposals.hpp:161-174) in production: only station st moves.
-// Warp 0 scores it; lanes take rows.
-template <typename YT>
-__device__ void arrival_pass(const Dev& d, const Prop& P, int nd, const int* dslot,
-                             const int* dsign, const double* Ls, const double* Is,
-                             double (&acc)[5], int& cnt) {
-  const int lane = threadIdx.x & 31;
-  if (threadIdx.x >= 32) return;
-  const int st = P.arr_st;
-  const double old_a = d.pool[(size_t)P.rslot[0] * d.S_pad + st];
-  const double new_a = old_a + P.arr_da;
-  const double mean = arrival_mean(d, P.rx[0], P.rt[0], d.stations[st]);
-  if (lane == 0) {
-    acc[1] += arr_logpdf(d, new_a, mean);
-    acc[3] += arr_logpdf(d, old_a, mean);
-  }
-  const Win wo = make_win(d, old_a), wn = make_win(d, new_a);
-  if (weq(wo, wn)) return;
-  const int blo = min(wo.hi > wo.lo ? wo.lo : INT_MAX, wn.hi > wn.lo ? wn.lo : INT_MAX);
-  const int bhi = max(wo.hi > wo.lo ? wo.hi : INT_MIN, wn.hi > wn.lo ? wn.hi : INT_MIN);
-  const YT* y = reinterpret_cast<const YT*>(d.y);
-  const uint16_t* c16 = reinterpret_cast<const uint16_t*>(d.cov);
-  for (int r = blo + lane; r < bhi; r += 32) {
-    const int dc = inw(r, wn) - inw(r, wo);
-    if (!dc) continue;
-    int co = (int)c16[(size_t)r * d.S_pad + st];
-    for (int q = 0; q < nd; ++q) {
-      const Win w = make_win(d, d.pool[(size_t)dslot[q] * d.S_pad + st]);
-      co += dsign[q] * inw(r, w);
-    }
-    acc[0] += sample_term(d, Ls, Is, (double)y[(size_t)r * d.S_pad + st], co, co + dc);
-    ++cnt;
-  }
-}
-
 // ----------------------------------------------------------------- phase kernel
 template <int MODE>
 __device__ void gen_proposal(const Dev& d, const Samp& sp, const PhaseArgs& pa, Prop& P,
@@ -306,6 +152,7 @@ __device__ void gen_proposal(const Dev& d, const Samp& sp, const PhaseArgs& pa, 
                              bool rclosed, int step, long long tape_idx, unsigned long long id_next,
                              int* err) {
   P.skip = 0;
+  P.bad = 0;
   P.scored = 0;
   P.nr = P.na = 0;
   P.accept = 0;
@@ -442,7 +289,9 @@ __device__ void gen_proposal(const Dev& d, const Samp& sp, const PhaseArgs& pa, 
             break;
           }
         if (f < 0) {
-          atomicExch(err, ERR_TAPE_UNKNOWN_ID);
+          // may name an event born by an earlier step of this speculative
+          // round; only an error if this proposal is actually reached
+          P.bad = 1;
           null_ = true;
           break;
         }
@@ -485,16 +334,19 @@ __device__ void gen_proposal(const Dev& d, const Samp& sp, const PhaseArgs& pa, 
 template <typename YT, int MODE>
 __global__ void __launch_bounds__(NT, 1)
     k_phase(const Dev d, const Samp sp, const PhaseArgs pa, Ctl* ctl, int stamp) {
-  __shared__ double Ls[TBL], Is[TBL];
+  extern __shared__ __align__(16) unsigned char smem_dyn[];
+  double2* Ts = reinterpret_cast<double2*>(smem_dyn);  // [TBL * 4] {dL, dI}
   __shared__ OwnEv own[MAXOWN];
   __shared__ StartEv st[MAXOWN];
   __shared__ int dslot[MAXDIFF], dsign[MAXDIFF];
   __shared__ int lfree[MAXOWN];
-  __shared__ Prop prop[2];
-  __shared__ double red[NW][5];
-  __shared__ int redc[NW];
+  __shared__ Prop prop[2][MSPEC];
+  __shared__ double red_sig[NW][MSPEC], red_arr[NW][MSPEC];
+  __shared__ int red_cnt[NW][MSPEC];
   __shared__ int s_w[NW];
-  __shared__ int s_nown, s_nd, s_abort, s_tmp;
+  __shared__ int s_nown, s_nd, s_abort, s_tmp, s_adv, s_accq;
+  __shared__ unsigned long long s_births;
+  __shared__ long long s_nlocal;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int slot_idx = blockIdx.x;
@@ -504,10 +356,7 @@ __global__ void __launch_bounds__(NT, 1)
   const bool rclosed = region + 1 == pa.nreg;
   const int N = ctl->n_events;
 
-  for (int i = tid; i < TBL; i += NT) {
-    Ls[i] = i < d.tab_n ? d.Lg[i] : 0.0;
-    Is[i] = i < d.tab_n ? d.Ig[i] : 0.0;
-  }
+  for (int i = tid; i < TBL * 4; i += NT) Ts[i] = i < d.tab_n * 4 ? d.Dg[i] : make_double2(0, 0);
   if (tid == 0) {
     s_nown = 0;
     s_abort = 0;
@@ -558,116 +407,156 @@ __global__ void __launch_bounds__(NT, 1)
     return;
   }
   const int nstart = s_nown;
-  // thread-0 chain state
+  // thread-0 chain state (mirrored in shared memory for the generators)
   int nown = nstart, nd = 0, nlfree = 0;
   long long n_local = N;
-  unsigned long long births = 0, n_acc = 0, n_scored = 0, n_arr = 0;
+  unsigned long long births = 0, n_acc = 0, n_scored = 0, n_arr = 0, n_changed = 0;
+  unsigned long long n_spec = 0;
   const unsigned long long id_base = pa.next_base + (unsigned long long)slot_idx * sp.k;
-  if (tid == 0) s_nd = 0;
-  unsigned long long n_changed = 0;
-  int cnt_total = 0;
-
-  for (int step = 0; step < (int)sp.k; ++step) {
-    Prop& P = prop[step & 1];
-    const long long tape_idx = pa.tape_base + (long long)slot_idx * sp.k + step;
+  if (tid == 0) {
+    s_nd = 0;
+    s_births = 0;
+    s_nlocal = N;
+  }
+  const int T_per = (d.P2 + 31) / 32;
+  int round = 0;
+  for (int i0 = 0; i0 < (int)sp.k; ++round) {
+    const int m = min(MSPEC, (int)sp.k - i0);
+    const int buf = round & 1;
+    __syncthreads();  // S0: previous round's write-back and state are visible
+    if (tid < m) {
+      const int step = i0 + tid;
+      gen_proposal<MODE>(d, sp, pa, prop[buf][tid], own, s_nown, region, rlo, rhi, rclosed,
+                         step, pa.tape_base + (long long)slot_idx * sp.k + step,
+                         id_base + s_births, &ctl->err);
+    }
+    if (lane < MSPEC) {
+      red_sig[warp][lane] = 0.0;
+      red_arr[warp][lane] = 0.0;
+      red_cnt[warp][lane] = 0;
+    }
+    __syncthreads();  // S1: proposals ready
+    {
+      // work items: (proposal q, tile of 32 station pairs), spread over warps
+      const int nd_now = s_nd;
+      int cur_q = -1;
+      double sig = 0.0, arr = 0.0;
+      int cnt = 0;
+      const int n_items = m * T_per;
+      for (int t = warp; t < n_items; t += NW) {
+        const int q = t / T_per, tile = t - q * T_per;
+        if (q != cur_q) {
+          if (cur_q >= 0) {
+            sig = warp_sum(sig);
+            arr = warp_sum(arr);
+            cnt = __reduce_add_sync(0xffffffffu, (unsigned)cnt);
+            if (lane == 0) {
+              red_sig[warp][cur_q] += sig;
+              red_arr[warp][cur_q] += arr;
+              red_cnt[warp][cur_q] += cnt;
+            }
+            sig = arr = 0.0;
+            cnt = 0;
+          }
+          cur_q = q;
+        }
+        const Prop& P = prop[buf][q];
+        PassIn in;
+        in.src = P.na == 0 ? SRC_NONE
+                           : (MODE == 1 ? SRC_ROWS : (P.type == 0 ? SRC_BIRTH : SRC_SHIFT));
+        in.rows[0] = pa.tape_arr + (MODE == 1 ? P.tape_off : 0);
+        in.rows[1] = in.rows[0] + d.S;
+        in.seed = sp.seed;
+        in.sweep = (uint32_t)pa.epoch;
+        in.region = (uint32_t)region;
+        in.step = (uint32_t)(i0 + q);
+        in.wlo = 0;
+        in.whi = d.n;
+        score_item<MODE, YT>(d, P, in, tile, nd_now, dslot, dsign, Ts, sig, arr, cnt);
+      }
+      if (cur_q >= 0) {
+        sig = warp_sum(sig);
+        arr = warp_sum(arr);
+        cnt = __reduce_add_sync(0xffffffffu, (unsigned)cnt);
+        if (lane == 0) {
+          red_sig[warp][cur_q] += sig;
+          red_arr[warp][cur_q] += arr;
+          red_cnt[warp][cur_q] += cnt;
+        }
+      }
+    }
+    __syncthreads();  // S2: partial sums ready
     if (tid == 0) {
-      gen_proposal<MODE>(d, sp, pa, P, own, nown, region, rlo, rhi, rclosed, step, tape_idx,
-                         id_base + births, &ctl->err);
-      if (P.scored) ++n_scored;
-      if (P.skip) {
-        // null (no draw), constrained out, or out of support: log_r = -inf
-        // -> reject (proposals.hpp:268-291)
+      int adv = m, accq = -1;
+      for (int q = 0; q < m; ++q) {
+        Prop& P = prop[buf][q];
+        if (MODE == 1 && P.bad) {
+          atomicExch(&ctl->err, ERR_TAPE_UNKNOWN_ID);
+          s_abort = 1;
+          adv = q + 1;
+          break;
+        }
+        if (P.scored) ++n_scored;
+        if (P.skip) {
+          // null (no draw), constrained out, or out of support: log_r = -inf
+          // -> reject (proposals.hpp:268-291)
+          if (MODE == 1) {
+            seis_step_out o;
+            o.delta = -INFINITY;
+            o.log_r = -INFINITY;
+            o.scored = P.scored;
+            o.accepted = 0;
+            pa.out[P.tape_idx] = o;
+          }
+          continue;
+        }
+        double sig = 0.0, A = 0.0;
+        int c = 0;
+        for (int w = 0; w < NW; ++w) {
+          sig += red_sig[w][q];
+          A += red_arr[w][q];
+          c += red_cnt[w][q];
+        }
+        n_changed += (unsigned long long)c;
+        n_arr += (P.type == 3) ? 2ull : (unsigned long long)d.S * (P.nr + P.na);
+        // delta_log_joint (density.hpp:223-240): prior terms with n0 = local
+        // event count and area T, arrival densities, likelihood
+        const long long n0 = n_local, n1 = n0 - P.nr + P.na;
+        double delta = 0.0;
+        if (n1 > n0) {
+          for (long long i = n0 + 1; i <= n1; ++i) delta += d.log_lambda_T - d.logi[i];
+        } else if (n1 < n0) {
+          for (long long i = n1 + 1; i <= n0; ++i) delta -= d.log_lambda_T - d.logi[i];
+        }
+        delta += (double)(n1 - n0) * d.lxa;
+        delta += A;
+        delta += sig;
+        // proposal log densities (proposals.hpp:100-104,120-126)
+        if (MODE == 0) {
+          if (P.type == 0) {
+            P.logq_f = sp.logw[0] - log(rhi - rlo) - d.log_xmax + A;
+            P.logq_r = sp.logw[1] - d.logi[nown + 1];
+          } else if (P.type == 1) {
+            P.logq_f = sp.logw[1] - d.logi[nown];
+            P.logq_r = sp.logw[0] - log(rhi - rlo) - d.log_xmax - A;
+          }
+        }
+        const double log_r = delta + P.logq_r - P.logq_f;  // log_accept_ratio
+        // mh_step decision (proposals.hpp:283-291)
+        bool acc_gpu = log_r >= 0.0;
+        if (!acc_gpu) acc_gpu = log(P.u) < log_r;
+        bool apply = acc_gpu;
         if (MODE == 1) {
           seis_step_out o;
-          o.delta = -INFINITY;
-          o.log_r = -INFINITY;
-          o.scored = P.scored;
-          o.accepted = 0;
-          pa.out[tape_idx] = o;
+          o.delta = delta;
+          o.log_r = log_r;
+          o.scored = 1;
+          o.accepted = acc_gpu ? 1 : 0;
+          pa.out[P.tape_idx] = o;
+          apply = P.tape_acc != 0;  // keep the state on the tape's trajectory
         }
-      }
-    }
-    __syncthreads();
-    if (P.skip) continue;
-    double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-    int cnt = 0;
-    if (MODE == 0 && P.type == 3) {
-      arrival_pass<YT>(d, P, s_nd, dslot, dsign, Ls, Is, acc, cnt);
-    } else {
-      PassIn in;
-      in.src = P.na == 0 ? SRC_NONE
-                         : (MODE == 1 ? SRC_ROWS : (P.type == 0 ? SRC_BIRTH : SRC_SHIFT));
-      in.rows[0] = pa.tape_arr + (MODE == 1 ? P.tape_off : 0);
-      in.rows[1] = in.rows[0] + d.S;
-      in.seed = sp.seed;
-      in.sweep = (uint32_t)pa.epoch;
-      in.region = (uint32_t)region;
-      in.step = (uint32_t)step;
-      in.wlo = 0;
-      in.whi = d.n;
-      station_pass<YT>(d, P, in, s_nd, dslot, dsign, Ls, Is, acc, cnt);
-    }
-#pragma unroll
-    for (int q = 0; q < 5; ++q) acc[q] = warp_sum(acc[q]);
-    cnt = __reduce_add_sync(0xffffffffu, (unsigned)cnt);
-    if (lane == 0) {
-#pragma unroll
-      for (int q = 0; q < 5; ++q) red[warp][q] = acc[q];
-      redc[warp] = cnt;
-    }
-    __syncthreads();
-    if (tid == 0) {
-      double sig = 0.0, A[5];
-      for (int q = 1; q < 5; ++q) A[q] = 0.0;
-      int c = 0;
-      for (int w = 0; w < NW; ++w) {
-        sig += red[w][0];
-        for (int q = 1; q < 5; ++q) A[q] += red[w][q];
-        c += redc[w];
-      }
-      n_changed += (unsigned long long)c;
-      n_arr += (P.type == 3) ? 2ull : (unsigned long long)d.S * (P.nr + P.na);
-      // delta_log_joint (density.hpp:223-240): prior terms with n0 = local
-      // event count and area T, arrival densities, likelihood
-      const long long n0 = n_local, n1 = n0 - P.nr + P.na;
-      double delta = 0.0;
-      if (n1 > n0) {
-        for (long long i = n0 + 1; i <= n1; ++i) delta += d.log_lambda_T - d.logi[i];
-      } else if (n1 < n0) {
-        for (long long i = n1 + 1; i <= n0; ++i) delta -= d.log_lambda_T - d.logi[i];
-      }
-      delta += (double)(n1 - n0) * d.lxa;
-      if (P.na >= 1) delta += A[1];
-      if (P.na >= 2) delta += A[2];
-      if (P.nr >= 1) delta -= A[3];
-      if (P.nr >= 2) delta -= A[4];
-      delta += sig;
-      // proposal log densities (proposals.hpp:100-104,120-126)
-      if (MODE == 0) {
-        if (P.type == 0) {
-          P.logq_f = sp.logw[0] - log(rhi - rlo) - d.log_xmax + A[1];
-          P.logq_r = sp.logw[1] - d.logi[nown + 1];
-        } else if (P.type == 1) {
-          P.logq_f = sp.logw[1] - d.logi[nown];
-          P.logq_r = sp.logw[0] - log(rhi - rlo) - d.log_xmax + A[3];
-        }
-      }
-      const double log_r = delta + P.logq_r - P.logq_f;  // log_accept_ratio
-      // mh_step decision (proposals.hpp:283-291)
-      bool acc_gpu = log_r >= 0.0;
-      if (!acc_gpu) acc_gpu = log(P.u) < log_r;
-      bool apply = acc_gpu;
-      if (MODE == 1) {
-        seis_step_out o;
-        o.delta = delta;
-        o.log_r = log_r;
-        o.scored = 1;
-        o.accepted = acc_gpu ? 1 : 0;
-        pa.out[tape_idx] = o;
-        apply = P.tape_acc != 0;  // keep the state on the tape's trajectory
-      }
-      P.accept = 0;
-      if (apply) {
+        P.accept = 0;
+        if (!apply) continue;
         // allocate destination slots; modify this-phase versions in place
         bool ok = true;
         for (int a = 0; a < P.na; ++a) {
@@ -695,59 +584,72 @@ __global__ void __launch_bounds__(NT, 1)
         }
         if (!ok) {
           s_abort = 1;
-        } else {
-          P.accept = 1;
-          ++n_acc;
-          if (P.type == 0) ++births;
-          // retire removed versions; deaths of this-phase versions free slots
-          for (int q = 0; q < P.nr; ++q) {
-            const int sidx = P.rsidx[q];
-            if (sidx >= 0)
-              st[sidx].current = 0;
-            else if (q >= P.na)
-              lfree[nlfree++] = P.rslot[q];
-          }
-          // apply_change (density.hpp:171-180): erase by id, push_back added
-          unsigned long long rid[2];
-          for (int q = 0; q < P.nr; ++q) rid[q] = own[P.rown[q]].id;
-          for (int q = 0; q < P.nr; ++q) {
-            int i = 0;
-            while (i < nown && own[i].id != rid[q]) ++i;
-            for (int j = i; j + 1 < nown; ++j) own[j] = own[j + 1];
-            --nown;
-          }
-          for (int a = 0; a < P.na; ++a) {
-            OwnEv e;
-            e.id = P.type == 0 ? P.aid : rid[a];
-            e.x = P.ax[a];
-            e.t = P.at[a];
-            e.slot = P.dslot[a];
-            e.sidx = -1;
-            own[nown++] = e;
-          }
-          n_local += P.na - P.nr;
-          // own diff vs the phase-start snapshot (frozen-snapshot view)
-          nd = 0;
-          for (int i = 0; i < nstart; ++i)
-            if (!st[i].current) {
-              dslot[nd] = st[i].slot;
-              dsign[nd++] = -1;
-            }
-          for (int i = 0; i < nown; ++i)
-            if (own[i].sidx < 0) {
-              dslot[nd] = own[i].slot;
-              dsign[nd++] = 1;
-            }
-          s_nd = nd;
-          if (MODE == 1 && P.type == 0 && P.aid != id_base + births - 1)
-            atomicAdd(&ctl->id_mismatch, 1ull);
+          adv = q + 1;
+          break;
         }
+        P.accept = 1;
+        ++n_acc;
+        if (P.type == 0) ++births;
+        // retire removed versions; deaths of this-phase versions free slots
+        for (int r = 0; r < P.nr; ++r) {
+          const int sidx = P.rsidx[r];
+          if (sidx >= 0)
+            st[sidx].current = 0;
+          else if (r >= P.na)
+            lfree[nlfree++] = P.rslot[r];
+        }
+        // apply_change (density.hpp:171-180): erase by id, push_back added
+        unsigned long long rid[2];
+        for (int r = 0; r < P.nr; ++r) rid[r] = own[P.rown[r]].id;
+        for (int r = 0; r < P.nr; ++r) {
+          int i = 0;
+          while (i < nown && own[i].id != rid[r]) ++i;
+          for (int j = i; j + 1 < nown; ++j) own[j] = own[j + 1];
+          --nown;
+        }
+        for (int a = 0; a < P.na; ++a) {
+          OwnEv e;
+          e.id = P.type == 0 ? P.aid : rid[a];
+          e.x = P.ax[a];
+          e.t = P.at[a];
+          e.slot = P.dslot[a];
+          e.sidx = -1;
+          own[nown++] = e;
+        }
+        n_local += P.na - P.nr;
+        // own diff vs the phase-start snapshot (frozen-snapshot view)
+        nd = 0;
+        for (int i = 0; i < nstart; ++i)
+          if (!st[i].current) {
+            dslot[nd] = st[i].slot;
+            dsign[nd++] = -1;
+          }
+        for (int i = 0; i < nown; ++i)
+          if (own[i].sidx < 0) {
+            dslot[nd] = own[i].slot;
+            dsign[nd++] = 1;
+          }
+        if (MODE == 1 && P.type == 0 && P.aid != id_base + births - 1)
+          atomicAdd(&ctl->id_mismatch, 1ull);
+        accq = q;
+        adv = q + 1;
+        break;
       }
+      n_spec += (unsigned long long)(m - adv);
+      s_adv = adv;
+      s_accq = accq;
+      s_nown = nown;
+      s_nd = nd;
+      s_births = births;
+      s_nlocal = n_local;
     }
-    __syncthreads();
+    __syncthreads();  // S3: decision
     if (s_abort) return;
-    if (P.accept) {
-      // write the accepted versions' arrivals (recomputed exactly as scored)
+    const int accq = s_accq;
+    if (accq >= 0) {
+      // write the accepted version's arrivals (recomputed exactly as scored)
+      const Prop& P = prop[buf][accq];
+      const int step = i0 + accq;
       double2* pool2 = reinterpret_cast<double2*>(d.pool);
       const double2* st2 = reinterpret_cast<const double2*>(d.stations);
       if (MODE == 0 && P.type == 3) {
@@ -791,12 +693,10 @@ __global__ void __launch_bounds__(NT, 1)
         }
       }
     }
+    i0 += s_adv;
   }
   __syncthreads();
   // ---- phase outputs (the barrier merge, samplers.hpp:459-462,471-482)
-  const int nown_f = s_nown;  // unused; thread 0 state below
-  (void)nown_f;
-  (void)cnt_total;
   if (tid == 0) {
     // fates of the phase-start versions
     for (int i = 0; i < nstart; ++i) {
@@ -851,6 +751,7 @@ __global__ void __launch_bounds__(NT, 1)
     atomicAdd(&ctl->changed, n_changed);
     atomicAdd(&ctl->arrvals, n_arr);
     atomicAdd(&ctl->accepted, n_acc);
+    atomicAdd(&ctl->speculative, n_spec);
   }
 }
 
@@ -987,18 +888,18 @@ template <typename YT>
 __global__ void __launch_bounds__(NT, 1)
     k_score_batch(const Dev d, Table tab, const Ctl* ctl, const ChangeDev* ch,
                   const double* rows, double* out) {
-  __shared__ double Ls[TBL], Is[TBL];
+  extern __shared__ __align__(16) unsigned char smem_dyn[];
+  double2* Ts = reinterpret_cast<double2*>(smem_dyn);
   __shared__ Prop P;
-  __shared__ double red[NW][5];
+  __shared__ double rsig[NW], rarr[NW];
   __shared__ int s_bad;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const ChangeDev c = ch[blockIdx.x];
-  for (int i = tid; i < TBL; i += NT) {
-    Ls[i] = i < d.tab_n ? d.Lg[i] : 0.0;
-    Is[i] = i < d.tab_n ? d.Ig[i] : 0.0;
-  }
+  for (int i = tid; i < TBL * 4; i += NT) Ts[i] = i < d.tab_n * 4 ? d.Dg[i] : make_double2(0, 0);
   if (tid == 0) {
     s_bad = 0;
+    P.type = -1;
+    P.skip = 0;
     P.nr = c.nr;
     P.na = c.na;
     const int N = ctl->n_events;
@@ -1041,26 +942,25 @@ __global__ void __launch_bounds__(NT, 1)
   in.whi = c.whi;
   in.seed = 0;
   in.sweep = in.region = in.step = 0;
-  double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  double sig = 0.0, arr = 0.0;
   int cnt = 0;
-  station_pass<YT>(d, P, in, 0, nullptr, nullptr, Ls, Is, acc, cnt);
-#pragma unroll
-  for (int q = 0; q < 5; ++q) acc[q] = warp_sum(acc[q]);
-  if (lane == 0)
-    for (int q = 0; q < 5; ++q) red[warp][q] = acc[q];
+  const int T_per = (d.P2 + 31) / 32;
+  for (int t = warp; t < T_per; t += NW)
+    score_item<1, YT>(d, P, in, t, 0, nullptr, nullptr, Ts, sig, arr, cnt);
+  sig = warp_sum(sig);
+  arr = warp_sum(arr);
+  if (lane == 0) {
+    rsig[warp] = sig;
+    rarr[warp] = arr;
+  }
   __syncthreads();
   if (tid == 0) {
-    double sig = 0.0, A[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    double s = 0.0, A = 0.0;
     for (int w = 0; w < NW; ++w) {
-      sig += red[w][0];
-      for (int q = 1; q < 5; ++q) A[q] += red[w][q];
+      s += rsig[w];
+      A += rarr[w];
     }
-    double delta = c.prior;
-    if (c.na >= 1) delta += A[1];
-    if (c.na >= 2) delta += A[2];
-    if (c.nr >= 1) delta -= A[3];
-    if (c.nr >= 2) delta -= A[4];
-    out[blockIdx.x] = delta + sig;
+    out[blockIdx.x] = c.prior + A + s;
   }
 }
 
@@ -1153,6 +1053,7 @@ __global__ void k_record(const Ctl* ctl, long long* count_out) { *count_out = ct
 
 __global__ void k_reset_counters(Ctl* ctl) {
   ctl->scored = ctl->changed = ctl->arrvals = ctl->accepted = ctl->id_mismatch = 0ull;
+  ctl->speculative = 0ull;
   ctl->err = 0;
 }
 
@@ -1164,6 +1065,7 @@ using namespace seis;
 namespace {
 
 thread_local std::string g_err;
+constexpr int kPhaseSmem = TBL * 4 * (int)sizeof(double2);
 
 int fail(int code, const std::string& m) {
   g_err = m;
@@ -1248,6 +1150,7 @@ struct seis_engine {
   double* pool = nullptr;
   double* Lg = nullptr;
   double* Ig = nullptr;
+  double2* Dg = nullptr;
   double* logi = nullptr;
   double* logfact = nullptr;
   std::vector<double> h_logi, h_logfact;
@@ -1269,6 +1172,7 @@ struct seis_engine {
     cudaFree(pool);
     cudaFree(Lg);
     cudaFree(Ig);
+    cudaFree(Dg);
     cudaFree(logi);
     cudaFree(logfact);
     for (auto& t : tab) {
@@ -1386,6 +1290,17 @@ int seis_engine_create(const seis_model_cfg* cfg, const double* stations, int64_
       L[c] = -0.5 * (kLog2Pi + std::log(var));
       I[c] = 0.5 / var;
     }
+    std::vector<double2> Dt((size_t)tab_n * 4);
+    const int dcs[4] = {-2, -1, 1, 2};
+    for (int c = 0; c < tab_n; ++c)
+      for (int k = 0; k < 4; ++k) {
+        const int cn = c + dcs[k];
+        Dt[(size_t)c * 4 + k] = (cn >= 0 && cn < tab_n)
+                                    ? make_double2(L[cn] - L[c], I[cn] - I[c])
+                                    : make_double2(0.0, 0.0);
+      }
+    e->Dg = dalloc<double2>((size_t)tab_n * 4);
+    ck(cudaMemcpy(e->Dg, Dt.data(), Dt.size() * sizeof(double2), cudaMemcpyHostToDevice), "H2D");
     e->Lg = dalloc<double>(tab_n);
     e->Ig = dalloc<double>(tab_n);
     ck(cudaMemcpy(e->Lg, L.data(), tab_n * 8, cudaMemcpyHostToDevice), "H2D");
@@ -1439,10 +1354,18 @@ int seis_engine_create(const seis_model_cfg* cfg, const double* stations, int64_
     d.pool = e->pool;
     d.Lg = e->Lg;
     d.Ig = e->Ig;
+    d.Dg = e->Dg;
     d.tab_n = tab_n;
     d.logi = e->logi;
     d.logi_n = tab_n;
     d.pool_cap = e->cap;
+    const int smem = TBL * 4 * (int)sizeof(double2);
+    ck(cudaFuncSetAttribute(k_phase<float, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "attr");
+    ck(cudaFuncSetAttribute(k_phase<float, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "attr");
+    ck(cudaFuncSetAttribute(k_phase<double, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "attr");
+    ck(cudaFuncSetAttribute(k_phase<double, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "attr");
+    ck(cudaFuncSetAttribute(k_score_batch<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "attr");
+    ck(cudaFuncSetAttribute(k_score_batch<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "attr");
     upload_signals(e, signals);
   });
   if (rc) {
@@ -1660,10 +1583,10 @@ int seis_score_batch(seis_engine* e, int64_t n_changes, const seis_change* chang
                          cudaMemcpyHostToDevice, e->stream),
          "H2D");
     if (e->dtype == SEIS_F64)
-      k_score_batch<double><<<(unsigned)n_changes, NT, 0, e->stream>>>(e->d, e->tab[e->cur],
+      k_score_batch<double><<<(unsigned)n_changes, NT, kPhaseSmem, e->stream>>>(e->d, e->tab[e->cur],
                                                                        e->ctl, dc, rows, o);
     else
-      k_score_batch<float><<<(unsigned)n_changes, NT, 0, e->stream>>>(e->d, e->tab[e->cur],
+      k_score_batch<float><<<(unsigned)n_changes, NT, kPhaseSmem, e->stream>>>(e->d, e->tab[e->cur],
                                                                       e->ctl, dc, rows, o);
     ck(cudaGetLastError(), "k_score_batch");
     ck(cudaMemcpyAsync(delta_out, o, n_changes * 8, cudaMemcpyDeviceToHost, e->stream), "D2H");
@@ -1876,14 +1799,14 @@ extern "C" int seis_run_chromatic(seis_engine* e, const seis_sampler_cfg* sc, in
           }
           if (e->dtype == SEIS_F64) {
             if (mode == 0)
-              k_phase<double, 0><<<ncr, NT, 0, e->stream>>>(e->d, sp, pa, e->ctl, stamp);
+              k_phase<double, 0><<<ncr, NT, kPhaseSmem, e->stream>>>(e->d, sp, pa, e->ctl, stamp);
             else
-              k_phase<double, 1><<<ncr, NT, 0, e->stream>>>(e->d, sp, pa, e->ctl, stamp);
+              k_phase<double, 1><<<ncr, NT, kPhaseSmem, e->stream>>>(e->d, sp, pa, e->ctl, stamp);
           } else {
             if (mode == 0)
-              k_phase<float, 0><<<ncr, NT, 0, e->stream>>>(e->d, sp, pa, e->ctl, stamp);
+              k_phase<float, 0><<<ncr, NT, kPhaseSmem, e->stream>>>(e->d, sp, pa, e->ctl, stamp);
             else
-              k_phase<float, 1><<<ncr, NT, 0, e->stream>>>(e->d, sp, pa, e->ctl, stamp);
+              k_phase<float, 1><<<ncr, NT, kPhaseSmem, e->stream>>>(e->d, sp, pa, e->ctl, stamp);
           }
           if (timing) {
             ck(cudaEventRecord(b, e->stream), "event");
@@ -1956,6 +1879,7 @@ extern "C" int seis_run_chromatic(seis_engine* e, const seis_sampler_cfg* sc, in
       stats->kernel_launches = launches;
       stats->n_rows = n_rows;
       stats->final_events = c.n_events;
+      stats->speculative_discarded = (int64_t)c.speculative;
     }
   });
   for (auto ev : evs) cudaEventDestroy(ev);

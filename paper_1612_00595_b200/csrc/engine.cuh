@@ -21,11 +21,12 @@
 namespace seis {
 
 constexpr int NT = 512;          // threads per region CTA
+constexpr int MSPEC = 4;         // speculative proposals evaluated per round
 constexpr int NW = NT / 32;
 constexpr int MAXOWN = 128;      // events a region may hold during a phase
 constexpr int MAXDIFF = 2 * MAXOWN;
 constexpr int MAXDOUT = 3 * MAXOWN;  // diff entries + recycled slots per region
-constexpr int TBL = 1024;        // per-count log/inverse-variance entries kept in smem
+constexpr int TBL = 1024;        // coverage counts whose {dL, dI} rows live in smem
 constexpr int BANDMAX = 256;     // rows of the generic diff-correction scratch
 constexpr double kLog2Pi = 1.8378770664093454835606594728112;
 
@@ -45,6 +46,7 @@ struct Dev {
   double* pool;                    // [P][S_pad]
   const double* Lg;                // [tab_n] -0.5 (log 2pi + log var_c)
   const double* Ig;                // [tab_n] 0.5 / var_c
+  const double2* Dg;               // [tab_n][4] {L[c+dc]-L[c], I[c+dc]-I[c]}, dc=-2,-1,1,2
   int tab_n;
   const double* logi;              // [logi_n] log((double) i)
   int logi_n;
@@ -82,7 +84,7 @@ struct Ctl {
   int free_top;
   int err;
   int phase_stamp;
-  unsigned long long scored, changed, arrvals, accepted, id_mismatch;
+  unsigned long long scored, changed, arrvals, accepted, id_mismatch, speculative;
 };
 
 struct PhaseArgs {

@@ -49,7 +49,7 @@ class _StatsC(C.Structure):
     _fields_ = [("total_steps", i64), ("total_accepted", i64), ("scored_proposals", i64),
                 ("changed_samples", i64), ("arrival_values", i64), ("algorithmic_bytes", f64),
                 ("sweep_kernel_ms", f64), ("total_ms", f64), ("kernel_launches", i64),
-                ("n_rows", i64), ("final_events", i64)]
+                ("n_rows", i64), ("final_events", i64), ("speculative_discarded", i64)]
 
 
 TAPE_DTYPE = np.dtype([
