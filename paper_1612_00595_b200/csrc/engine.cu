@@ -338,13 +338,13 @@ __global__ void __launch_bounds__(NT, 1)
   double2* Ts = reinterpret_cast<double2*>(smem_dyn);  // [TBL * 4] {dL, dI}
   __shared__ OwnEv own[MAXOWN];
   __shared__ StartEv st[MAXOWN];
-  __shared__ int dslot[MAXDIFF], dsign[MAXDIFF];
+  __shared__ int pold[MAXDIFF], pnew[MAXDIFF];
   __shared__ int lfree[MAXOWN];
   __shared__ Prop prop[2][MSPEC];
   __shared__ double red_sig[NW][MSPEC], red_arr[NW][MSPEC];
   __shared__ int red_cnt[NW][MSPEC];
   __shared__ int s_w[NW];
-  __shared__ int s_nown, s_nd, s_abort, s_tmp, s_adv, s_accq;
+  __shared__ int s_nown, s_np, s_abort, s_tmp, s_adv, s_accq;
   __shared__ unsigned long long s_births;
   __shared__ long long s_nlocal;
 
@@ -408,17 +408,17 @@ __global__ void __launch_bounds__(NT, 1)
   }
   const int nstart = s_nown;
   // thread-0 chain state (mirrored in shared memory for the generators)
-  int nown = nstart, nd = 0, nlfree = 0;
+  int nown = nstart, np = 0, nlfree = 0;
   long long n_local = N;
   unsigned long long births = 0, n_acc = 0, n_scored = 0, n_arr = 0, n_changed = 0;
   unsigned long long n_spec = 0;
   const unsigned long long id_base = pa.next_base + (unsigned long long)slot_idx * sp.k;
   if (tid == 0) {
-    s_nd = 0;
+    s_np = 0;
     s_births = 0;
     s_nlocal = N;
   }
-  const int T_per = (d.P2 + 31) / 32;
+  const int T_per = (d.S_pad + 31) / 32;  // tiles of 32 stations
   int round = 0;
   for (int i0 = 0; i0 < (int)sp.k; ++round) {
     const int m = min(MSPEC, (int)sp.k - i0);
@@ -438,7 +438,7 @@ __global__ void __launch_bounds__(NT, 1)
     __syncthreads();  // S1: proposals ready
     {
       // work items: (proposal q, tile of 32 station pairs), spread over warps
-      const int nd_now = s_nd;
+      const int np_now = s_np;
       int cur_q = -1;
       double sig = 0.0, arr = 0.0;
       int cnt = 0;
@@ -472,7 +472,7 @@ __global__ void __launch_bounds__(NT, 1)
         in.step = (uint32_t)(i0 + q);
         in.wlo = 0;
         in.whi = d.n;
-        score_item<MODE, YT>(d, P, in, tile, nd_now, dslot, dsign, Ts, sig, arr, cnt);
+        score_item<MODE, YT>(d, P, in, tile, np_now, pold, pnew, Ts, sig, arr, cnt);
       }
       if (cur_q >= 0) {
         sig = warp_sum(sig);
@@ -617,17 +617,24 @@ __global__ void __launch_bounds__(NT, 1)
           own[nown++] = e;
         }
         n_local += P.na - P.nr;
-        // own diff vs the phase-start snapshot (frozen-snapshot view)
-        nd = 0;
+        // own diff vs the phase-start snapshot (frozen-snapshot view) as
+        // (start version, current version) pairs
+        np = 0;
         for (int i = 0; i < nstart; ++i)
           if (!st[i].current) {
-            dslot[nd] = st[i].slot;
-            dsign[nd++] = -1;
+            int f = -1;
+            for (int j = 0; j < nown; ++j)
+              if (own[j].id == st[i].id) {
+                f = j;
+                break;
+              }
+            pold[np] = st[i].slot;
+            pnew[np++] = f >= 0 ? own[f].slot : -1;
           }
         for (int i = 0; i < nown; ++i)
-          if (own[i].sidx < 0) {
-            dslot[nd] = own[i].slot;
-            dsign[nd++] = 1;
+          if (own[i].sidx < 0 && own[i].id >= pa.next_base) {
+            pold[np] = -1;
+            pnew[np++] = own[i].slot;
           }
         if (MODE == 1 && P.type == 0 && P.aid != id_base + births - 1)
           atomicAdd(&ctl->id_mismatch, 1ull);
@@ -639,7 +646,7 @@ __global__ void __launch_bounds__(NT, 1)
       s_adv = adv;
       s_accq = accq;
       s_nown = nown;
-      s_nd = nd;
+      s_np = np;
       s_births = births;
       s_nlocal = n_local;
     }
@@ -737,16 +744,18 @@ __global__ void __launch_bounds__(NT, 1)
     // coverage diff for the commit, then this-phase versions that died (sign
     // 0): k_commit returns those slots to the pool, after every CTA of this
     // phase has stopped popping from it
-    DiffEnt* dout = pa.diff + (size_t)slot_idx * MAXDOUT;
-    for (int q = 0; q < nd; ++q) {
-      dout[q].slot = dslot[q];
-      dout[q].sign = dsign[q];
+    DiffPair* dout = pa.diff + (size_t)slot_idx * MAXDOUT;
+    for (int q = 0; q < np; ++q) {
+      dout[q].old_slot = pold[q];
+      dout[q].new_slot = pnew[q];
+      dout[q].kind = 0;
     }
     for (int q = 0; q < nlfree; ++q) {
-      dout[nd + q].slot = lfree[q];
-      dout[nd + q].sign = 0;
+      dout[np + q].old_slot = lfree[q];
+      dout[np + q].new_slot = -1;
+      dout[np + q].kind = 1;
     }
-    pa.diff_cnt[slot_idx] = nd + nlfree;
+    pa.diff_cnt[slot_idx] = np + nlfree;
     atomicAdd(&ctl->scored, n_scored);
     atomicAdd(&ctl->changed, n_changed);
     atomicAdd(&ctl->arrvals, n_arr);
@@ -759,35 +768,53 @@ __global__ void __launch_bounds__(NT, 1)
 // Coverage commit: C += sum over regions of (own_now - own_start) windows;
 // same-color footprints overlap, so packed 32-bit atomics.
 __global__ void k_commit(Dev d, int color, int ncol, int nreg, const int* diff_cnt,
-                         const DiffEnt* diff, int* free_stack, Ctl* ctl) {
+                         const DiffPair* diff, int* free_stack, Ctl* ctl) {
   const int slot_idx = blockIdx.x;
   const int region = color + slot_idx * ncol;
   if (region >= nreg) return;
   const int nd = diff_cnt[slot_idx];
-  const DiffEnt* de = diff + (size_t)slot_idx * MAXDOUT;
+  const DiffPair* de = diff + (size_t)slot_idx * MAXDOUT;
   const double2* pool2 = reinterpret_cast<const double2*>(d.pool);
   for (int q = 0; q < nd; ++q) {
-    const int slot = de[q].slot, sign = de[q].sign;
-    if (sign == 0) continue;
+    if (de[q].kind != 0) continue;
+    const int so = de[q].old_slot, sn = de[q].new_slot;
     for (int p = threadIdx.x; p < d.P2; p += blockDim.x) {
-      const double2 a = pool2[(size_t)slot * d.P2 + p];
-      const Win w0 = 2 * p < d.S ? make_win(d, a.x) : empty_win();
-      const Win w1 = 2 * p + 1 < d.S ? make_win(d, a.y) : empty_win();
-      const int lo = min(w0.hi > w0.lo ? w0.lo : INT_MAX, w1.hi > w1.lo ? w1.lo : INT_MAX);
-      const int hi = max(w0.hi > w0.lo ? w0.hi : INT_MIN, w1.hi > w1.lo ? w1.hi : INT_MIN);
+      Win o0 = empty_win(), o1 = empty_win(), n0 = empty_win(), n1 = empty_win();
+      if (so >= 0) {
+        const double2 a = pool2[(size_t)so * d.P2 + p];
+        if (2 * p < d.S) o0 = make_win(d, a.x);
+        if (2 * p + 1 < d.S) o1 = make_win(d, a.y);
+      }
+      if (sn >= 0) {
+        const double2 a = pool2[(size_t)sn * d.P2 + p];
+        if (2 * p < d.S) n0 = make_win(d, a.x);
+        if (2 * p + 1 < d.S) n1 = make_win(d, a.y);
+      }
+      if (weq(o0, n0)) o0 = n0 = empty_win();  // unchanged at this station
+      if (weq(o1, n1)) o1 = n1 = empty_win();
+      int lo = INT_MAX, hi = INT_MIN;
+      const Win ws[4] = {o0, o1, n0, n1};
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (ws[k].hi > ws[k].lo) {
+          lo = min(lo, ws[k].lo);
+          hi = max(hi, ws[k].hi);
+        }
       for (int r = lo; r < hi; ++r) {
-        const int inc = sign * inw(r, w0) + sign * inw(r, w1) * 65536;
+        const int inc = (inw(r, n0) - inw(r, o0)) + (inw(r, n1) - inw(r, o1)) * 65536;
         if (inc) atomicAdd(d.cov + (size_t)r * d.P2 + p, (unsigned)inc);
       }
     }
   }
   __syncthreads();
   if (threadIdx.x == 0)
-    for (int q = 0; q < nd; ++q)
-      if (de[q].sign <= 0) {
+    for (int q = 0; q < nd; ++q) {
+      const int slot = de[q].old_slot;
+      if (slot >= 0) {  // replaced / dead start versions and recycled versions
         const int top = atomicAdd(&ctl->free_top, 1);
-        free_stack[top] = de[q].slot;
+        free_stack[top] = slot;
       }
+    }
 }
 
 // block-wide exclusive scan of one int per thread (1024 threads)
@@ -944,7 +971,7 @@ __global__ void __launch_bounds__(NT, 1)
   in.sweep = in.region = in.step = 0;
   double sig = 0.0, arr = 0.0;
   int cnt = 0;
-  const int T_per = (d.P2 + 31) / 32;
+  const int T_per = (d.S_pad + 31) / 32;
   for (int t = warp; t < T_per; t += NW)
     score_item<1, YT>(d, P, in, t, 0, nullptr, nullptr, Ts, sig, arr, cnt);
   sig = warp_sum(sig);
@@ -1702,7 +1729,7 @@ extern "C" int seis_run_chromatic(seis_engine* e, const seis_sampler_cfg* sc, in
     int* births_cnt = static_cast<int*>(alloc((size_t)n_slots * 4));
     OutEv* births = static_cast<OutEv*>(alloc((size_t)n_slots * MAXOWN * sizeof(OutEv)));
     int* diff_cnt = static_cast<int*>(alloc((size_t)n_slots * 4));
-    DiffEnt* diff = static_cast<DiffEnt*>(alloc((size_t)n_slots * MAXDOUT * sizeof(DiffEnt)));
+    DiffPair* diff = static_cast<DiffPair*>(alloc((size_t)n_slots * MAXDOUT * sizeof(DiffPair)));
     seis_tape_step* d_tape = nullptr;
     double* d_tarr = nullptr;
     seis_step_out* d_out = nullptr;

@@ -24,8 +24,8 @@ constexpr int NT = 512;          // threads per region CTA
 constexpr int MSPEC = 4;         // speculative proposals evaluated per round
 constexpr int NW = NT / 32;
 constexpr int MAXOWN = 128;      // events a region may hold during a phase
-constexpr int MAXDIFF = 2 * MAXOWN;
-constexpr int MAXDOUT = 3 * MAXOWN;  // diff entries + recycled slots per region
+constexpr int MAXDIFF = 2 * MAXOWN;  // diff pairs a region may hold
+constexpr int MAXDOUT = 3 * MAXOWN;  // diff pairs + recycled slots per region
 constexpr int TBL = 1024;        // coverage counts whose {dL, dI} rows live in smem
 constexpr int BANDMAX = 256;     // rows of the generic diff-correction scratch
 constexpr double kLog2Pi = 1.8378770664093454835606594728112;
@@ -75,8 +75,12 @@ struct OutEv {
   int slot, pad;
 };
 
-struct DiffEnt {
-  int slot, sign;
+// One entry of a region's diff against the phase-start snapshot: the
+// start version (old_slot, -1 for a birth) and the current version
+// (new_slot, -1 for a death). kind 1 = slot to recycle only (a this-phase
+// version that died).
+struct DiffPair {
+  int old_slot, new_slot, kind, pad;
 };
 
 struct Ctl {
@@ -101,7 +105,7 @@ struct PhaseArgs {
   int* births_cnt;                 // [n_slots]
   OutEv* births;                   // [n_slots][MAXOWN]
   int* diff_cnt;                   // [n_slots]
-  DiffEnt* diff;                   // [n_slots][MAXDOUT]
+  DiffPair* diff;                  // [n_slots][MAXDOUT]
   int* free_stack;
   const seis_tape_step* tape;
   const double* tape_arr;

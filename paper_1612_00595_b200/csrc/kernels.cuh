@@ -96,262 +96,230 @@ __device__ __forceinline__ double term(const Dev& d, const double2* Ts, double y
 
 template <int N>
 struct Wins {
-  Win w[N > 0 ? N : 1][2];
+  Win w[N > 0 ? N : 1];
 };
 
-// Rows [blo, bhi) of one station pair, RU rows' loads in flight at a time.
-// dc = added - removed windows covering the row; c = phase-start count + own
-// diff correction (the region's frozen view); only rows with dc != 0 load.
+// Rows [blo, bhi) of one station (one lane), RU rows' loads in flight at a
+// time. dc = added - removed windows covering the row; c = phase-start count
+// + own diff correction (the region's frozen view); only rows with dc != 0
+// load. Time-major layout: the warp's 32 stations of a row are contiguous.
 template <int NR, int NA, int ND, typename YT>
-__device__ __forceinline__ void band(const Dev& d, int p, int blo, int bhi, const Wins<NR>& R,
+__device__ __forceinline__ void band(const Dev& d, int j, int blo, int bhi, const Wins<NR>& R,
                                      const Wins<NA>& A, const Wins<ND>& D,
                                      const int (&sg)[ND > 0 ? ND : 1], const double2* Ts,
                                      double& sig, int& cnt) {
-  using T2 = typename Y2<YT>::T;
-  constexpr int RU = 4;
-  const T2* __restrict__ yp = reinterpret_cast<const T2*>(d.y) + (size_t)blo * d.P2 + p;
-  const uint32_t* __restrict__ cp = d.cov + (size_t)blo * d.P2 + p;
-  const size_t stride = (size_t)d.P2;
+  constexpr int RU = sizeof(YT) == 4 ? 8 : 4;
+  const int stride = d.S_pad;
+  const YT* __restrict__ yp = reinterpret_cast<const YT*>(d.y) + (size_t)blo * stride + j;
+  const uint16_t* __restrict__ cp =
+      reinterpret_cast<const uint16_t*>(d.cov) + (size_t)blo * stride + j;
   for (int r0 = blo; r0 < bhi; r0 += RU, yp += RU * stride, cp += RU * stride) {
-    int dc0[RU], dc1[RU];
+    int dc[RU];
 #pragma unroll
     for (int k = 0; k < RU; ++k) {
       const int r = r0 + k;  // rows past bhi lie outside every window: dc = 0
-      int a0 = 0, a1 = 0;
+      int a = 0;
 #pragma unroll
-      for (int a = 0; a < NA; ++a) {
-        a0 += inw(r, A.w[a][0]);
-        a1 += inw(r, A.w[a][1]);
-      }
+      for (int q = 0; q < NA; ++q) a += inw(r, A.w[q]);
 #pragma unroll
-      for (int q = 0; q < NR; ++q) {
-        a0 -= inw(r, R.w[q][0]);
-        a1 -= inw(r, R.w[q][1]);
-      }
-      dc0[k] = a0;
-      dc1[k] = a1;
+      for (int q = 0; q < NR; ++q) a -= inw(r, R.w[q]);
+      dc[k] = a;
     }
-    uint32_t w[RU];
-    T2 yy[RU];
+    unsigned short c[RU];
+    YT y[RU];
 #pragma unroll
     for (int k = 0; k < RU; ++k)
-      if (dc0[k] | dc1[k]) {
-        w[k] = __ldg(cp + k * stride);
-        yy[k] = __ldg(yp + k * stride);
+      if (dc[k]) {
+        c[k] = __ldg(cp + k * stride);
+        y[k] = __ldg(yp + k * stride);
       }
 #pragma unroll
     for (int k = 0; k < RU; ++k)
-      if (dc0[k] | dc1[k]) {
-        const int r = r0 + k;
-        int c0 = (int)(w[k] & 0xffffu), c1 = (int)(w[k] >> 16);
+      if (dc[k]) {
+        int cc = (int)c[k];
 #pragma unroll
-        for (int q = 0; q < ND; ++q) {
-          c0 += sg[q] * inw(r, D.w[q][0]);
-          c1 += sg[q] * inw(r, D.w[q][1]);
-        }
-        if (dc0[k]) {
-          sig += term(d, Ts, (double)yy[k].x, c0, dc0[k]);
-          ++cnt;
-        }
-        if (dc1[k]) {
-          sig += term(d, Ts, (double)yy[k].y, c1, dc1[k]);
-          ++cnt;
-        }
+        for (int q = 0; q < ND; ++q) cc += sg[q] * inw(r0 + k, D.w[q]);
+        sig += term(d, Ts, (double)y[k], cc, dc[k]);
+        ++cnt;
       }
   }
 }
 
-// Many own diff entries: the correction of the band rows is accumulated in a
-// per-thread scratch column first (nd > 2).
+// Many effective diff windows at a station (> 4): the correction of the band
+// rows is accumulated in a per-thread scratch column first (rare).
 template <int NR, int NA, typename YT>
-__device__ __noinline__ void band_generic(const Dev& d, int p, int blo, int bhi,
-                                          const Wins<NR> R, const Wins<NA> A, int nd,
-                                          const int* dslot, const int* dsign,
-                                          const double2* Ts, double& sig, int& cnt) {
-  using T2 = typename Y2<YT>::T;
-  const T2* __restrict__ y2 = reinterpret_cast<const T2*>(d.y);
-  const double2* pool2 = reinterpret_cast<const double2*>(d.pool);
-  signed char corr[2][BANDMAX];
+__device__ __noinline__ void band_generic(const Dev& d, int j, bool v, int blo, int bhi,
+                                          const Wins<NR> R, const Wins<NA> A, int np,
+                                          const int* pold, const int* pnew,
+                                          const double2* Ts, double* out_sig, int* out_cnt) {
+  const YT* __restrict__ y = reinterpret_cast<const YT*>(d.y);
+  const uint16_t* __restrict__ c16 = reinterpret_cast<const uint16_t*>(d.cov);
+  signed char corr[BANDMAX];
+  double sig = 0.0;
+  int cnt = 0;
   for (int c0 = blo; c0 < bhi; c0 += BANDMAX) {
     const int c1 = min(bhi, c0 + BANDMAX);
-    for (int i = 0; i < c1 - c0; ++i) corr[0][i] = corr[1][i] = 0;
-    for (int q = 0; q < nd; ++q) {
-      const double2 a = pool2[(size_t)dslot[q] * d.P2 + p];
-      const Win w0 = 2 * p < d.S ? make_win(d, a.x) : empty_win();
-      const Win w1 = 2 * p + 1 < d.S ? make_win(d, a.y) : empty_win();
-      for (int r = max(w0.lo, c0); r < min(w0.hi, c1); ++r) corr[0][r - c0] += dsign[q];
-      for (int r = max(w1.lo, c0); r < min(w1.hi, c1); ++r) corr[1][r - c0] += dsign[q];
+    for (int i = 0; i < c1 - c0; ++i) corr[i] = 0;
+    for (int q = 0; q < np && v; ++q) {
+      const Win wo = pold[q] >= 0 ? make_win(d, d.pool[(size_t)pold[q] * d.S_pad + j]) : empty_win();
+      const Win wn = pnew[q] >= 0 ? make_win(d, d.pool[(size_t)pnew[q] * d.S_pad + j]) : empty_win();
+      if (weq(wo, wn)) continue;
+      for (int r = max(wo.lo, c0); r < min(wo.hi, c1); ++r) corr[r - c0] -= 1;
+      for (int r = max(wn.lo, c0); r < min(wn.hi, c1); ++r) corr[r - c0] += 1;
     }
     for (int r = c0; r < c1; ++r) {
-      int dc0 = 0, dc1 = 0;
-      for (int a = 0; a < NA; ++a) {
-        dc0 += inw(r, A.w[a][0]);
-        dc1 += inw(r, A.w[a][1]);
-      }
-      for (int q = 0; q < NR; ++q) {
-        dc0 -= inw(r, R.w[q][0]);
-        dc1 -= inw(r, R.w[q][1]);
-      }
-      if (dc0 | dc1) {
-        const size_t off = (size_t)r * d.P2 + p;
-        const uint32_t w = __ldg(d.cov + off);
-        const T2 yy = __ldg(y2 + off);
-        const int co0 = (int)(w & 0xffffu) + corr[0][r - c0];
-        const int co1 = (int)(w >> 16) + corr[1][r - c0];
-        if (dc0) {
-          sig += term(d, Ts, (double)yy.x, co0, dc0);
-          ++cnt;
-        }
-        if (dc1) {
-          sig += term(d, Ts, (double)yy.y, co1, dc1);
-          ++cnt;
-        }
+      int dc = 0;
+      for (int q = 0; q < NA; ++q) dc += inw(r, A.w[q]);
+      for (int q = 0; q < NR; ++q) dc -= inw(r, R.w[q]);
+      if (dc) {
+        const size_t off = (size_t)r * d.S_pad + j;
+        const int co = (int)__ldg(c16 + off) + corr[r - c0];
+        sig += term(d, Ts, (double)__ldg(y + off), co, dc);
+        ++cnt;
       }
     }
   }
+  *out_sig += sig;
+  *out_cnt += cnt;
 }
 
-template <int NR, int NA, int ND, typename YT>
-__device__ __forceinline__ void band_diff(const Dev& d, int p, bool v0, bool v1, int blo, int bhi,
-                                          const Wins<NR>& R, const Wins<NA>& A, int nd,
-                                          const int* dslot, const int* dsign, const double2* Ts,
-                                          double& sig, int& cnt) {
-  Wins<ND> D;
-  int sg[ND > 0 ? ND : 1];
-  const double2* pool2 = reinterpret_cast<const double2*>(d.pool);
-#pragma unroll
-  for (int q = 0; q < ND; ++q) {
-    D.w[q][0] = D.w[q][1] = empty_win();
-    sg[q] = 0;
-    if (q < nd) {
-      const double2 a = pool2[(size_t)dslot[q] * d.P2 + p];
-      if (v0) D.w[q][0] = make_win(d, a.x);
-      if (v1) D.w[q][1] = make_win(d, a.y);
-      sg[q] = dsign[q];
-    }
-  }
-  band<NR, NA, ND, YT>(d, p, blo, bhi, R, A, D, sg, Ts, sig, cnt);
-}
-
-// One station pair of one proposal (density.hpp:239-301): arrival densities
-// of the added/removed versions (arr += added - removed) and the per-sample
-// terms where the coverage changes (sig). Called by a whole warp (p = tile
-// base + lane), so the band reduction is warp-uniform.
+// One station of one proposal (density.hpp:239-301): arrival densities of
+// the added/removed versions (arr += added - removed) and the per-sample
+// terms where the coverage changes (sig). Called by a whole warp
+// (j = tile base + lane) so the band reduction is warp-uniform.
 template <int NR, int NA, typename YT>
-__device__ __noinline__ void pair_item(const Dev& d, const Prop& P, const PassIn& in, int p,
-                                          int nd, const int* dslot, const int* dsign,
-                                          const double2* Ts, double& sig, double& arr,
-                                          int& cnt) {
-  const bool pv = p < d.P2;
-  const bool v0 = pv && 2 * p < d.S, v1 = pv && 2 * p + 1 < d.S;
-  const double2* pool2 = reinterpret_cast<const double2*>(d.pool);
+__device__ __forceinline__ void station_item(const Dev& d, const Prop& P, const PassIn& in,
+                                             int j, int np, const int* pold, const int* pnew,
+                                             const double2* Ts, double& sig, double& arr,
+                                             int& cnt) {
+  const bool v = j < d.S;
   Wins<NR> R;
   Wins<NA> A;
-  double s0 = 0.0, s1 = 0.0;
-  if (pv) {
-    const double2 s = reinterpret_cast<const double2*>(d.stations)[p];
-    s0 = s.x;
-    s1 = s.y;
-  }
-  double ra[NR > 0 ? NR : 1][2];
+  const double s = v ? d.stations[j] : 0.0;
+  double ra[NR > 0 ? NR : 1];
 #pragma unroll
   for (int q = 0; q < NR; ++q) {
-    R.w[q][0] = R.w[q][1] = empty_win();
-    ra[q][0] = ra[q][1] = 0.0;
-    if (pv) {
-      const double2 v = pool2[(size_t)P.rslot[q] * d.P2 + p];
-      ra[q][0] = v.x;
-      ra[q][1] = v.y;
-      if (v0) {
-        R.w[q][0] = clampw(make_win(d, v.x), in.wlo, in.whi);
-        arr -= arr_logpdf(d, v.x, arrival_mean(d, P.rx[q], P.rt[q], s0));
-      }
-      if (v1) {
-        R.w[q][1] = clampw(make_win(d, v.y), in.wlo, in.whi);
-        arr -= arr_logpdf(d, v.y, arrival_mean(d, P.rx[q], P.rt[q], s1));
-      }
+    R.w[q] = empty_win();
+    ra[q] = 0.0;
+    if (v && q < P.nr) {
+      ra[q] = d.pool[(size_t)P.rslot[q] * d.S_pad + j];
+      R.w[q] = clampw(make_win(d, ra[q]), in.wlo, in.whi);
+      arr -= arr_logpdf(d, ra[q], arrival_mean(d, P.rx[q], P.rt[q], s));
     }
   }
 #pragma unroll
   for (int a = 0; a < NA; ++a) {
-    A.w[a][0] = A.w[a][1] = empty_win();
-    if (pv) {
-      double a0 = 0.0, a1 = 0.0;
-      const double m0 = arrival_mean(d, P.ax[a], P.at[a], s0);
-      const double m1 = arrival_mean(d, P.ax[a], P.at[a], s1);
+    A.w[a] = empty_win();
+    if (v && a < P.na) {
+      double aa;
+      const double m = arrival_mean(d, P.ax[a], P.at[a], s);
       if (in.src == SRC_BIRTH) {
-        float z0, z1;
-        seis_normal_pair(in.seed, in.sweep, in.region, in.step, (uint32_t)p, &z0, &z1);
-        a0 = m0 + d.sigma * (double)z0;
-        a1 = m1 + d.sigma * (double)z1;
+        aa = m + d.sigma * (double)seis_normal(in.seed, in.sweep, in.region, in.step,
+                                               (uint32_t)j);
       } else if (in.src == SRC_SHIFT) {
         const int q = a < NR ? a : 0;
-        a0 = ra[q][0] + (m0 - arrival_mean(d, P.rx[q], P.rt[q], s0));
-        a1 = ra[q][1] + (m1 - arrival_mean(d, P.rx[q], P.rt[q], s1));
+        aa = ra[q] + (m - arrival_mean(d, P.rx[q], P.rt[q], s));
       } else {
-        if (v0) a0 = in.rows[a][2 * p];
-        if (v1) a1 = in.rows[a][2 * p + 1];
+        aa = in.rows[a][j];
       }
-      if (v0) {
-        A.w[a][0] = clampw(make_win(d, a0), in.wlo, in.whi);
-        arr += arr_logpdf(d, a0, m0);
-      }
-      if (v1) {
-        A.w[a][1] = clampw(make_win(d, a1), in.wlo, in.whi);
-        arr += arr_logpdf(d, a1, m1);
-      }
+      A.w[a] = clampw(make_win(d, aa), in.wlo, in.whi);
+      arr += arr_logpdf(d, aa, m);
     }
   }
   // windows that do not move leave every count unchanged
-  if (NR == NA && NR > 0) {
+  if (NR == NA && NR > 0 && P.nr == P.na) {
+    bool same;
+    if (NR == 1)
+      same = weq(A.w[0], R.w[0]);
+    else
+      same = (weq(A.w[0], R.w[0]) && weq(A.w[NA - 1], R.w[NR - 1])) ||
+             (weq(A.w[0], R.w[NR - 1]) && weq(A.w[NA - 1], R.w[0]));
+    if (same) {
 #pragma unroll
-    for (int s = 0; s < 2; ++s) {
-      bool same;
-      if (NR == 1)
-        same = weq(A.w[0][s], R.w[0][s]);
-      else
-        same = (weq(A.w[0][s], R.w[0][s]) && weq(A.w[NA - 1][s], R.w[NR - 1][s])) ||
-               (weq(A.w[0][s], R.w[NR - 1][s]) && weq(A.w[NA - 1][s], R.w[0][s]));
-      if (same) {
+      for (int q = 0; q < NR; ++q) R.w[q] = empty_win();
 #pragma unroll
-        for (int q = 0; q < NR; ++q) R.w[q][s] = empty_win();
-#pragma unroll
-        for (int a = 0; a < NA; ++a) A.w[a][s] = empty_win();
-      }
+      for (int a = 0; a < NA; ++a) A.w[a] = empty_win();
     }
   }
   int lo = INT_MAX, hi = INT_MIN;
 #pragma unroll
-  for (int s = 0; s < 2; ++s) {
+  for (int a = 0; a < NA; ++a)
+    if (A.w[a].hi > A.w[a].lo) {
+      lo = min(lo, A.w[a].lo);
+      hi = max(hi, A.w[a].hi);
+    }
 #pragma unroll
-    for (int a = 0; a < NA; ++a)
-      if (A.w[a][s].hi > A.w[a][s].lo) {
-        lo = min(lo, A.w[a][s].lo);
-        hi = max(hi, A.w[a][s].hi);
-      }
-#pragma unroll
-    for (int q = 0; q < NR; ++q)
-      if (R.w[q][s].hi > R.w[q][s].lo) {
-        lo = min(lo, R.w[q][s].lo);
-        hi = max(hi, R.w[q][s].hi);
-      }
-  }
+  for (int q = 0; q < NR; ++q)
+    if (R.w[q].hi > R.w[q].lo) {
+      lo = min(lo, R.w[q].lo);
+      hi = max(hi, R.w[q].hi);
+    }
   const int blo = __reduce_min_sync(0xffffffffu, lo);
   const int bhi = __reduce_max_sync(0xffffffffu, hi);
   if (blo >= bhi) return;
-  if (nd == 0)
-    band_diff<NR, NA, 0, YT>(d, p, v0, v1, blo, bhi, R, A, nd, dslot, dsign, Ts, sig, cnt);
-  else if (nd <= 2)
-    band_diff<NR, NA, 2, YT>(d, p, v0, v1, blo, bhi, R, A, nd, dslot, dsign, Ts, sig, cnt);
-  else
-    band_generic<NR, NA, YT>(d, p, blo, bhi, R, A, nd, dslot, dsign, Ts, sig, cnt);
+  // effective diff windows at this station: a (start, current) version pair
+  // whose windows coincide here (an arrival move elsewhere) corrects nothing
+  Wins<4> D;
+  int sg[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    D.w[q] = empty_win();
+    sg[q] = 0;
+  }
+  int nw = 0;
+  for (int q = 0; q < np && v; ++q) {
+    const Win wo = pold[q] >= 0 ? make_win(d, d.pool[(size_t)pold[q] * d.S_pad + j]) : empty_win();
+    const Win wn = pnew[q] >= 0 ? make_win(d, d.pool[(size_t)pnew[q] * d.S_pad + j]) : empty_win();
+    if (weq(wo, wn)) continue;
+    if (wo.hi > wo.lo) {
+      if (nw < 4) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (k == nw) {
+            D.w[k] = wo;
+            sg[k] = -1;
+          }
+      }
+      ++nw;
+    }
+    if (wn.hi > wn.lo) {
+      if (nw < 4) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (k == nw) {
+            D.w[k] = wn;
+            sg[k] = 1;
+          }
+      }
+      ++nw;
+    }
+  }
+  const int nwmax = __reduce_max_sync(0xffffffffu, (unsigned)nw);
+  if (nwmax == 0) {
+    Wins<0> D0;
+    int sg0[1];
+    band<NR, NA, 0, YT>(d, j, blo, bhi, R, A, D0, sg0, Ts, sig, cnt);
+  } else if (nwmax <= 2) {
+    Wins<2> D2;
+    int sg2[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      D2.w[q] = D.w[q];
+      sg2[q] = sg[q];
+    }
+    band<NR, NA, 2, YT>(d, j, blo, bhi, R, A, D2, sg2, Ts, sig, cnt);
+  } else if (nwmax <= 4) {
+    band<NR, NA, 4, YT>(d, j, blo, bhi, R, A, D, sg, Ts, sig, cnt);
+  } else {
+    band_generic<NR, NA, YT>(d, j, v, blo, bhi, R, A, np, pold, pnew, Ts, &sig, &cnt);
+  }
 }
 
 // Arrival move (proposals.hpp:161-174) in production: only station st moves;
 // the warp's lanes take rows.
 template <typename YT>
-__device__ __forceinline__ void arrival_item(const Dev& d, const Prop& P, int nd,
-                                             const int* dslot, const int* dsign,
+__device__ __forceinline__ void arrival_item(const Dev& d, const Prop& P, int np,
+                                             const int* pold, const int* pnew,
                                              const double2* Ts, double& sig, double& arr,
                                              int& cnt) {
   const int lane = threadIdx.x & 31;
@@ -370,43 +338,36 @@ __device__ __forceinline__ void arrival_item(const Dev& d, const Prop& P, int nd
     const int dc = inw(r, wn) - inw(r, wo);
     if (!dc) continue;
     int co = (int)c16[(size_t)r * d.S_pad + st];
-    for (int q = 0; q < nd; ++q) {
-      const Win w = make_win(d, d.pool[(size_t)dslot[q] * d.S_pad + st]);
-      co += dsign[q] * inw(r, w);
+    for (int q = 0; q < np; ++q) {
+      if (pold[q] >= 0) co -= inw(r, make_win(d, d.pool[(size_t)pold[q] * d.S_pad + st]));
+      if (pnew[q] >= 0) co += inw(r, make_win(d, d.pool[(size_t)pnew[q] * d.S_pad + st]));
     }
     sig += term(d, Ts, (double)y[(size_t)r * d.S_pad + st], co, dc);
     ++cnt;
   }
 }
 
-// Dispatch one work item (tile of 32 station pairs) of proposal P.
+// Dispatch one work item (tile of 32 stations) of proposal P.
 template <int MODE, typename YT>
 __device__ __forceinline__ void score_item(const Dev& d, const Prop& P, const PassIn& in,
-                                           int tile, int nd, const int* dslot,
-                                           const int* dsign, const double2* Ts, double& sig,
+                                           int tile, int np, const int* pold,
+                                           const int* pnew, const double2* Ts, double& sig,
                                            double& arr, int& cnt) {
   if (P.skip) return;
-  const int p = tile * 32 + (threadIdx.x & 31);
+  const int j = tile * 32 + (threadIdx.x & 31);
   if (MODE == 0 && P.type == 3) {
-    if (tile == 0) arrival_item<YT>(d, P, nd, dslot, dsign, Ts, sig, arr, cnt);
+    if (tile == 0) arrival_item<YT>(d, P, np, pold, pnew, Ts, sig, arr, cnt);
     return;
   }
-  if (P.nr == 0 && P.na == 1)
-    pair_item<0, 1, YT>(d, P, in, p, nd, dslot, dsign, Ts, sig, arr, cnt);
-  else if (P.nr == 1 && P.na == 0)
-    pair_item<1, 0, YT>(d, P, in, p, nd, dslot, dsign, Ts, sig, arr, cnt);
-  else if (P.nr == 1 && P.na == 1)
-    pair_item<1, 1, YT>(d, P, in, p, nd, dslot, dsign, Ts, sig, arr, cnt);
-  else if (P.nr == 2 && P.na == 2)
-    pair_item<2, 2, YT>(d, P, in, p, nd, dslot, dsign, Ts, sig, arr, cnt);
-  else if (P.nr == 2 && P.na == 0)
-    pair_item<2, 0, YT>(d, P, in, p, nd, dslot, dsign, Ts, sig, arr, cnt);
-  else if (P.nr == 0 && P.na == 2)
-    pair_item<0, 2, YT>(d, P, in, p, nd, dslot, dsign, Ts, sig, arr, cnt);
-  else if (P.nr == 1 && P.na == 2)
-    pair_item<1, 2, YT>(d, P, in, p, nd, dslot, dsign, Ts, sig, arr, cnt);
-  else if (P.nr == 2 && P.na == 1)
-    pair_item<2, 1, YT>(d, P, in, p, nd, dslot, dsign, Ts, sig, arr, cnt);
+  const int shape = P.nr * 3 + P.na;
+  if (shape == 1)  // birth
+    station_item<0, 1, YT>(d, P, in, j, np, pold, pnew, Ts, sig, arr, cnt);
+  else if (shape == 3)  // death
+    station_item<1, 0, YT>(d, P, in, j, np, pold, pnew, Ts, sig, arr, cnt);
+  else if (shape == 4)  // location / arrival
+    station_item<1, 1, YT>(d, P, in, j, np, pold, pnew, Ts, sig, arr, cnt);
+  else  // joint pair, and any other change of <= 2 removed / 2 added events
+    station_item<2, 2, YT>(d, P, in, j, np, pold, pnew, Ts, sig, arr, cnt);
 }
 
 }  // namespace seis
