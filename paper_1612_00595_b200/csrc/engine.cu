@@ -334,8 +334,7 @@ __device__ void gen_proposal(const Dev& d, const Samp& sp, const PhaseArgs& pa, 
 template <typename YT, int MODE>
 __global__ void __launch_bounds__(NT, 1)
     k_phase(const Dev d, const Samp sp, const PhaseArgs pa, Ctl* ctl, int stamp) {
-  extern __shared__ __align__(16) unsigned char smem_dyn[];
-  double2* Ts = reinterpret_cast<double2*>(smem_dyn);  // [TBL * 4] {dL, dI}
+  __shared__ double2 Ts[TBL * 4];  // {dL, dI} per (count, dc)
   __shared__ OwnEv own[MAXOWN];
   __shared__ StartEv st[MAXOWN];
   __shared__ int pold[MAXDIFF], pnew[MAXDIFF];
@@ -915,8 +914,7 @@ template <typename YT>
 __global__ void __launch_bounds__(NT, 1)
     k_score_batch(const Dev d, Table tab, const Ctl* ctl, const ChangeDev* ch,
                   const double* rows, double* out) {
-  extern __shared__ __align__(16) unsigned char smem_dyn[];
-  double2* Ts = reinterpret_cast<double2*>(smem_dyn);
+  __shared__ double2 Ts[TBL * 4];
   __shared__ Prop P;
   __shared__ double rsig[NW], rarr[NW];
   __shared__ int s_bad;
@@ -1092,7 +1090,7 @@ using namespace seis;
 namespace {
 
 thread_local std::string g_err;
-constexpr int kPhaseSmem = TBL * 4 * (int)sizeof(double2);
+constexpr int kPhaseSmem = 0;  // all shared memory is static
 
 int fail(int code, const std::string& m) {
   g_err = m;
@@ -1386,13 +1384,6 @@ int seis_engine_create(const seis_model_cfg* cfg, const double* stations, int64_
     d.logi = e->logi;
     d.logi_n = tab_n;
     d.pool_cap = e->cap;
-    const int smem = TBL * 4 * (int)sizeof(double2);
-    ck(cudaFuncSetAttribute(k_phase<float, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "attr");
-    ck(cudaFuncSetAttribute(k_phase<float, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "attr");
-    ck(cudaFuncSetAttribute(k_phase<double, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "attr");
-    ck(cudaFuncSetAttribute(k_phase<double, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "attr");
-    ck(cudaFuncSetAttribute(k_score_batch<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "attr");
-    ck(cudaFuncSetAttribute(k_score_batch<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "attr");
     upload_signals(e, signals);
   });
   if (rc) {

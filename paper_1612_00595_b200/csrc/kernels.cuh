@@ -85,13 +85,19 @@ __device__ __forceinline__ double warp_sum(double v) {
 // Per-sample likelihood change for coverage c -> c + dc (density.hpp:286-301):
 // (L[c+dc] - y^2 I[c+dc]) - (L[c] - y^2 I[c]) = dL - y^2 dI with the per-count
 // differences precomputed on the host from glibc log (one 16-byte lookup).
+__device__ __forceinline__ int dc_code(int dc) { return dc > 0 ? dc + 1 : dc + 2; }
+
 __device__ __forceinline__ double term(const Dev& d, const double2* Ts, double y, int c, int dc) {
-  const int code = dc < 0 ? dc + 2 : dc + 1;  // dc in {-2,-1,1,2} -> 0..3
-  const int idx = c * 4 + code;
-  double2 e = Ts[min(idx, TBL * 4 - 1)];
-  if (c >= TBL) e = d.Dg[idx];  // counts beyond the shared-memory table (rare)
+  const int idx = c * 4 + dc_code(dc);
+  const double2 e = c < TBL ? Ts[idx] : d.Dg[idx];
   const double y2 = y * y;
   return fma(-y2, e.y, e.x);
+}
+
+// shared-memory-only lookup; the caller guarantees c < TBL
+__device__ __forceinline__ double term_fast(const double2* Ts, double y, int c, int dc) {
+  const double2 e = Ts[c * 4 + dc_code(dc)];
+  return fma(-(y * y), e.y, e.x);
 }
 
 template <int N>
@@ -100,20 +106,25 @@ struct Wins {
 };
 
 // Rows [blo, bhi) of one station (one lane), RU rows' loads in flight at a
-// time. dc = added - removed windows covering the row; c = phase-start count
-// + own diff correction (the region's frozen view); only rows with dc != 0
-// load. Time-major layout: the warp's 32 stations of a row are contiguous.
+// time, branch-free: dc = added - removed windows covering the row; c =
+// phase-start count + own diff correction (the region's frozen view); only
+// rows with dc != 0 load. Time-major layout: the warp's 32 stations of a row
+// are contiguous. Counts at or above the shared table fall back to a slow
+// pass over the whole item (rare: > TBL - 3 overlapping events).
 template <int NR, int NA, int ND, typename YT>
 __device__ __forceinline__ void band(const Dev& d, int j, int blo, int bhi, const Wins<NR>& R,
                                      const Wins<NA>& A, const Wins<ND>& D,
                                      const int (&sg)[ND > 0 ? ND : 1], const double2* Ts,
                                      double& sig, int& cnt) {
-  constexpr int RU = sizeof(YT) == 4 ? 8 : 4;
+  constexpr int RU = 4;
   const int stride = d.S_pad;
-  const YT* __restrict__ yp = reinterpret_cast<const YT*>(d.y) + (size_t)blo * stride + j;
-  const uint16_t* __restrict__ cp =
-      reinterpret_cast<const uint16_t*>(d.cov) + (size_t)blo * stride + j;
-  for (int r0 = blo; r0 < bhi; r0 += RU, yp += RU * stride, cp += RU * stride) {
+  const YT* __restrict__ y = reinterpret_cast<const YT*>(d.y);
+  const uint16_t* __restrict__ c16 = reinterpret_cast<const uint16_t*>(d.cov);
+  double s_loc = 0.0;
+  int c_loc = 0;
+  bool big = false;
+  int off = blo * stride + j;
+  for (int r0 = blo; r0 < bhi; r0 += RU, off += RU * stride) {
     int dc[RU];
 #pragma unroll
     for (int k = 0; k < RU; ++k) {
@@ -125,24 +136,53 @@ __device__ __forceinline__ void band(const Dev& d, int j, int blo, int bhi, cons
       for (int q = 0; q < NR; ++q) a -= inw(r, R.w[q]);
       dc[k] = a;
     }
-    unsigned short c[RU];
-    YT y[RU];
+    int c[RU];
+    float yv[RU];
+    double yd[RU];
 #pragma unroll
-    for (int k = 0; k < RU; ++k)
-      if (dc[k]) {
-        c[k] = __ldg(cp + k * stride);
-        y[k] = __ldg(yp + k * stride);
-      }
+    for (int k = 0; k < RU; ++k) {
+      c[k] = dc[k] ? (int)__ldg(c16 + off + k * stride) : 0;
+      if (sizeof(YT) == 4)
+        yv[k] = dc[k] ? (float)__ldg(y + off + k * stride) : 0.0f;
+      else
+        yd[k] = dc[k] ? (double)__ldg(y + off + k * stride) : 0.0;
+    }
 #pragma unroll
-    for (int k = 0; k < RU; ++k)
-      if (dc[k]) {
-        int cc = (int)c[k];
+    for (int k = 0; k < RU; ++k) {
+      int cc = c[k];
 #pragma unroll
-        for (int q = 0; q < ND; ++q) cc += sg[q] * inw(r0 + k, D.w[q]);
-        sig += term(d, Ts, (double)y[k], cc, dc[k]);
-        ++cnt;
-      }
+      for (int q = 0; q < ND; ++q) cc += sg[q] * inw(r0 + k, D.w[q]);
+      big |= cc >= TBL - 2;
+      const int ci = min(cc, TBL - 3) & (dc[k] ? 0x7fffffff : 0);
+      const int dk = dc[k] ? dc[k] : 1;
+      const double yy = sizeof(YT) == 4 ? (double)yv[k] : yd[k];
+      const double t = term_fast(Ts, yy, ci, dk);
+      s_loc += dc[k] ? t : 0.0;
+      c_loc += dc[k] ? 1 : 0;
+    }
   }
+  if (__any_sync(0xffffffffu, big)) {
+    // slow exact pass with the global table
+    s_loc = 0.0;
+    c_loc = 0;
+    for (int r = blo; r < bhi; ++r) {
+      int dcv = 0;
+#pragma unroll
+      for (int q = 0; q < NA; ++q) dcv += inw(r, A.w[q]);
+#pragma unroll
+      for (int q = 0; q < NR; ++q) dcv -= inw(r, R.w[q]);
+      if (dcv) {
+        const int o = r * stride + j;
+        int cc = (int)__ldg(c16 + o);
+#pragma unroll
+        for (int q = 0; q < ND; ++q) cc += sg[q] * inw(r, D.w[q]);
+        s_loc += term(d, Ts, (double)__ldg(y + o), cc, dcv);
+        ++c_loc;
+      }
+    }
+  }
+  sig += s_loc;
+  cnt += c_loc;
 }
 
 // Many effective diff windows at a station (> 4): the correction of the band
