@@ -100,6 +100,11 @@ __device__ __forceinline__ double term_fast(const double2* Ts, double y, int c, 
   return fma(-(y * y), e.y, e.x);
 }
 
+#ifndef SEIS_SCATTER_SINGLE
+#define SEIS_SCATTER_SINGLE 1
+#endif
+constexpr bool kScatterSingle = SEIS_SCATTER_SINGLE;
+
 template <int N>
 struct Wins {
   Win w[N > 0 ? N : 1];
@@ -179,6 +184,84 @@ __device__ __forceinline__ void band(const Dev& d, int j, int blo, int bhi, cons
         s_loc += term(d, Ts, (double)__ldg(y + o), cc, dcv);
         ++c_loc;
       }
+    }
+  }
+  sig += s_loc;
+  cnt += c_loc;
+}
+
+// A one-event move (location / arrival, NR = NA = 1) whose windows overlap
+// changes only the rows of their symmetric difference: each lane walks its own
+// <= 2 edge intervals (a uniform trip count across the warp) instead of the
+// warp's whole band. Loads are scattered over the ~10 distinct rows the warp's
+// lanes sit on, which costs L1 wavefronts but saves most of the issue slots.
+template <int ND, typename YT>
+__device__ __forceinline__ void edges(const Dev& d, int j, Win A0, Win R0, const Wins<ND>& D,
+                                      const int (&sg)[ND > 0 ? ND : 1], const double2* Ts,
+                                      double& sig, int& cnt) {
+  int lo1, n1, dc1, lo2, n2, dc2;
+  if (A0.hi <= R0.lo || R0.hi <= A0.lo || A0.hi == A0.lo || R0.hi == R0.lo) {
+    lo1 = A0.lo;
+    n1 = A0.hi - A0.lo;
+    dc1 = 1;
+    lo2 = R0.lo;
+    n2 = R0.hi - R0.lo;
+    dc2 = -1;
+  } else {
+    lo1 = min(A0.lo, R0.lo);
+    n1 = max(A0.lo, R0.lo) - lo1;
+    dc1 = A0.lo < R0.lo ? 1 : -1;
+    lo2 = min(A0.hi, R0.hi);
+    n2 = max(A0.hi, R0.hi) - lo2;
+    dc2 = A0.hi > R0.hi ? 1 : -1;
+  }
+  const int total = n1 + n2;
+  const int trips = __reduce_max_sync(0xffffffffu, (unsigned)total);
+  const int stride = d.S_pad;
+  const YT* __restrict__ y = reinterpret_cast<const YT*>(d.y) + j;
+  const uint16_t* __restrict__ c16 = reinterpret_cast<const uint16_t*>(d.cov) + j;
+  double s_loc = 0.0;
+  int c_loc = 0;
+  bool big = false;
+  constexpr int RU = 4;
+  for (int i0 = 0; i0 < trips; i0 += RU) {
+    int r[RU], dc[RU], c[RU];
+    double yv[RU];
+#pragma unroll
+    for (int k = 0; k < RU; ++k) {
+      const int i = i0 + k;
+      r[k] = i < n1 ? lo1 + i : lo2 + (i - n1);
+      dc[k] = i < total ? (i < n1 ? dc1 : dc2) : 0;
+    }
+#pragma unroll
+    for (int k = 0; k < RU; ++k) {
+      const size_t o = (size_t)r[k] * stride;
+      c[k] = dc[k] ? (int)__ldg(c16 + o) : 0;
+      yv[k] = dc[k] ? (double)__ldg(y + o) : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < RU; ++k) {
+      int cc = c[k];
+#pragma unroll
+      for (int q = 0; q < ND; ++q) cc += sg[q] * inw(r[k], D.w[q]);
+      big |= cc >= TBL - 2;
+      const int ci = min(cc, TBL - 3) & (dc[k] ? 0x7fffffff : 0);
+      const double t = term_fast(Ts, yv[k], ci, dc[k] ? dc[k] : 1);
+      s_loc += dc[k] ? t : 0.0;
+      c_loc += dc[k] ? 1 : 0;
+    }
+  }
+  if (__any_sync(0xffffffffu, big)) {
+    s_loc = 0.0;
+    c_loc = 0;
+    for (int i = 0; i < total; ++i) {
+      const int rr = i < n1 ? lo1 + i : lo2 + (i - n1);
+      const size_t o = (size_t)rr * stride;
+      int cc = (int)__ldg(c16 + o);
+#pragma unroll
+      for (int q = 0; q < ND; ++q) cc += sg[q] * inw(rr, D.w[q]);
+      s_loc += term(d, Ts, (double)__ldg(y + o), cc, i < n1 ? dc1 : dc2);
+      ++c_loc;
     }
   }
   sig += s_loc;
@@ -338,7 +421,13 @@ __device__ __forceinline__ void station_item(const Dev& d, const Prop& P, const 
   if (nwmax == 0) {
     Wins<0> D0;
     int sg0[1];
-    band<NR, NA, 0, YT>(d, j, blo, bhi, R, A, D0, sg0, Ts, sig, cnt);
+    if (NR + NA == 1 && kScatterSingle)
+      edges<0, YT>(d, j, NA ? A.w[0] : empty_win(), NR ? R.w[0] : empty_win(), D0, sg0, Ts,
+                   sig, cnt);
+    else if (NR == 1 && NA == 1 && P.nr == 1 && P.na == 1)
+      edges<0, YT>(d, j, A.w[0], R.w[0], D0, sg0, Ts, sig, cnt);
+    else
+      band<NR, NA, 0, YT>(d, j, blo, bhi, R, A, D0, sg0, Ts, sig, cnt);
   } else if (nwmax <= 2) {
     Wins<2> D2;
     int sg2[2];
@@ -347,7 +436,13 @@ __device__ __forceinline__ void station_item(const Dev& d, const Prop& P, const 
       D2.w[q] = D.w[q];
       sg2[q] = sg[q];
     }
-    band<NR, NA, 2, YT>(d, j, blo, bhi, R, A, D2, sg2, Ts, sig, cnt);
+    if (NR + NA == 1 && kScatterSingle)
+      edges<2, YT>(d, j, NA ? A.w[0] : empty_win(), NR ? R.w[0] : empty_win(), D2, sg2, Ts,
+                   sig, cnt);
+    else if (NR == 1 && NA == 1 && P.nr == 1 && P.na == 1)
+      edges<2, YT>(d, j, A.w[0], R.w[0], D2, sg2, Ts, sig, cnt);
+    else
+      band<NR, NA, 2, YT>(d, j, blo, bhi, R, A, D2, sg2, Ts, sig, cnt);
   } else if (nwmax <= 4) {
     band<NR, NA, 4, YT>(d, j, blo, bhi, R, A, D, sg, Ts, sig, cnt);
   } else {
