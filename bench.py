@@ -283,7 +283,7 @@ def main():
         sweep(i)
     torch.cuda.synchronize()
     acc = dict(total_ms=0.0, sweep_ms=0.0, bytes=0.0, steps=0, scored=0, launches=0,
-               changed=0, arrvals=0, phases=0)
+               changed=0, arrvals=0, phases=0, accepted=0, spec=0)
     barrier(dist)
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
@@ -300,6 +300,8 @@ def main():
             acc["launches"] += st["kernel_launches"]
             acc["changed"] += st["changed_samples"]
             acc["arrvals"] += st["arrival_values"]
+            acc["accepted"] += st["total_accepted"]
+            acc["spec"] += st["speculative_discarded"]
     torch.cuda.synchronize()
     barrier(dist)
     t_max = reduce_max(dist, acc["total_ms"])
@@ -321,7 +323,9 @@ def main():
                    "scored_proposals_per_s": reduce_sum(dist, acc["scored"]) / (t_max / 1e3),
                    "events": int(ev.N), "stations": c["S"], "regions": c["n_regions"],
                    "k": c["k"], "l2": "flushed between timed sweeps (256 MiB write)",
-                   "sweep_kernel_ms_per_step": acc["sweep_ms"] / args.steps},
+                   "sweep_kernel_ms_per_step": acc["sweep_ms"] / args.steps,
+                   "acceptance": acc["accepted"] / max(1, acc["steps"]),
+                   "speculative_discarded_frac": acc["spec"] / max(1, acc["steps"])},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": ncu_traffic(args.config),
                      "peak_kind": peak_kind, "kernel": "k_phase (region sweep, fused delta)",

@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -334,7 +335,7 @@ __device__ void gen_proposal(const Dev& d, const Samp& sp, const PhaseArgs& pa, 
 template <typename YT, int MODE>
 __global__ void __launch_bounds__(NT, 1)
     k_phase(const Dev d, const Samp sp, const PhaseArgs pa, Ctl* ctl, int stamp) {
-  __shared__ double2 Ts[TBL * 4];  // {dL, dI} per (count, dc)
+  __shared__ double2 Ts[TBL * 4 + 4];  // {dL, dI} per (count, dc) + a zero row
   __shared__ OwnEv own[MAXOWN];
   __shared__ StartEv st[MAXOWN];
   __shared__ int pold[MAXDIFF], pnew[MAXDIFF];
@@ -345,6 +346,7 @@ __global__ void __launch_bounds__(NT, 1)
   __shared__ int s_w[NW];
   __shared__ int s_nown, s_np, s_abort, s_tmp, s_adv, s_accq;
   __shared__ unsigned long long s_births;
+  __shared__ unsigned long long s_tprof[2][8];
   __shared__ long long s_nlocal;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -355,11 +357,13 @@ __global__ void __launch_bounds__(NT, 1)
   const bool rclosed = region + 1 == pa.nreg;
   const int N = ctl->n_events;
 
-  for (int i = tid; i < TBL * 4; i += NT) Ts[i] = i < d.tab_n * 4 ? d.Dg[i] : make_double2(0, 0);
+  for (int i = tid; i < TBL * 4 + 4; i += NT)
+    Ts[i] = i < TBL * 4 && i < d.tab_n * 4 ? d.Dg[i] : make_double2(0, 0);
   if (tid == 0) {
     s_nown = 0;
     s_abort = 0;
   }
+  if (tid < 16) s_tprof[tid >> 3][tid & 7] = 0ull;
   __syncthreads();
   // own events: table entries (id order) inside the region
   // (events_in_region, proposals.hpp:65-71, on the local copy of samplers.hpp:448)
@@ -419,10 +423,17 @@ __global__ void __launch_bounds__(NT, 1)
   }
   const int T_per = (d.S_pad + 31) / 32;  // tiles of 32 stations
   int round = 0;
+  long long tprof[5] = {0, 0, 0, 0, 0};
+  long long tc = clock64();
   for (int i0 = 0; i0 < (int)sp.k; ++round) {
     const int m = min(MSPEC, (int)sp.k - i0);
     const int buf = round & 1;
     __syncthreads();  // S0: previous round's write-back and state are visible
+    if (tid == 0) {
+      const long long now = clock64();
+      tprof[3] += now - tc;
+      tc = now;
+    }
     if (tid < m) {
       const int step = i0 + tid;
       gen_proposal<MODE>(d, sp, pa, prop[buf][tid], own, s_nown, region, rlo, rhi, rclosed,
@@ -435,6 +446,11 @@ __global__ void __launch_bounds__(NT, 1)
       red_cnt[warp][lane] = 0;
     }
     __syncthreads();  // S1: proposals ready
+    if (tid == 0) {
+      const long long now = clock64();
+      tprof[0] += now - tc;
+      tc = now;
+    }
     {
       // work items: (proposal q, tile of 32 station pairs), spread over warps
       const int np_now = s_np;
@@ -442,8 +458,16 @@ __global__ void __launch_bounds__(NT, 1)
       double sig = 0.0, arr = 0.0;
       int cnt = 0;
       const int n_items = m * T_per;
-      for (int t = warp; t < n_items; t += NW) {
-        const int q = t / T_per, tile = t - q * T_per;
+      int q = 0, tile = warp;  // t = q * T_per + tile, advanced without division
+      while (tile >= T_per) {
+        tile -= T_per;
+        ++q;
+      }
+      for (int t = warp; t < n_items; t += NW, tile += NW) {
+        while (tile >= T_per) {
+          tile -= T_per;
+          ++q;
+        }
         if (q != cur_q) {
           if (cur_q >= 0) {
             sig = warp_sum(sig);
@@ -471,7 +495,13 @@ __global__ void __launch_bounds__(NT, 1)
         in.step = (uint32_t)(i0 + q);
         in.wlo = 0;
         in.whi = d.n;
+        const long long t0i = clock64();
         score_item<MODE, YT>(d, P, in, tile, np_now, pold, pnew, Ts, sig, arr, cnt);
+        if (kProfItems && lane == 0 && !P.skip) {
+          const int ty = P.type < 0 ? 5 : P.type;
+          atomicAdd(&s_tprof[0][ty], (unsigned long long)(clock64() - t0i));
+          atomicAdd(&s_tprof[1][ty], 1ull);
+        }
       }
       if (cur_q >= 0) {
         sig = warp_sum(sig);
@@ -485,6 +515,11 @@ __global__ void __launch_bounds__(NT, 1)
       }
     }
     __syncthreads();  // S2: partial sums ready
+    if (tid == 0) {
+      const long long now = clock64();
+      tprof[1] += now - tc;
+      tc = now;
+    }
     if (tid == 0) {
       int adv = m, accq = -1;
       for (int q = 0; q < m; ++q) {
@@ -650,6 +685,12 @@ __global__ void __launch_bounds__(NT, 1)
       s_nlocal = n_local;
     }
     __syncthreads();  // S3: decision
+    if (tid == 0) {
+      const long long now = clock64();
+      tprof[2] += now - tc;
+      tc = now;
+      tprof[4] += 1;
+    }
     if (s_abort) return;
     const int accq = s_accq;
     if (accq >= 0) {
@@ -760,6 +801,8 @@ __global__ void __launch_bounds__(NT, 1)
     atomicAdd(&ctl->arrvals, n_arr);
     atomicAdd(&ctl->accepted, n_acc);
     atomicAdd(&ctl->speculative, n_spec);
+    for (int q = 0; q < 5; ++q) atomicAdd(&ctl->prof[q], (unsigned long long)tprof[q]);
+    for (int q = 0; q < 16; ++q) atomicAdd(&ctl->tprof[q >> 3][q & 7], s_tprof[q >> 3][q & 7]);
   }
 }
 
@@ -914,13 +957,14 @@ template <typename YT>
 __global__ void __launch_bounds__(NT, 1)
     k_score_batch(const Dev d, Table tab, const Ctl* ctl, const ChangeDev* ch,
                   const double* rows, double* out) {
-  __shared__ double2 Ts[TBL * 4];
+  __shared__ double2 Ts[TBL * 4 + 4];
   __shared__ Prop P;
   __shared__ double rsig[NW], rarr[NW];
   __shared__ int s_bad;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const ChangeDev c = ch[blockIdx.x];
-  for (int i = tid; i < TBL * 4; i += NT) Ts[i] = i < d.tab_n * 4 ? d.Dg[i] : make_double2(0, 0);
+  for (int i = tid; i < TBL * 4 + 4; i += NT)
+    Ts[i] = i < TBL * 4 && i < d.tab_n * 4 ? d.Dg[i] : make_double2(0, 0);
   if (tid == 0) {
     s_bad = 0;
     P.type = -1;
@@ -1079,6 +1123,8 @@ __global__ void k_record(const Ctl* ctl, long long* count_out) { *count_out = ct
 __global__ void k_reset_counters(Ctl* ctl) {
   ctl->scored = ctl->changed = ctl->arrvals = ctl->accepted = ctl->id_mismatch = 0ull;
   ctl->speculative = 0ull;
+  for (int q = 0; q < 8; ++q) ctl->prof[q] = 0ull;
+  for (int q = 0; q < 16; ++q) ctl->tprof[q >> 3][q & 7] = 0ull;
   ctl->err = 0;
 }
 
@@ -1876,6 +1922,13 @@ extern "C" int seis_run_chromatic(seis_engine* e, const seis_sampler_cfg* sc, in
       ck(cudaMemcpy(step_out, d_out, (size_t)n_tape * sizeof(seis_step_out),
                     cudaMemcpyDeviceToHost),
          "D2H out");
+    if (getenv("SEIS_PROF"))
+      fprintf(stderr, "[seis prof] cycles: gen %llu items %llu decide %llu writeback %llu rounds %llu\n",
+              c.prof[0], c.prof[1], c.prof[2], c.prof[3], c.prof[4]);
+    if (getenv("SEIS_PROF"))
+      for (int q = 0; q < 6; ++q)
+        fprintf(stderr, "[seis prof] type %d: items %llu warp-cycles/item %.0f\n", q,
+                c.tprof[1][q], c.tprof[1][q] ? (double)c.tprof[0][q] / c.tprof[1][q] : 0.0);
     if (stats) {
       std::memset(stats, 0, sizeof *stats);
       stats->total_steps = executed;

@@ -22,6 +22,10 @@ namespace seis {
 
 constexpr int NT = 512;          // threads per region CTA
 constexpr int MSPEC = 4;         // speculative proposals evaluated per round
+#ifndef SEIS_PROF_ITEMS
+#define SEIS_PROF_ITEMS 0
+#endif
+constexpr bool kProfItems = SEIS_PROF_ITEMS;
 constexpr int NW = NT / 32;
 constexpr int MAXOWN = 128;      // events a region may hold during a phase
 constexpr int MAXDIFF = 2 * MAXOWN;  // diff pairs a region may hold
@@ -89,6 +93,8 @@ struct Ctl {
   int err;
   int phase_stamp;
   unsigned long long scored, changed, arrvals, accepted, id_mismatch, speculative;
+  unsigned long long prof[8];  // clock64 cycles per round section (thread 0 of every CTA)
+  unsigned long long tprof[2][8];  // per move type: warp-cycles in items, items
 };
 
 struct PhaseArgs {
@@ -122,15 +128,12 @@ enum : int {
 };
 
 __device__ __forceinline__ Win make_win(const Dev& d, double a) {
-  // arrival_sample_range, density.hpp:29-36 (fp64, no contraction: --fmad=false)
-  const double n = (double)d.n;
-  double lo = ceil(a * d.rate);
-  double hi = ceil((a + d.t_s) * d.rate);
-  lo = fmin(fmax(lo, 0.0), n);
-  hi = fmin(fmax(hi, 0.0), n);
+  // arrival_sample_range, density.hpp:29-36: ceil in fp64 (no contraction:
+  // --fmad=false), clamp to [0, n]. cvt.rpi.s32.f64 rounds up and saturates
+  // out-of-range values, so clamping the int equals clamping the double.
   Win w;
-  w.lo = (int)lo;
-  w.hi = (int)hi;
+  w.lo = min(max(__double2int_ru(a * d.rate), 0), d.n);
+  w.hi = min(max(__double2int_ru((a + d.t_s) * d.rate), 0), d.n);
   return w;
 }
 

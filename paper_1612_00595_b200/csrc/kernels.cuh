@@ -190,6 +190,63 @@ __device__ __forceinline__ void band(const Dev& d, int j, int blo, int bhi, cons
   cnt += c_loc;
 }
 
+// Dense single-window moves (birth: SIGN +1, death: SIGN -1): every row of
+// the lane's window changes, so the warp walks its common band row by row
+// (coalesced: one line per row for the 32 stations) with the lane's window
+// test as a predicate. cnt is the window length (computed by the caller).
+template <int SIGN, int ND, typename YT>
+__device__ __forceinline__ void band1(const Dev& d, int j, int blo, int bhi, Win W,
+                                      const Wins<ND>& D, const int (&sg)[ND > 0 ? ND : 1],
+                                      const double2* Ts, double& sig) {
+  constexpr int RU = sizeof(YT) == 4 ? 8 : 4;
+  constexpr int code = SIGN > 0 ? 2 : 1;  // dc_code(+1) / dc_code(-1)
+  const unsigned len = (unsigned)(W.hi - W.lo);
+  const size_t stride = (size_t)d.S_pad;
+  const YT* __restrict__ yp = reinterpret_cast<const YT*>(d.y) + (size_t)blo * stride + j;
+  const uint16_t* __restrict__ cp =
+      reinterpret_cast<const uint16_t*>(d.cov) + (size_t)blo * stride + j;
+  double s = 0.0;
+  int mx = 0;
+  // every lane loads every band row (the band's sectors are shared by the
+  // warp's 32 stations anyway); rows outside the lane's window index the zero
+  // row of the table
+  for (int r0 = blo; r0 < bhi; r0 += RU) {
+    int c[RU];
+    YT yv[RU];
+#pragma unroll
+    for (int k = 0; k < RU; ++k) {
+      const bool rowok = r0 + k < bhi;
+      c[k] = rowok ? (int)__ldg(cp) : 0;
+      yv[k] = rowok ? __ldg(yp) : YT(0);
+      cp += stride;
+      yp += stride;
+    }
+#pragma unroll
+    for (int k = 0; k < RU; ++k) {
+      int cc = c[k];
+#pragma unroll
+      for (int q = 0; q < ND; ++q) cc += sg[q] * inw(r0 + k, D.w[q]);
+      mx = max(mx, cc);
+      const bool in = (unsigned)(r0 + k - W.lo) < len;
+      const int idx = in ? min(cc, TBL - 3) * 4 + code : TBL * 4;
+      const double2 e = Ts[idx];
+      const double yy = (double)yv[k];
+      s += fma(-(yy * yy), e.y, e.x);
+    }
+  }
+  if (__any_sync(0xffffffffu, mx >= TBL - 3)) {
+    s = 0.0;  // slow exact pass with the global table
+    for (int r = W.lo; r < W.hi; ++r) {
+      const size_t o = (size_t)r * stride + j;
+      int cc = (int)__ldg(reinterpret_cast<const uint16_t*>(d.cov) + o);
+#pragma unroll
+      for (int q = 0; q < ND; ++q) cc += sg[q] * inw(r, D.w[q]);
+      s += term(d, Ts, (double)__ldg(reinterpret_cast<const YT*>(d.y) + o), cc, SIGN);
+    }
+  }
+  sig += s;
+}
+
 // A one-event move (location / arrival, NR = NA = 1) whose windows overlap
 // changes only the rows of their symmetric difference: each lane walks its own
 // <= 2 edge intervals (a uniform trip count across the warp) instead of the
@@ -245,12 +302,12 @@ __device__ __forceinline__ void edges(const Dev& d, int j, Win A0, Win R0, const
 #pragma unroll
       for (int q = 0; q < ND; ++q) cc += sg[q] * inw(r[k], D.w[q]);
       big |= cc >= TBL - 2;
-      const int ci = min(cc, TBL - 3) & (dc[k] ? 0x7fffffff : 0);
-      const double t = term_fast(Ts, yv[k], ci, dc[k] ? dc[k] : 1);
-      s_loc += dc[k] ? t : 0.0;
-      c_loc += dc[k] ? 1 : 0;
+      const int idx = dc[k] ? min(cc, TBL - 3) * 4 + dc_code(dc[k]) : TBL * 4;
+      const double2 e = Ts[idx];
+      s_loc += fma(-(yv[k] * yv[k]), e.y, e.x);
     }
   }
+  c_loc = total;
   if (__any_sync(0xffffffffu, big)) {
     s_loc = 0.0;
     c_loc = 0;
@@ -421,9 +478,11 @@ __device__ __forceinline__ void station_item(const Dev& d, const Prop& P, const 
   if (nwmax == 0) {
     Wins<0> D0;
     int sg0[1];
-    if (NR + NA == 1 && kScatterSingle)
-      edges<0, YT>(d, j, NA ? A.w[0] : empty_win(), NR ? R.w[0] : empty_win(), D0, sg0, Ts,
-                   sig, cnt);
+    if (NR + NA == 1) {
+      const Win W = NA ? A.w[0] : R.w[0];
+      band1<NA ? 1 : -1, 0, YT>(d, j, blo, bhi, W, D0, sg0, Ts, sig);
+      cnt += W.hi - W.lo;
+    }
     else if (NR == 1 && NA == 1 && P.nr == 1 && P.na == 1)
       edges<0, YT>(d, j, A.w[0], R.w[0], D0, sg0, Ts, sig, cnt);
     else
@@ -436,9 +495,11 @@ __device__ __forceinline__ void station_item(const Dev& d, const Prop& P, const 
       D2.w[q] = D.w[q];
       sg2[q] = sg[q];
     }
-    if (NR + NA == 1 && kScatterSingle)
-      edges<2, YT>(d, j, NA ? A.w[0] : empty_win(), NR ? R.w[0] : empty_win(), D2, sg2, Ts,
-                   sig, cnt);
+    if (NR + NA == 1) {
+      const Win W = NA ? A.w[0] : R.w[0];
+      band1<NA ? 1 : -1, 2, YT>(d, j, blo, bhi, W, D2, sg2, Ts, sig);
+      cnt += W.hi - W.lo;
+    }
     else if (NR == 1 && NA == 1 && P.nr == 1 && P.na == 1)
       edges<2, YT>(d, j, A.w[0], R.w[0], D2, sg2, Ts, sig, cnt);
     else
