@@ -177,6 +177,7 @@ __device__ void gen_proposal(const Dev& d, const Samp& sp, const PhaseArgs& pa, 
       }
     P.type = type;
     P.u = seis_u53(d0.w[2], d0.w[3]);
+    P.logu = log(P.u);
     const seis_u32x4 d1 = seis_draw(sp.seed, (uint32_t)pa.epoch, (uint32_t)region,
                                     (uint32_t)step, SEIS_DRAW_SCALAR);
     switch (type) {
@@ -274,6 +275,7 @@ __device__ void gen_proposal(const Dev& d, const Samp& sp, const PhaseArgs& pa, 
     P.type = (int)ts.type;
     null_ = ts.is_null != 0;
     P.u = ts.u;
+    P.logu = log(ts.u);
     P.u_drawn = (int)ts.u_drawn;
     P.tape_acc = (int)ts.accepted;
     P.logq_f = ts.logq_f;
@@ -347,6 +349,11 @@ __global__ void __launch_bounds__(NT, 1)
   __shared__ int s_nown, s_np, s_abort, s_tmp, s_adv, s_accq;
   __shared__ unsigned long long s_births;
   __shared__ unsigned long long s_tprof[2][8];
+  __shared__ double s_delta[MSPEC], s_logr[MSPEC], s_prior[2];
+  __shared__ int s_item;
+  __shared__ double s_logi_k[MAXOWN + 2];   // log(i), i <= MAXOWN + 1 (proposal terms)
+  extern __shared__ double s_logi_n[];       // [LOGIWIN] log(i), i in [N - LOGIWIN/2, N + LOGIWIN/2)
+  __shared__ int s_accg[MSPEC], s_cnt[MSPEC];
   __shared__ long long s_nlocal;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -356,9 +363,16 @@ __global__ void __launch_bounds__(NT, 1)
   const double rlo = pa.bnd[region], rhi = pa.bnd[region + 1];
   const bool rclosed = region + 1 == pa.nreg;
   const int N = ctl->n_events;
+  const double log_len = log(rhi - rlo);  // std::log(region.length()), proposals.hpp:102
 
   for (int i = tid; i < TBL * 4 + 4; i += NT)
     Ts[i] = i < TBL * 4 && i < d.tab_n * 4 ? d.Dg[i] : make_double2(0, 0);
+  const int logi_base = N - LOGIWIN / 2;
+  for (int i = tid; i < MAXOWN + 2; i += NT) s_logi_k[i] = i < d.logi_n ? d.logi[i] : 0.0;
+  for (int i = tid; i < LOGIWIN; i += NT) {
+    const int g = logi_base + i;
+    s_logi_n[i] = (g >= 0 && g < d.logi_n) ? d.logi[g] : 0.0;
+  }
   if (tid == 0) {
     s_nown = 0;
     s_abort = 0;
@@ -423,7 +437,7 @@ __global__ void __launch_bounds__(NT, 1)
   }
   const int T_per = (d.S_pad + 31) / 32;  // tiles of 32 stations
   int round = 0;
-  long long tprof[5] = {0, 0, 0, 0, 0};
+  long long tprof[6] = {0, 0, 0, 0, 0, 0};
   long long tc = clock64();
   for (int i0 = 0; i0 < (int)sp.k; ++round) {
     const int m = min(MSPEC, (int)sp.k - i0);
@@ -434,9 +448,23 @@ __global__ void __launch_bounds__(NT, 1)
       tprof[3] += now - tc;
       tc = now;
     }
-    if (tid < m) {
-      const int step = i0 + tid;
-      gen_proposal<MODE>(d, sp, pa, prop[buf][tid], own, s_nown, region, rlo, rhi, rclosed,
+    if (tid == 0) {
+      s_item = 0;
+      const long long n0 = s_nlocal;
+      const long long wb = n0 + 1 - logi_base, wd = n0 - logi_base;
+      const double lb = (wb >= 0 && wb < LOGIWIN) ? s_logi_n[wb] : d.logi[n0 + 1];
+      const double ld = (wd >= 0 && wd < LOGIWIN) ? s_logi_n[wd] : d.logi[n0];
+      double pb = 0.0, pdth = 0.0;
+      pb += d.log_lambda_T - lb;
+      pb += 1.0 * d.lxa;
+      pdth -= d.log_lambda_T - ld;
+      pdth += -1.0 * d.lxa;
+      s_prior[0] = pb;
+      s_prior[1] = pdth;
+    }
+    if (warp < m && lane == 0) {  // one lane per warp: move types do not diverge
+      const int step = i0 + warp;
+      gen_proposal<MODE>(d, sp, pa, prop[buf][warp], own, s_nown, region, rlo, rhi, rclosed,
                          step, pa.tape_base + (long long)slot_idx * sp.k + step,
                          id_base + s_births, &ctl->err);
     }
@@ -520,6 +548,71 @@ __global__ void __launch_bounds__(NT, 1)
       tprof[1] += now - tc;
       tc = now;
     }
+    if (warp == 0) {
+      // per-proposal delta / log_r / decision against the round's state, in
+      // parallel lanes (delta_log_joint density.hpp:223-240; log_accept_ratio
+      // and mh_step proposals.hpp:255-291). Lanes 8q..8q+7 reduce proposal q's
+      // per-warp partials (fixed order, deterministic).
+      static_assert(MSPEC * 8 <= 32 && NW % 8 == 0, "reduction layout");
+      const int q = lane >> 3, g = lane & 7;
+      double sig = 0.0, A = 0.0;
+      int c = 0;
+      if (q < m)
+        for (int w = g; w < NW; w += 8) {
+          sig += red_sig[w][q];
+          A += red_arr[w][q];
+          c += red_cnt[w][q];
+        }
+#pragma unroll
+      for (int o = 4; o; o >>= 1) {
+        sig += __shfl_down_sync(0xffffffffu, sig, o, 8);
+        A += __shfl_down_sync(0xffffffffu, A, o, 8);
+        c += __shfl_down_sync(0xffffffffu, c, o, 8);
+      }
+      Prop& P = prop[buf][q < m ? q : 0];
+      if (g == 0 && q < m && !P.skip) {
+        const long long n0 = s_nlocal, n1 = n0 - P.nr + P.na;
+        double delta = 0.0;
+        // every move changes the count by -1, 0 or +1; thread 0 prepared the
+        // two prior deltas of this round (density.hpp:223-237)
+        if (n1 == n0 + 1) {
+          delta = s_prior[0];
+        } else if (n1 == n0 - 1) {
+          delta = s_prior[1];
+        } else if (n1 != n0) {
+          if (n1 > n0) {
+            for (long long i = n0 + 1; i <= n1; ++i) delta += d.log_lambda_T - d.logi[i];
+          } else {
+            for (long long i = n1 + 1; i <= n0; ++i) delta -= d.log_lambda_T - d.logi[i];
+          }
+          delta += (double)(n1 - n0) * d.lxa;
+        }
+        delta += A;
+        delta += sig;
+        if (MODE == 0) {  // proposal log densities (proposals.hpp:100-104,120-126)
+          const int k = s_nown;
+          if (P.type == 0) {
+            P.logq_f = sp.logw[0] - log_len - d.log_xmax + A;
+            P.logq_r = sp.logw[1] - s_logi_k[k + 1];
+          } else if (P.type == 1) {
+            P.logq_f = sp.logw[1] - s_logi_k[k];
+            P.logq_r = sp.logw[0] - log_len - d.log_xmax - A;
+          }
+        }
+        const double log_r = delta + P.logq_r - P.logq_f;
+        bool acc_gpu = log_r >= 0.0;
+        if (!acc_gpu) acc_gpu = P.logu < log_r;
+        s_delta[q] = delta;
+        s_logr[q] = log_r;
+        s_accg[q] = acc_gpu ? 1 : 0;
+        s_cnt[q] = c;
+      }
+    }
+    __syncwarp();
+    if (tid == 0) {
+      const long long now = clock64();
+      tprof[5] += now - tc;
+    }
     if (tid == 0) {
       int adv = m, accq = -1;
       for (int q = 0; q < m; ++q) {
@@ -544,41 +637,10 @@ __global__ void __launch_bounds__(NT, 1)
           }
           continue;
         }
-        double sig = 0.0, A = 0.0;
-        int c = 0;
-        for (int w = 0; w < NW; ++w) {
-          sig += red_sig[w][q];
-          A += red_arr[w][q];
-          c += red_cnt[w][q];
-        }
-        n_changed += (unsigned long long)c;
+        n_changed += (unsigned long long)s_cnt[q];
         n_arr += (P.type == 3) ? 2ull : (unsigned long long)d.S * (P.nr + P.na);
-        // delta_log_joint (density.hpp:223-240): prior terms with n0 = local
-        // event count and area T, arrival densities, likelihood
-        const long long n0 = n_local, n1 = n0 - P.nr + P.na;
-        double delta = 0.0;
-        if (n1 > n0) {
-          for (long long i = n0 + 1; i <= n1; ++i) delta += d.log_lambda_T - d.logi[i];
-        } else if (n1 < n0) {
-          for (long long i = n1 + 1; i <= n0; ++i) delta -= d.log_lambda_T - d.logi[i];
-        }
-        delta += (double)(n1 - n0) * d.lxa;
-        delta += A;
-        delta += sig;
-        // proposal log densities (proposals.hpp:100-104,120-126)
-        if (MODE == 0) {
-          if (P.type == 0) {
-            P.logq_f = sp.logw[0] - log(rhi - rlo) - d.log_xmax + A;
-            P.logq_r = sp.logw[1] - d.logi[nown + 1];
-          } else if (P.type == 1) {
-            P.logq_f = sp.logw[1] - d.logi[nown];
-            P.logq_r = sp.logw[0] - log(rhi - rlo) - d.log_xmax - A;
-          }
-        }
-        const double log_r = delta + P.logq_r - P.logq_f;  // log_accept_ratio
-        // mh_step decision (proposals.hpp:283-291)
-        bool acc_gpu = log_r >= 0.0;
-        if (!acc_gpu) acc_gpu = log(P.u) < log_r;
+        const double delta = s_delta[q], log_r = s_logr[q];
+        const bool acc_gpu = s_accg[q] != 0;
         bool apply = acc_gpu;
         if (MODE == 1) {
           seis_step_out o;
@@ -801,7 +863,7 @@ __global__ void __launch_bounds__(NT, 1)
     atomicAdd(&ctl->arrvals, n_arr);
     atomicAdd(&ctl->accepted, n_acc);
     atomicAdd(&ctl->speculative, n_spec);
-    for (int q = 0; q < 5; ++q) atomicAdd(&ctl->prof[q], (unsigned long long)tprof[q]);
+    for (int q = 0; q < 6; ++q) atomicAdd(&ctl->prof[q], (unsigned long long)tprof[q]);
     for (int q = 0; q < 16; ++q) atomicAdd(&ctl->tprof[q >> 3][q & 7], s_tprof[q >> 3][q & 7]);
   }
 }
@@ -1136,7 +1198,7 @@ using namespace seis;
 namespace {
 
 thread_local std::string g_err;
-constexpr int kPhaseSmem = 0;  // all shared memory is static
+constexpr int kPhaseSmem = LOGIWIN * (int)sizeof(double);  // dynamic: the log(i) window
 
 int fail(int code, const std::string& m) {
   g_err = m;
@@ -1430,6 +1492,10 @@ int seis_engine_create(const seis_model_cfg* cfg, const double* stations, int64_
     d.logi = e->logi;
     d.logi_n = tab_n;
     d.pool_cap = e->cap;
+    for (auto f : {(const void*)k_phase<float, 0>, (const void*)k_phase<float, 1>,
+                   (const void*)k_phase<double, 0>, (const void*)k_phase<double, 1>})
+      ck(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, kPhaseSmem),
+         "smem attribute");
     upload_signals(e, signals);
   });
   if (rc) {
@@ -1647,10 +1713,10 @@ int seis_score_batch(seis_engine* e, int64_t n_changes, const seis_change* chang
                          cudaMemcpyHostToDevice, e->stream),
          "H2D");
     if (e->dtype == SEIS_F64)
-      k_score_batch<double><<<(unsigned)n_changes, NT, kPhaseSmem, e->stream>>>(e->d, e->tab[e->cur],
+      k_score_batch<double><<<(unsigned)n_changes, NT, 0, e->stream>>>(e->d, e->tab[e->cur],
                                                                        e->ctl, dc, rows, o);
     else
-      k_score_batch<float><<<(unsigned)n_changes, NT, kPhaseSmem, e->stream>>>(e->d, e->tab[e->cur],
+      k_score_batch<float><<<(unsigned)n_changes, NT, 0, e->stream>>>(e->d, e->tab[e->cur],
                                                                       e->ctl, dc, rows, o);
     ck(cudaGetLastError(), "k_score_batch");
     ck(cudaMemcpyAsync(delta_out, o, n_changes * 8, cudaMemcpyDeviceToHost, e->stream), "D2H");
@@ -1923,8 +1989,8 @@ extern "C" int seis_run_chromatic(seis_engine* e, const seis_sampler_cfg* sc, in
                     cudaMemcpyDeviceToHost),
          "D2H out");
     if (getenv("SEIS_PROF"))
-      fprintf(stderr, "[seis prof] cycles: gen %llu items %llu decide %llu writeback %llu rounds %llu\n",
-              c.prof[0], c.prof[1], c.prof[2], c.prof[3], c.prof[4]);
+      fprintf(stderr, "[seis prof] cycles: gen %llu items %llu decide %llu (parallel part %llu) writeback %llu rounds %llu\n",
+              c.prof[0], c.prof[1], c.prof[2], c.prof[5], c.prof[3], c.prof[4]);
     if (getenv("SEIS_PROF"))
       for (int q = 0; q < 6; ++q)
         fprintf(stderr, "[seis prof] type %d: items %llu warp-cycles/item %.0f\n", q,

@@ -38,7 +38,7 @@ struct Prop {
   int arr_st;
   double arr_da;
   long long tape_idx, tape_off;
-  double logq_f, logq_r, u;
+  double logq_f, logq_r, u, logu;
   int u_drawn, tape_acc;
   int accept;
   int dslot[2], inplace[2];
