@@ -1356,7 +1356,7 @@ Ctl read_ctl(seis_engine* e) {
 
 const char* err_name(int e) {
   switch (e) {
-    case ERR_OWN_OVERFLOW: return "a region exceeded the per-region event limit (128)";
+    case ERR_OWN_OVERFLOW: return "a region exceeded the per-region event limit (64)";
     case ERR_POOL_EXHAUSTED: return "event pool exhausted: raise event_capacity";
     case ERR_TAPE_UNKNOWN_ID: return "replay tape names an event the region does not hold";
     case ERR_TABLE_OVERFLOW: return "event table overflow: raise event_capacity";

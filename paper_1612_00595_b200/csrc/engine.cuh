@@ -21,13 +21,16 @@
 namespace seis {
 
 constexpr int NT = 512;          // threads per region CTA
-constexpr int MSPEC = 4;         // speculative proposals evaluated per round
+#ifndef SEIS_MSPEC
+#define SEIS_MSPEC 4
+#endif
+constexpr int MSPEC = SEIS_MSPEC;  // speculative proposals evaluated per round
 #ifndef SEIS_PROF_ITEMS
 #define SEIS_PROF_ITEMS 0
 #endif
 constexpr bool kProfItems = SEIS_PROF_ITEMS;
 constexpr int NW = NT / 32;
-constexpr int MAXOWN = 128;      // events a region may hold during a phase
+constexpr int MAXOWN = 64;       // events a region may hold during a phase
 constexpr int MAXDIFF = 2 * MAXOWN;  // diff pairs a region may hold
 constexpr int MAXDOUT = 3 * MAXOWN;  // diff pairs + recycled slots per region
 constexpr int TBL = 512;         // coverage counts whose {dL, dI} rows live in smem
