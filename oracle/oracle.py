@@ -286,6 +286,23 @@ class Oracle:
         self._sigw(lo, hi, tau, T, rate, C.byref(a), C.byref(b))
         return a.value, b.value
 
+    # -- evaluation.hpp
+    def match_events(self, truth: Events, inferred: Events, threshold: float = 12.0):
+        """match_events (evaluation.hpp:51-103) -> (precision, recall, location_error, n)."""
+        f = getattr(self.lib, self.pre + "match_events")
+        f.argtypes = [i64, P, P, P, i64, P, P, P, f64, P]
+        f.restype = C.c_int
+        out = np.zeros(4)
+        a = [np.ascontiguousarray(v, dt) for v, dt in ((truth.ids, np.uint64), (truth.x, np.float64),
+                                                        (truth.t, np.float64))]
+        b = [np.ascontiguousarray(v, dt) for v, dt in ((inferred.ids, np.uint64),
+                                                        (inferred.x, np.float64),
+                                                        (inferred.t, np.float64))]
+        rc = f(truth.N, *[_p(v) for v in a], inferred.N, *[_p(v) for v in b], threshold, _p(out))
+        if rc:
+            raise ValueError(self.err())
+        return out[0], out[1], out[2], int(out[3])
+
     # -- samplers.hpp
     def run_chromatic(self, world: World, sampler: Sampler, init: Events | None = None,
                       tape: bool = True, rowlj: bool = False) -> dict:

@@ -25,6 +25,7 @@
 #include <vector>
 
 #include "seismic/density.hpp"
+#include "seismic/evaluation.hpp"
 #include "seismic/model.hpp"
 #include "seismic/partition.hpp"
 #include "seismic/proposals.hpp"
@@ -525,6 +526,21 @@ int sr_bench_region_steps(const so_model* mm, const double* signals, int64_t N,
     for (auto& p : pool) p.join();
     *wall_seconds = elapsed();
     *proposals = total.load();
+  });
+}
+
+int sr_match_events(int64_t nt, const uint64_t* tid, const double* tx, const double* tt,
+                    int64_t ni, const uint64_t* iid, const double* ix, const double* it,
+                    double threshold, double* out) {
+  return guarded([&] {
+    std::vector<EventPoint> a, b;
+    for (int64_t i = 0; i < nt; ++i) a.push_back({tid[i], tx[i], tt[i]});
+    for (int64_t i = 0; i < ni; ++i) b.push_back({iid[i], ix[i], it[i]});
+    const MatchReport r = match_events(a, b, threshold);
+    out[0] = r.precision;
+    out[1] = r.recall;
+    out[2] = r.location_error;
+    out[3] = static_cast<double>(r.n_matched);
   });
 }
 

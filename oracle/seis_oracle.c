@@ -1193,3 +1193,64 @@ float so_philox_normal(uint64_t seed, uint32_t sweep, uint32_t region, uint32_t 
 }
 
 float so_bm(uint32_t w0, uint32_t w1) { return seis_bm(w0, w1); }
+
+/* ------------------------------------------------------------ evaluation.hpp */
+
+typedef struct {
+  uint64_t id;
+  double x, t;
+} pt_t;
+
+static int cmp_tx(const void* a, const void* b) {
+  const pt_t* p = (const pt_t*)a;
+  const pt_t* q = (const pt_t*)b;
+  if (p->t != q->t) return p->t < q->t ? -1 : 1;
+  if (p->x != q->x) return p->x < q->x ? -1 : 1;
+  return p->id < q->id ? -1 : (p->id > q->id ? 1 : 0);
+}
+
+/* match_events, evaluation.hpp:51-103: greedy matching in ascending (t, x)
+ * order; a pair counts when within threshold in time and in distance
+ * separately. out = {precision, recall, location_error, n_matched}. */
+int so_match_events(int64_t nt, const uint64_t* tid, const double* tx, const double* tt,
+                    int64_t ni, const uint64_t* iid, const double* ix, const double* it,
+                    double threshold, double* out) {
+  if (!(threshold > 0)) return fail(SO_EINVAL, "match_events: threshold must be > 0");
+  pt_t* T = (pt_t*)malloc(sizeof(pt_t) * (size_t)(nt + 1));
+  pt_t* I = (pt_t*)malloc(sizeof(pt_t) * (size_t)(ni + 1));
+  char* taken = (char*)calloc((size_t)ni + 1, 1);
+  for (int64_t i = 0; i < nt; ++i) T[i] = (pt_t){tid[i], tx[i], tt[i]};
+  for (int64_t i = 0; i < ni; ++i) I[i] = (pt_t){iid[i], ix[i], it[i]};
+  qsort(T, (size_t)nt, sizeof(pt_t), cmp_tx);
+  qsort(I, (size_t)ni, sizeof(pt_t), cmp_tx);
+  int64_t matched = 0;
+  double sum = 0.0;
+  for (int64_t a = 0; a < nt; ++a) {
+    int64_t best = ni;
+    double best_dist = 0.0;
+    for (int64_t i = 0; i < ni; ++i) {
+      if (taken[i]) continue;
+      const double dx = T[a].x - I[i].x;
+      const double dt = T[a].t - I[i].t;
+      const double dist = sqrt(dx * dx + dt * dt);
+      if (best == ni || dist < best_dist) {
+        best = i;
+        best_dist = dist;
+      }
+    }
+    if (best == ni) continue;
+    if (fabs(T[a].t - I[best].t) < threshold && fabs(T[a].x - I[best].x) < threshold) {
+      taken[best] = 1;
+      ++matched;
+      sum += best_dist;
+    }
+  }
+  out[0] = ni == 0 ? 1.0 : (double)matched / (double)ni;
+  out[1] = nt == 0 ? 1.0 : (double)matched / (double)nt;
+  out[2] = matched ? sum / (double)matched : 0.0;
+  out[3] = (double)matched;
+  free(T);
+  free(I);
+  free(taken);
+  return SO_OK;
+}

@@ -116,6 +116,11 @@ void so_run_rows(const so_run* r, int64_t* step, double* log_joint, int64_t* eve
 void so_run_final(const so_run* r, uint64_t* ids, double* x, double* t, double* arr);
 void so_run_free(so_run* r);
 
+/* ---- evaluation.hpp: match_events; out = {precision, recall, location_error, n_matched} */
+int so_match_events(int64_t nt, const uint64_t* tid, const double* tx, const double* tt,
+                    int64_t ni, const uint64_t* iid, const double* ix, const double* it,
+                    double threshold, double* out);
+
 /* ---- philox stream spec v1 (include/seis_philox.h) probes ---- */
 void so_philox(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0, uint32_t k1,
                uint32_t* out);

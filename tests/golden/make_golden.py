@@ -138,6 +138,23 @@ def main():
                             total_accepted=r["total_accepted"],
                             sampler=np.array([sc.steps_per_epoch, sc.epochs, sc.n_regions,
                                               sc.seed, sc.dynamic]))
+    # --- posterior statistics of the reference's own run_sampler
+    # (chromatic-dynamic from empty; acceptance.cpp:154-194 style), final
+    # hypothesis matched to the truth with match_events (evaluation.hpp:51-103)
+    post = []
+    for ws in range(8):
+        w = R.sample_world(m, 300 + ws)
+        for rs in (1, 2, 3):
+            sc = O.Sampler(steps_per_epoch=500, epochs=40, n_regions=4, seed=rs, dynamic=1,
+                           burn_in_fraction=0.0, record_every=1 << 30)
+            r = O.ref_run_sampler(w, sc, workers=1)
+            pr, rc, le, nm = R.match_events(w.events, r["final"])
+            post.append((300 + ws, rs, pr, rc, le, r["final"].N, w.events.N,
+                         r["total_accepted"]))
+    np.savez_compressed(os.path.join(HERE, "posterior.npz"), rows=np.array(post, np.float64),
+                        cols=np.array(["world_seed", "run_seed", "precision", "recall",
+                                       "location_error", "n_final", "n_true", "accepted"]),
+                        sampler=np.array([500, 40, 4, 1]))
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))

@@ -258,3 +258,36 @@ def test_sampler_validation_errors(E):
         eng.run_chromatic(E.SamplerConfig(n_regions=12))
     with pytest.raises(ValueError):
         E.Engine(engine_model(O.Model(var_event=0.5)), g.signals)
+
+
+# ------------------------------------------------------------------ posterior
+def test_posterior_statistics_within_seed_spread(E, oc):
+    """north_star: posterior precision, recall and mean location error agree
+    with the reference within seed-to-seed spread. Reference numbers: the
+    reference's own run_sampler (tests/golden/posterior.npz, 8 worlds x 3
+    seeds); engine: production mode (philox stream) on the same worlds, 6
+    seeds each."""
+    g = golden("posterior.npz")
+    rows = g["rows"]
+    k, ep, nr, dyn = [int(v) for v in g["sampler"]]
+    m = default_model()
+    stats = []
+    for ws in sorted(set(int(v) for v in rows[:, 0])):
+        w = oc.sample_world(m, ws)
+        eng = E.Engine(engine_model(m), w.signals)
+        for rs in range(11, 17):
+            sc = E.SamplerConfig(algorithm="chromatic-dynamic" if dyn else "chromatic-static",
+                                 steps_per_epoch=k, epochs=ep, n_regions=nr, seed=rs,
+                                 burn_in_fraction=0.0, record_every=1 << 30)
+            eng.set_hypothesis(E.Events(np.zeros(0, np.uint64), np.zeros(0), np.zeros(0),
+                                        np.zeros((0, m.S))))
+            tr = eng.run_chromatic(sc)
+            f = tr.final
+            p, rc, le, _ = oc.match_events(w.events, O.Events(f.ids, f.x, f.t, f.arrivals))
+            stats.append((p, rc, le))
+    gpu = np.array(stats)
+    ref = rows[:, 2:5]
+    for c, name in enumerate(["precision", "recall", "location_error"]):
+        a, b = gpu[:, c], ref[:, c]
+        se = np.sqrt(a.var(ddof=1) / len(a) + b.var(ddof=1) / len(b))
+        assert abs(a.mean() - b.mean()) <= 2.5 * se + 0.02, (name, a.mean(), b.mean(), se)

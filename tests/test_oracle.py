@@ -170,3 +170,34 @@ def test_philox_normals_are_standard(built):
                   for i in range(25)])
     assert abs(z.mean()) < 0.05 and abs(z.std() - 1) < 0.05
     assert abs(np.mean(z ** 4) - 3) < 0.3
+
+
+def test_match_events_reference_kats(oc):
+    # evaluation.hpp:51-103 conventions: vacuous precision/recall, threshold
+    T = O.Events(np.array([1, 2], np.uint64), np.array([10.0, 50.0]), np.array([20.0, 100.0]),
+                 np.zeros((2, 4)))
+    E = O.Events.empty(4)
+    assert oc.match_events(T, E) == (1.0, 0.0, 0.0, 0)
+    assert oc.match_events(E, T) == (0.0, 1.0, 0.0, 0)
+    I = O.Events(np.array([7], np.uint64), np.array([13.0]), np.array([24.0]), np.zeros((1, 4)))
+    p, r, le, n = oc.match_events(T, I)
+    assert (p, r, n) == (1.0, 0.5, 1) and abs(le - 5.0) < 1e-12
+    far = O.Events(np.array([7], np.uint64), np.array([10.0]), np.array([32.5]), np.zeros((1, 4)))
+    assert oc.match_events(T, far)[3] == 0  # |dt| = 12.5 >= threshold 12
+
+
+def test_posterior_statistics_match_reference(oc):
+    # the restatement's reference-mode driver reproduces the reference's own
+    # run_sampler trajectories, hence its posterior statistics, exactly
+    g = golden("posterior.npz")
+    k, ep, nr, dyn = [int(v) for v in g["sampler"]]
+    m = default_model()
+    for row in g["rows"][::5]:
+        ws, rs = int(row[0]), int(row[1])
+        w = oc.sample_world(m, ws)
+        s = O.Sampler(steps_per_epoch=k, epochs=ep, n_regions=nr, seed=rs, dynamic=dyn,
+                      burn_in_fraction=0.0, record_every=1 << 30)
+        r = oc.run_chromatic(w, s, tape=False)
+        p, rc, le, _ = oc.match_events(w.events, r["final"])
+        assert (p, rc, le) == (row[2], row[3], row[4])
+        assert r["final"].N == row[5] and r["total_accepted"] == row[7]
