@@ -1411,9 +1411,12 @@ int seis_engine_create(const seis_model_cfg* cfg, const double* stations, int64_
     e->stations = dalloc<double>(e->S_pad);
     ck(cudaMemcpy(e->stations, st.data(), st.size() * 8, cudaMemcpyHostToDevice), "H2D");
     const size_t esz = dtype == SEIS_F64 ? 8 : 4;
-    ck(cudaMalloc(&e->y, (size_t)e->n * e->S_pad * esz), "cudaMalloc y");
-    e->cov = dalloc<uint32_t>((size_t)e->n * e->P2);
-    ck(cudaMemset(e->cov, 0, (size_t)e->n * e->P2 * 4), "memset");
+    // kRowPad zero rows after the last sample: band loops load whole row
+    // chunks without a bounds predicate
+    ck(cudaMalloc(&e->y, (size_t)(e->n + kRowPad) * e->S_pad * esz), "cudaMalloc y");
+    ck(cudaMemset(e->y, 0, (size_t)(e->n + kRowPad) * e->S_pad * esz), "memset");
+    e->cov = dalloc<uint32_t>((size_t)(e->n + kRowPad) * e->P2);
+    ck(cudaMemset(e->cov, 0, (size_t)(e->n + kRowPad) * e->P2 * 4), "memset");
     e->pool = dalloc<double>((size_t)e->cap * e->S_pad);
     // per-count terms with glibc log, exactly as density.hpp:288-297
     const int tab_n = e->cap + 8;

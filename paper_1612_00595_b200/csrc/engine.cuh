@@ -34,6 +34,7 @@ constexpr int MAXOWN = 64;       // events a region may hold during a phase
 constexpr int MAXDIFF = 2 * MAXOWN;  // diff pairs a region may hold
 constexpr int MAXDOUT = 3 * MAXOWN;  // diff pairs + recycled slots per region
 constexpr int TBL = 512;         // coverage counts whose {dL, dI} rows live in smem
+constexpr int kRowPad = 16;      // zero rows appended to y and cov (unpredicated chunk loads)
 constexpr int LOGIWIN = 1024;    // log(i) window around the phase-start event count
 constexpr int BANDMAX = 256;     // rows of the generic diff-correction scratch
 constexpr double kLog2Pi = 1.8378770664093454835606594728112;

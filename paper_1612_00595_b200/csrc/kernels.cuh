@@ -194,6 +194,7 @@ __device__ __forceinline__ void band(const Dev& d, int j, int blo, int bhi, cons
 // the lane's window changes, so the warp walks its common band row by row
 // (coalesced: one line per row for the 32 stations) with the lane's window
 // test as a predicate. cnt is the window length (computed by the caller).
+static_assert(kRowPad >= 8, "band1 loads RU <= 8 rows past the band");
 template <int SIGN, int ND, typename YT>
 __device__ __forceinline__ void band1(const Dev& d, int j, int blo, int bhi, Win W,
                                       const Wins<ND>& D, const int (&sg)[ND > 0 ? ND : 1],
@@ -214,10 +215,9 @@ __device__ __forceinline__ void band1(const Dev& d, int j, int blo, int bhi, Win
     int c[RU];
     YT yv[RU];
 #pragma unroll
-    for (int k = 0; k < RU; ++k) {
-      const bool rowok = r0 + k < bhi;
-      c[k] = rowok ? (int)__ldg(cp) : 0;
-      yv[k] = rowok ? __ldg(yp) : YT(0);
+    for (int k = 0; k < RU; ++k) {  // rows up to bhi + RU - 1 <= n + kRowPad exist
+      c[k] = (int)__ldg(cp);
+      yv[k] = __ldg(yp);
       cp += stride;
       yp += stride;
     }
