@@ -283,18 +283,19 @@ __device__ __forceinline__ void edges(const Dev& d, int j, Win A0, Win R0, const
   constexpr int RU = 4;
   for (int i0 = 0; i0 < trips; i0 += RU) {
     int r[RU], dc[RU], c[RU];
-    double yv[RU];
+    YT yv[RU];
 #pragma unroll
     for (int k = 0; k < RU; ++k) {
       const int i = i0 + k;
-      r[k] = i < n1 ? lo1 + i : lo2 + (i - n1);
+      // dead slots read the zero pad row n and index the zero table row
+      r[k] = min(i < n1 ? lo1 + i : lo2 + (i - n1), d.n);
       dc[k] = i < total ? (i < n1 ? dc1 : dc2) : 0;
     }
 #pragma unroll
     for (int k = 0; k < RU; ++k) {
       const size_t o = (size_t)r[k] * stride;
-      c[k] = dc[k] ? (int)__ldg(c16 + o) : 0;
-      yv[k] = dc[k] ? (double)__ldg(y + o) : 0.0;
+      c[k] = (int)__ldg(c16 + o);
+      yv[k] = __ldg(y + o);
     }
 #pragma unroll
     for (int k = 0; k < RU; ++k) {
@@ -304,7 +305,8 @@ __device__ __forceinline__ void edges(const Dev& d, int j, Win A0, Win R0, const
       big |= cc >= TBL - 2;
       const int idx = dc[k] ? min(cc, TBL - 3) * 4 + dc_code(dc[k]) : TBL * 4;
       const double2 e = Ts[idx];
-      s_loc += fma(-(yv[k] * yv[k]), e.y, e.x);
+      const double yy = (double)yv[k];
+      s_loc += fma(-(yy * yy), e.y, e.x);
     }
   }
   c_loc = total;
