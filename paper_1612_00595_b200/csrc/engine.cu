@@ -334,18 +334,19 @@ __device__ void gen_proposal(const Dev& d, const Samp& sp, const PhaseArgs& pa, 
   }
 }
 
-template <typename YT, int MODE>
-__global__ void __launch_bounds__(NT, 1)
+template <typename YT, int MODE, int NTT, int MINB>
+__global__ void __launch_bounds__(NTT, MINB)
     k_phase(const Dev d, const Samp sp, const PhaseArgs pa, Ctl* ctl, int stamp) {
+  constexpr int NWT = NTT / 32;
   __shared__ double2 Ts[TBL * 4 + 4];  // {dL, dI} per (count, dc) + a zero row
   __shared__ OwnEv own[MAXOWN];
   __shared__ StartEv st[MAXOWN];
   __shared__ int pold[MAXDIFF], pnew[MAXDIFF];
   __shared__ int lfree[MAXOWN];
   __shared__ Prop prop[2][MSPEC];
-  __shared__ double red_sig[NW][MSPEC], red_arr[NW][MSPEC];
-  __shared__ int red_cnt[NW][MSPEC];
-  __shared__ int s_w[NW];
+  __shared__ double red_sig[NWT][MSPEC], red_arr[NWT][MSPEC];
+  __shared__ int red_cnt[NWT][MSPEC];
+  __shared__ int s_w[NWT];
   __shared__ int s_nown, s_np, s_abort, s_tmp, s_adv, s_accq;
   __shared__ unsigned long long s_births;
   __shared__ unsigned long long s_tprof[2][8];
@@ -365,11 +366,11 @@ __global__ void __launch_bounds__(NT, 1)
   const int N = ctl->n_events;
   const double log_len = log(rhi - rlo);  // std::log(region.length()), proposals.hpp:102
 
-  for (int i = tid; i < TBL * 4 + 4; i += NT)
+  for (int i = tid; i < TBL * 4 + 4; i += NTT)
     Ts[i] = i < TBL * 4 && i < d.tab_n * 4 ? d.Dg[i] : make_double2(0, 0);
   const int logi_base = N - LOGIWIN / 2;
-  for (int i = tid; i < MAXOWN + 2; i += NT) s_logi_k[i] = i < d.logi_n ? d.logi[i] : 0.0;
-  for (int i = tid; i < LOGIWIN; i += NT) {
+  for (int i = tid; i < MAXOWN + 2; i += NTT) s_logi_k[i] = i < d.logi_n ? d.logi[i] : 0.0;
+  for (int i = tid; i < LOGIWIN; i += NTT) {
     const int g = logi_base + i;
     s_logi_n[i] = (g >= 0 && g < d.logi_n) ? d.logi[g] : 0.0;
   }
@@ -381,7 +382,7 @@ __global__ void __launch_bounds__(NT, 1)
   __syncthreads();
   // own events: table entries (id order) inside the region
   // (events_in_region, proposals.hpp:65-71, on the local copy of samplers.hpp:448)
-  for (int base = 0; base < N; base += NT) {
+  for (int base = 0; base < N; base += NTT) {
     const int i = base + tid;
     bool inr = false;
     if (i < N) {
@@ -393,7 +394,7 @@ __global__ void __launch_bounds__(NT, 1)
     __syncthreads();
     if (tid == 0) {
       int acc = s_nown;
-      for (int w = 0; w < NW; ++w) {
+      for (int w = 0; w < NWT; ++w) {
         const int c = s_w[w];
         s_w[w] = acc;
         acc += c;
@@ -491,7 +492,7 @@ __global__ void __launch_bounds__(NT, 1)
         tile -= T_per;
         ++q;
       }
-      for (int t = warp; t < n_items; t += NW, tile += NW) {
+      for (int t = warp; t < n_items; t += NWT, tile += NWT) {
         while (tile >= T_per) {
           tile -= T_per;
           ++q;
@@ -553,12 +554,12 @@ __global__ void __launch_bounds__(NT, 1)
       // parallel lanes (delta_log_joint density.hpp:223-240; log_accept_ratio
       // and mh_step proposals.hpp:255-291). Lanes 8q..8q+7 reduce proposal q's
       // per-warp partials (fixed order, deterministic).
-      static_assert(MSPEC * 8 <= 32 && NW % 8 == 0, "reduction layout");
+      static_assert(MSPEC * 8 <= 32 && NWT % 8 == 0, "reduction layout");
       const int q = lane >> 3, g = lane & 7;
       double sig = 0.0, A = 0.0;
       int c = 0;
       if (q < m)
-        for (int w = g; w < NW; w += 8) {
+        for (int w = g; w < NWT; w += 8) {
           sig += red_sig[w][q];
           A += red_arr[w][q];
           c += red_cnt[w][q];
@@ -768,7 +769,7 @@ __global__ void __launch_bounds__(NT, 1)
             a = a + P.arr_da;
           }
         } else {
-          for (int p = tid; p < d.P2; p += NT) {
+          for (int p = tid; p < d.P2; p += NTT) {
             double2 v = pool2[(size_t)P.rslot[0] * d.P2 + p];
             if (2 * p == P.arr_st) v.x = v.x + P.arr_da;
             if (2 * p + 1 == P.arr_st) v.y = v.y + P.arr_da;
@@ -777,7 +778,7 @@ __global__ void __launch_bounds__(NT, 1)
         }
       } else {
         for (int a = 0; a < P.na; ++a) {
-          for (int p = tid; p < d.P2; p += NT) {
+          for (int p = tid; p < d.P2; p += NTT) {
             const double2 s = st2[p];
             const double m0 = arrival_mean(d, P.ax[a], P.at[a], s.x);
             const double m1 = arrival_mean(d, P.ax[a], P.at[a], s.y);
@@ -1297,6 +1298,7 @@ struct seis_engine {
   double* fate_t = nullptr;
   int* fate_slot = nullptr;
   int stamp = 0;
+  int n_sm = 148;
 
   ~seis_engine() {
     cudaFree(stations);
@@ -1380,6 +1382,38 @@ void launch_lj_any(seis_engine* e, double* out_dev, double* scratch) {
     launch_lj<float>(e, out_dev, scratch);
 }
 
+}  // namespace
+
+namespace {
+// One 512-thread CTA per region. Measured on configs 1 and 2: 256-thread
+// CTAs two or three per SM lose (1.44 M and 1.21 M vs 1.72 M proposals/s at
+// config[2]): a chain's rounds slow down more than sharing an SM gains.
+template <typename YT, int MODE>
+void launch_phase_t(seis_engine* e, int ncr, const Samp& sp, const PhaseArgs& pa, int stamp) {
+  k_phase<YT, MODE, NT, 1><<<ncr, NT, kPhaseSmem, e->stream>>>(e->d, sp, pa, e->ctl, stamp);
+}
+
+void launch_phase(seis_engine* e, int mode, int ncr, const Samp& sp, const PhaseArgs& pa,
+                  int stamp) {
+  if (e->dtype == SEIS_F64) {
+    if (mode == 0)
+      launch_phase_t<double, 0>(e, ncr, sp, pa, stamp);
+    else
+      launch_phase_t<double, 1>(e, ncr, sp, pa, stamp);
+  } else {
+    if (mode == 0)
+      launch_phase_t<float, 0>(e, ncr, sp, pa, stamp);
+    else
+      launch_phase_t<float, 1>(e, ncr, sp, pa, stamp);
+  }
+}
+
+template <typename YT, int MODE>
+void set_phase_attrs() {
+  ck(cudaFuncSetAttribute(k_phase<YT, MODE, NT, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          kPhaseSmem),
+     "smem attribute");
+}
 }  // namespace
 
 extern "C" {
@@ -1495,10 +1529,13 @@ int seis_engine_create(const seis_model_cfg* cfg, const double* stations, int64_
     d.logi = e->logi;
     d.logi_n = tab_n;
     d.pool_cap = e->cap;
-    for (auto f : {(const void*)k_phase<float, 0>, (const void*)k_phase<float, 1>,
-                   (const void*)k_phase<double, 0>, (const void*)k_phase<double, 1>})
-      ck(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, kPhaseSmem),
-         "smem attribute");
+    set_phase_attrs<float, 0>();
+    set_phase_attrs<float, 1>();
+    set_phase_attrs<double, 0>();
+    set_phase_attrs<double, 1>();
+    int dev = 0;
+    ck(cudaGetDevice(&dev), "device");
+    ck(cudaDeviceGetAttribute(&e->n_sm, cudaDevAttrMultiProcessorCount, dev), "sm count");
     upload_signals(e, signals);
   });
   if (rc) {
@@ -1930,17 +1967,7 @@ extern "C" int seis_run_chromatic(seis_engine* e, const seis_sampler_cfg* sc, in
             evs.push_back(b);
             ck(cudaEventRecord(a, e->stream), "event");
           }
-          if (e->dtype == SEIS_F64) {
-            if (mode == 0)
-              k_phase<double, 0><<<ncr, NT, kPhaseSmem, e->stream>>>(e->d, sp, pa, e->ctl, stamp);
-            else
-              k_phase<double, 1><<<ncr, NT, kPhaseSmem, e->stream>>>(e->d, sp, pa, e->ctl, stamp);
-          } else {
-            if (mode == 0)
-              k_phase<float, 0><<<ncr, NT, kPhaseSmem, e->stream>>>(e->d, sp, pa, e->ctl, stamp);
-            else
-              k_phase<float, 1><<<ncr, NT, kPhaseSmem, e->stream>>>(e->d, sp, pa, e->ctl, stamp);
-          }
+          launch_phase(e, mode, ncr, sp, pa, stamp);
           if (timing) {
             ck(cudaEventRecord(b, e->stream), "event");
             phase_ev.emplace_back(a, b);

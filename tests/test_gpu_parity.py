@@ -291,3 +291,30 @@ def test_posterior_statistics_within_seed_spread(E, oc):
         a, b = gpu[:, c], ref[:, c]
         se = np.sqrt(a.var(ddof=1) / len(a) + b.var(ddof=1) / len(b))
         assert abs(a.mean() - b.mean()) <= 2.5 * se + 0.02, (name, a.mean(), b.mean(), se)
+
+
+def test_production_many_regions(E, oc):
+    # more same-colored regions than SMs (several CTA waves per phase, as at
+    # configs 2-4); trajectories must still match the oracle
+    m = _mapped_model(S=24, T=2400.0, n_regions=400, x_max=1000.0, lam_events=150)
+    w = oc.sample_world(m, 21)
+    w32 = O.World(m, w.events, w.signals.astype(np.float32).astype(np.float64))
+    s = O.Sampler(steps_per_epoch=8, epochs=3, n_regions=400, seed=13, dynamic=1, rng_mode=1)
+    _prod_vs_oracle(E, oc, m, w32, s, init=w.events, dtype=np.float32)
+
+
+def test_replay_many_regions(E, oc):
+    m = _mapped_model(S=24, T=2400.0, n_regions=400, x_max=1000.0, lam_events=150)
+    w = oc.sample_world(m, 22)
+    s = O.Sampler(steps_per_epoch=8, epochs=2, n_regions=400, seed=14, dynamic=1)
+    r = oc.run_chromatic(w, s, init=w.events, tape=True)
+    eng = E.Engine(engine_model(m), w.signals, event_capacity=1024)
+    eng.set_hypothesis(E.Events(w.events.ids, w.events.x, w.events.t, w.events.arr))
+    tr = eng.run_chromatic(engine_sampler(s), tape=r["tape"], tape_arrivals=r["tape_arr"])
+    t = r["tape"]
+    drawn = t["u_drawn"] == 1
+    tie = np.zeros(len(t), bool)
+    tie[drawn] = np.abs(t["log_r"][drawn] - np.log(t["u"][drawn])) < TIE
+    assert not ((tr.step_out["accepted"] != t["accepted"]) & ~tie).any()
+    assert np.array_equal(tr.final.ids, r["final"].ids)
+    assert np.array_equal(tr.final.arrivals, r["final"].arr)
