@@ -481,65 +481,96 @@ __global__ void __launch_bounds__(NTT, MINB)
       tc = now;
     }
     {
-      // work items: (proposal q, tile of 32 station pairs), spread over warps
       const int np_now = s_np;
-      int cur_q = -1;
-      double sig = 0.0, arr = 0.0;
-      int cnt = 0;
-      const int n_items = m * T_per;
-      int q = 0, tile = warp;  // t = q * T_per + tile, advanced without division
-      while (tile >= T_per) {
-        tile -= T_per;
-        ++q;
-      }
-      for (int t = warp; t < n_items; t += NWT, tile += NWT) {
+      // Two item orders. Many tiles per warp (configs 2-4): one item = one
+      // tile, the warp scores every proposal of the round on it back to back,
+      // so the later proposals (same region, overlapping rows) hit the lines
+      // the first brought into L1. Few tiles (config 1): items (proposal,
+      // tile) proposal-major, which balances the warps better.
+      if (T_per >= 4 * NWT) {
+        for (int tile = warp; tile < T_per; tile += NWT) {
+#pragma unroll 1
+          for (int q = 0; q < m; ++q) {
+            const Prop& P = prop[buf][q];
+            if (P.skip) continue;
+            if (MODE == 0 && P.type == 3 && tile != 0) continue;
+            PassIn in;
+            in.src = P.na == 0 ? SRC_NONE
+                               : (MODE == 1 ? SRC_ROWS : (P.type == 0 ? SRC_BIRTH : SRC_SHIFT));
+            in.rows[0] = pa.tape_arr + (MODE == 1 ? P.tape_off : 0);
+            in.rows[1] = in.rows[0] + d.S;
+            in.seed = sp.seed;
+            in.sweep = (uint32_t)pa.epoch;
+            in.region = (uint32_t)region;
+            in.step = (uint32_t)(i0 + q);
+            in.wlo = 0;
+            in.whi = d.n;
+            double sig = 0.0, arr = 0.0;
+            int cnt = 0;
+            score_item<MODE, YT>(d, P, in, tile, np_now, pold, pnew, Ts, sig, arr, cnt);
+            sig = warp_sum(sig);
+            arr = warp_sum(arr);
+            cnt = (int)__reduce_add_sync(0xffffffffu, (unsigned)cnt);
+            if (lane == 0) {
+              red_sig[warp][q] += sig;
+              red_arr[warp][q] += arr;
+              red_cnt[warp][q] += cnt;
+            }
+          }
+        }
+      } else {
+        int cur_q = -1;
+        double sig = 0.0, arr = 0.0;
+        int cnt = 0;
+        const int n_items = m * T_per;
+        int q = 0, tile = warp;  // t = q * T_per + tile, advanced without division
         while (tile >= T_per) {
           tile -= T_per;
           ++q;
         }
-        if (q != cur_q) {
-          if (cur_q >= 0) {
-            sig = warp_sum(sig);
-            arr = warp_sum(arr);
-            cnt = __reduce_add_sync(0xffffffffu, (unsigned)cnt);
-            if (lane == 0) {
-              red_sig[warp][cur_q] += sig;
-              red_arr[warp][cur_q] += arr;
-              red_cnt[warp][cur_q] += cnt;
-            }
-            sig = arr = 0.0;
-            cnt = 0;
+        for (int t = warp; t < n_items; t += NWT, tile += NWT) {
+          while (tile >= T_per) {
+            tile -= T_per;
+            ++q;
           }
-          cur_q = q;
+          if (q != cur_q) {
+            if (cur_q >= 0) {
+              sig = warp_sum(sig);
+              arr = warp_sum(arr);
+              cnt = __reduce_add_sync(0xffffffffu, (unsigned)cnt);
+              if (lane == 0) {
+                red_sig[warp][cur_q] += sig;
+                red_arr[warp][cur_q] += arr;
+                red_cnt[warp][cur_q] += cnt;
+              }
+              sig = arr = 0.0;
+              cnt = 0;
+            }
+            cur_q = q;
+          }
+          const Prop& P = prop[buf][q];
+          PassIn in;
+          in.src = P.na == 0 ? SRC_NONE
+                             : (MODE == 1 ? SRC_ROWS : (P.type == 0 ? SRC_BIRTH : SRC_SHIFT));
+          in.rows[0] = pa.tape_arr + (MODE == 1 ? P.tape_off : 0);
+          in.rows[1] = in.rows[0] + d.S;
+          in.seed = sp.seed;
+          in.sweep = (uint32_t)pa.epoch;
+          in.region = (uint32_t)region;
+          in.step = (uint32_t)(i0 + q);
+          in.wlo = 0;
+          in.whi = d.n;
+          score_item<MODE, YT>(d, P, in, tile, np_now, pold, pnew, Ts, sig, arr, cnt);
         }
-        const Prop& P = prop[buf][q];
-        PassIn in;
-        in.src = P.na == 0 ? SRC_NONE
-                           : (MODE == 1 ? SRC_ROWS : (P.type == 0 ? SRC_BIRTH : SRC_SHIFT));
-        in.rows[0] = pa.tape_arr + (MODE == 1 ? P.tape_off : 0);
-        in.rows[1] = in.rows[0] + d.S;
-        in.seed = sp.seed;
-        in.sweep = (uint32_t)pa.epoch;
-        in.region = (uint32_t)region;
-        in.step = (uint32_t)(i0 + q);
-        in.wlo = 0;
-        in.whi = d.n;
-        const long long t0i = clock64();
-        score_item<MODE, YT>(d, P, in, tile, np_now, pold, pnew, Ts, sig, arr, cnt);
-        if (kProfItems && lane == 0 && !P.skip) {
-          const int ty = P.type < 0 ? 5 : P.type;
-          atomicAdd(&s_tprof[0][ty], (unsigned long long)(clock64() - t0i));
-          atomicAdd(&s_tprof[1][ty], 1ull);
-        }
-      }
-      if (cur_q >= 0) {
-        sig = warp_sum(sig);
-        arr = warp_sum(arr);
-        cnt = __reduce_add_sync(0xffffffffu, (unsigned)cnt);
-        if (lane == 0) {
-          red_sig[warp][cur_q] += sig;
-          red_arr[warp][cur_q] += arr;
-          red_cnt[warp][cur_q] += cnt;
+        if (cur_q >= 0) {
+          sig = warp_sum(sig);
+          arr = warp_sum(arr);
+          cnt = __reduce_add_sync(0xffffffffu, (unsigned)cnt);
+          if (lane == 0) {
+            red_sig[warp][cur_q] += sig;
+            red_arr[warp][cur_q] += arr;
+            red_cnt[warp][cur_q] += cnt;
+          }
         }
       }
     }
