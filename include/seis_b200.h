@@ -137,6 +137,14 @@ int seis_set_hypothesis(seis_engine* eng, int64_t n, const uint64_t* ids, const 
 int seis_get_hypothesis(seis_engine* eng, int64_t cap, int64_t* n, uint64_t* ids, double* x,
                         double* t, double* arrivals);
 
+/* Trace snapshots (reference Trace::snapshots, samplers.hpp:80-85,430-433):
+ * with a capacity set, seis_run_chromatic stores the event table (id, x, t)
+ * at every trace row once executed >= burn_in_fraction * planned steps.
+ * Snapshots are packed back to back: snapshot i holds snap_count[i] events. */
+int seis_set_snapshot_capacity(seis_engine* eng, int64_t max_events, int64_t max_snapshots);
+int seis_get_snapshots(seis_engine* eng, int64_t cap_snap, int64_t* n_snap, int64_t* snap_step,
+                       int64_t* snap_count, int64_t cap_ev, uint64_t* ids, double* x, double* t);
+
 int seis_partition(double T, double l, double offset, double tau, int64_t cap,
                    int64_t* n_regions, double* boundaries /* cap */, int32_t* colors /* cap */,
                    int32_t* n_colors);

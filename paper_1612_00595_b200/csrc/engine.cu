@@ -1214,6 +1214,45 @@ __global__ void k_max_id(Table tab, const Ctl* ctl, unsigned long long* out) {
 
 __global__ void k_record(const Ctl* ctl, long long* count_out) { *count_out = ctl->n_events; }
 
+// arrivals of hypothesis rows: pool slot rows <-> dense [m][S] (one launch,
+// one copy, instead of one copy per event)
+__global__ void k_gather_arrivals(const double* pool, const int* slot, int S, int S_pad, int m,
+                                  double* out) {
+  const int e = blockIdx.y;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < S; j += gridDim.x * blockDim.x)
+    out[(size_t)e * S + j] = pool[(size_t)slot[e] * S_pad + j];
+}
+
+__global__ void k_scatter_arrivals(const double* in, const long long* row_of_slot, int S,
+                                   int S_pad, int n, double* pool) {
+  const int slot = blockIdx.y;
+  const double* src = in + (size_t)row_of_slot[slot] * S;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < S_pad; j += gridDim.x * blockDim.x)
+    pool[(size_t)slot * S_pad + j] = j < S ? src[j] : 0.0;
+}
+
+// Trace snapshot (samplers.hpp:430-433): append the event table to the arena
+__global__ void k_snapshot(Table tab, const Ctl* ctl, unsigned long long* arena_id,
+                           double* arena_x, double* arena_t, long long* arena_top,
+                           long long arena_cap, long long* rec) {
+  __shared__ long long base;
+  const int N = ctl->n_events;
+  if (threadIdx.x == 0) {
+    base = *arena_top;
+    const long long nb = base + N <= arena_cap ? base + N : base;
+    *arena_top = nb;
+    rec[0] = base;
+    rec[1] = nb > base ? N : -1;  // -1: arena full
+  }
+  __syncthreads();
+  if (base + N > arena_cap) return;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    arena_id[base + i] = tab.id[i];
+    arena_x[base + i] = tab.x[i];
+    arena_t[base + i] = tab.t[i];
+  }
+}
+
 __global__ void k_reset_counters(Ctl* ctl) {
   ctl->scored = ctl->changed = ctl->arrvals = ctl->accepted = ctl->id_mismatch = 0ull;
   ctl->speculative = 0ull;
@@ -1330,6 +1369,15 @@ struct seis_engine {
   int* fate_slot = nullptr;
   int stamp = 0;
   int n_sm = 148;
+  // trace snapshots of the last run (samplers.hpp:80-85,430-433)
+  int64_t snap_cap = 0;
+  unsigned long long* snap_id = nullptr;
+  double* snap_x = nullptr;
+  double* snap_t = nullptr;
+  long long* snap_top = nullptr;
+  long long* snap_rec = nullptr;  // [max_snaps][2] {offset, count}
+  int64_t snap_rec_cap = 0;
+  std::vector<int64_t> snap_steps;
 
   ~seis_engine() {
     cudaFree(stations);
@@ -1354,6 +1402,11 @@ struct seis_engine {
     cudaFree(fate_x);
     cudaFree(fate_t);
     cudaFree(fate_slot);
+    cudaFree(snap_id);
+    cudaFree(snap_x);
+    cudaFree(snap_t);
+    cudaFree(snap_top);
+    cudaFree(snap_rec);
     if (stream) cudaStreamDestroy(stream);
   }
 };
@@ -1599,7 +1652,8 @@ int seis_set_hypothesis(seis_engine* e, int64_t N, const uint64_t* ids, const do
     for (int64_t i = 1; i < N; ++i)
       if (ids[order[i]] == ids[order[i - 1]]) throw std::invalid_argument("duplicate event id");
     std::vector<unsigned long long> hid(N);
-    std::vector<double> hx(N), ht(N), ha((size_t)N * e->S_pad, 0.0);
+    std::vector<double> hx(N), ht(N);
+    std::vector<long long> row(N);
     std::vector<int> hs(N), fs(e->cap);
     for (int64_t i = 0; i < N; ++i) {
       const int64_t k = order[i];
@@ -1607,11 +1661,11 @@ int seis_set_hypothesis(seis_engine* e, int64_t N, const uint64_t* ids, const do
       hx[i] = x[k];
       ht[i] = t[k];
       hs[i] = (int)i;
-      std::copy(arrivals + k * e->S, arrivals + (k + 1) * e->S, ha.begin() + i * e->S_pad);
+      row[i] = k;  // slot i holds input row k
     }
     // free stack: slots N..cap-1 (top of stack = lowest)
     int nf = 0;
-    for (int s = e->cap - 1; s >= (int)N; --s) fs[nf++] = s;
+    for (int s2 = e->cap - 1; s2 >= (int)N; --s2) fs[nf++] = s2;
     e->cur = 0;
     Table& tb = e->tab[0];
     if (N) {
@@ -1619,7 +1673,18 @@ int seis_set_hypothesis(seis_engine* e, int64_t N, const uint64_t* ids, const do
       ck(cudaMemcpy(tb.x, hx.data(), N * 8, cudaMemcpyHostToDevice), "H2D");
       ck(cudaMemcpy(tb.t, ht.data(), N * 8, cudaMemcpyHostToDevice), "H2D");
       ck(cudaMemcpy(tb.slot, hs.data(), N * 4, cudaMemcpyHostToDevice), "H2D");
-      ck(cudaMemcpy(e->pool, ha.data(), ha.size() * 8, cudaMemcpyHostToDevice), "H2D");
+      double* raw = dalloc<double>((size_t)N * e->S);
+      long long* drow = dalloc<long long>(N);
+      ck(cudaMemcpyAsync(raw, arrivals, (size_t)N * e->S * 8, cudaMemcpyHostToDevice, e->stream),
+         "H2D arrivals");
+      ck(cudaMemcpyAsync(drow, row.data(), (size_t)N * 8, cudaMemcpyHostToDevice, e->stream),
+         "H2D");
+      dim3 grid((unsigned)std::min(64, (e->S_pad + 255) / 256), (unsigned)N);
+      k_scatter_arrivals<<<grid, 256, 0, e->stream>>>(raw, drow, e->S, e->S_pad, (int)N, e->pool);
+      ck(cudaGetLastError(), "k_scatter_arrivals");
+      ck(cudaStreamSynchronize(e->stream), "sync");
+      cudaFree(raw);
+      cudaFree(drow);
     }
     if (nf) ck(cudaMemcpy(e->free_stack, fs.data(), (size_t)nf * 4, cudaMemcpyHostToDevice), "H2D");
     Ctl c{};
@@ -1648,12 +1713,64 @@ int seis_get_hypothesis(seis_engine* e, int64_t cap, int64_t* n, uint64_t* ids, 
     ck(cudaMemcpy(x, tb.x, m * 8, cudaMemcpyDeviceToHost), "D2H");
     ck(cudaMemcpy(t, tb.t, m * 8, cudaMemcpyDeviceToHost), "D2H");
     if (arrivals) {
-      std::vector<int> sl(m);
-      ck(cudaMemcpy(sl.data(), tb.slot, m * 4, cudaMemcpyDeviceToHost), "D2H");
-      for (int64_t i = 0; i < m; ++i)
-        ck(cudaMemcpy(arrivals + i * e->S, e->pool + (size_t)sl[i] * e->S_pad, e->S * 8,
-                      cudaMemcpyDeviceToHost),
-           "D2H");
+      double* buf = dalloc<double>((size_t)m * e->S);
+      dim3 grid((unsigned)std::min(64, (e->S + 255) / 256), (unsigned)m);
+      k_gather_arrivals<<<grid, 256, 0, e->stream>>>(e->pool, tb.slot, e->S, e->S_pad, (int)m, buf);
+      ck(cudaGetLastError(), "k_gather_arrivals");
+      ck(cudaMemcpyAsync(arrivals, buf, (size_t)m * e->S * 8, cudaMemcpyDeviceToHost, e->stream),
+         "D2H arrivals");
+      ck(cudaStreamSynchronize(e->stream), "sync");
+      cudaFree(buf);
+    }
+  });
+}
+
+int seis_set_snapshot_capacity(seis_engine* e, int64_t max_events, int64_t max_snapshots) {
+  return guarded([&] {
+    if (max_events < 0 || max_snapshots < 0) throw std::invalid_argument("negative capacity");
+    cudaFree(e->snap_id);
+    cudaFree(e->snap_x);
+    cudaFree(e->snap_t);
+    cudaFree(e->snap_top);
+    cudaFree(e->snap_rec);
+    e->snap_id = nullptr;
+    e->snap_x = e->snap_t = nullptr;
+    e->snap_top = e->snap_rec = nullptr;
+    e->snap_cap = max_events;
+    e->snap_rec_cap = max_snapshots;
+    e->snap_steps.clear();
+    if (max_events == 0 || max_snapshots == 0) {
+      e->snap_cap = 0;
+      return;
+    }
+    e->snap_id = dalloc<unsigned long long>(max_events);
+    e->snap_x = dalloc<double>(max_events);
+    e->snap_t = dalloc<double>(max_events);
+    e->snap_top = dalloc<long long>(1);
+    e->snap_rec = dalloc<long long>(2 * max_snapshots);
+  });
+}
+
+int seis_get_snapshots(seis_engine* e, int64_t cap_snap, int64_t* n_snap, int64_t* snap_step,
+                       int64_t* snap_count, int64_t cap_ev, uint64_t* ids, double* x, double* t) {
+  return guarded([&] {
+    const int64_t ns = (int64_t)e->snap_steps.size();
+    *n_snap = ns;
+    if (ns == 0 || cap_snap <= 0) return;
+    std::vector<long long> rec(2 * ns);
+    ck(cudaMemcpy(rec.data(), e->snap_rec, rec.size() * 8, cudaMemcpyDeviceToHost), "D2H");
+    int64_t total = 0;
+    for (int64_t i = 0; i < ns && i < cap_snap; ++i) {
+      if (rec[2 * i + 1] < 0) throw std::runtime_error("snapshot arena full: raise max_events");
+      snap_step[i] = e->snap_steps[i];
+      snap_count[i] = rec[2 * i + 1];
+      total = std::max<int64_t>(total, rec[2 * i] + rec[2 * i + 1]);
+    }
+    if (total > cap_ev) throw std::invalid_argument("event buffer too small for the snapshots");
+    if (total > 0) {
+      ck(cudaMemcpy(ids, e->snap_id, total * 8, cudaMemcpyDeviceToHost), "D2H");
+      ck(cudaMemcpy(x, e->snap_x, total * 8, cudaMemcpyDeviceToHost), "D2H");
+      ck(cudaMemcpy(t, e->snap_t, total * 8, cudaMemcpyDeviceToHost), "D2H");
     }
   });
 }
@@ -1940,6 +2057,23 @@ extern "C" int seis_run_chromatic(seis_engine* e, const seis_sampler_cfg* sc, in
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> phase_ev;
     int64_t n_rows = 0;
     std::vector<int64_t> h_row_step;
+    // snapshots at record points once executed >= burn (samplers.hpp:411-413,430-433)
+    const int64_t planned = sc->epochs * sc->steps_per_epoch * sc->n_regions;
+    const int64_t burn = (int64_t)(sc->burn_in_fraction * (double)planned);
+    e->snap_steps.clear();
+    if (e->snap_cap > 0) {
+      const long long zero = 0;
+      ck(cudaMemcpyAsync(e->snap_top, &zero, 8, cudaMemcpyHostToDevice, e->stream), "H2D");
+    }
+    auto take_snapshot = [&](int64_t executed) {
+      if (e->snap_cap <= 0 || executed < burn) return;
+      if ((int64_t)e->snap_steps.size() >= e->snap_rec_cap) return;
+      k_snapshot<<<1, 256, 0, e->stream>>>(e->tab[e->cur], e->ctl, e->snap_id, e->snap_x,
+                                            e->snap_t, e->snap_top, e->snap_cap,
+                                            e->snap_rec + 2 * e->snap_steps.size());
+      ++launches;
+      e->snap_steps.push_back(executed);
+    };
     auto record_row = [&](int64_t executed) {
       if (n_rows < row_cap) {
         if (sc->record_log_joint) {
@@ -1951,6 +2085,7 @@ extern "C" int seis_run_chromatic(seis_engine* e, const seis_sampler_cfg* sc, in
         h_row_step.push_back(executed);
       }
       ++n_rows;
+      if (executed > 0 || n_rows > 1) take_snapshot(executed);
     };
     ck(cudaEventRecord(ev_start, e->stream), "event");
     record_row(0);

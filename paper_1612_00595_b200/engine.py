@@ -66,7 +66,7 @@ EXPORTS = ("seis_last_error", "seis_engine_create", "seis_engine_destroy", "seis
            "seis_set_hypothesis", "seis_get_hypothesis", "seis_partition", "seis_assign_regions",
            "seis_partition_offset", "seis_score_batch", "seis_log_joint", "seis_run_chromatic",
            "seis_world_last_error", "seis_world_generate", "seis_world_with_events",
-           "seis_thomas_events")
+           "seis_thomas_events", "seis_set_snapshot_capacity", "seis_get_snapshots")
 
 _LIB = None
 
@@ -97,6 +97,8 @@ def load_library(path: str | None = None) -> C.CDLL:
     L.seis_world_generate.argtypes = [P, P, i64, u64, i64, P, P, P, P, P, P, i32, i32]
     L.seis_world_with_events.argtypes = [P, P, i64, i64, P, P, u64, P, P, i32, i32]
     L.seis_thomas_events.argtypes = [u64, f64, f64, f64, f64, f64, f64, i64, P, P, P]
+    L.seis_set_snapshot_capacity.argtypes = [P, i64, i64]
+    L.seis_get_snapshots.argtypes = [P, i64, P, P, P, i64, P, P, P]
     if path == _build.LIB:
         _LIB = L
     return L
@@ -185,6 +187,16 @@ class Events:
 
 
 @dataclass
+class Snapshot:
+    """reference Snapshot (samplers.hpp:80-85): the hypothesis at a trace row."""
+    id: int
+    step: int
+    ids: np.ndarray
+    x: np.ndarray
+    t: np.ndarray
+
+
+@dataclass
 class Trace:
     """reference Trace (samplers.hpp:97-103) + engine measurement counters."""
     row_step: np.ndarray
@@ -195,6 +207,34 @@ class Trace:
     stats: dict
     final: Events | None = None
     step_out: np.ndarray | None = None
+    snapshots: list = field(default_factory=list)
+
+    def write_trace_csv(self, path: str) -> None:
+        """write_trace_csv (samplers.hpp:511-516). wall_seconds is not
+        measured per row on the device: written as 0."""
+        with open(path, "w") as f:
+            f.write("wall_seconds,step,log_joint,event_count\n")
+            for st, lj, c in zip(self.row_step, self.row_log_joint, self.row_count):
+                f.write(f"0,{int(st)},{_fmt(lj)},{int(c)}\n")
+
+    def write_samples_csv(self, path: str) -> None:
+        """write_samples_csv (samplers.hpp:518-524)."""
+        with open(path, "w") as f:
+            f.write("snapshot_id,event_id,x,t\n")
+            for sn in self.snapshots:
+                for i, x, t in zip(sn.ids, sn.x, sn.t):
+                    f.write(f"{sn.id},{int(i)},{_fmt(x)},{_fmt(t)}\n")
+
+
+def _fmt(v: float) -> str:
+    """format_double (csv.hpp:15-19): shortest round-trip decimal."""
+    v = float(v)
+    if v == float("inf"):
+        return "inf"
+    if v == float("-inf"):
+        return "-inf"
+    r = repr(v)
+    return r[:-2] if r.endswith(".0") else r
 
 
 @dataclass
@@ -354,6 +394,31 @@ class Engine:
                                           _p(a) if arrivals else None), self.L)
         return Events(ids[:N], x[:N], t[:N], a[:N] if arrivals else None)
 
+    def set_snapshot_capacity(self, max_events: int, max_snapshots: int = 4096):
+        """keep trace snapshots (reference Trace::snapshots) of the next runs."""
+        _check(self.L.seis_set_snapshot_capacity(self.h, max_events, max_snapshots), self.L)
+        self._snap_cap = (max_events, max_snapshots)
+
+    def _get_snapshots(self) -> list:
+        cap = getattr(self, "_snap_cap", (0, 0))
+        if cap[0] == 0:
+            return []
+        ns = i64(0)
+        steps = np.zeros(cap[1], np.int64)
+        counts = np.zeros(cap[1], np.int64)
+        ids = np.zeros(max(cap[0], 1), np.uint64)
+        x = np.zeros(max(cap[0], 1))
+        t = np.zeros(max(cap[0], 1))
+        _check(self.L.seis_get_snapshots(self.h, cap[1], C.byref(ns), _p(steps), _p(counts),
+                                         cap[0], _p(ids), _p(x), _p(t)), self.L)
+        out, off = [], 0
+        for i in range(min(ns.value, cap[1])):
+            c = int(counts[i])
+            out.append(Snapshot(i, int(steps[i]), ids[off:off + c].copy(), x[off:off + c].copy(),
+                                t[off:off + c].copy()))
+            off += c
+        return out
+
     def log_joint(self) -> float:
         out = f64(0)
         _check(self.L.seis_log_joint(self.h, C.byref(out)), self.L)
@@ -424,6 +489,7 @@ class Engine:
                    step_out=out)
         if final:
             tr.final = self.get_hypothesis()
+        tr.snapshots = self._get_snapshots()
         return tr
 
 

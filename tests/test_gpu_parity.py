@@ -318,3 +318,31 @@ def test_replay_many_regions(E, oc):
     assert not ((tr.step_out["accepted"] != t["accepted"]) & ~tie).any()
     assert np.array_equal(tr.final.ids, r["final"].ids)
     assert np.array_equal(tr.final.arrivals, r["final"].arr)
+
+
+def test_trace_rows_and_snapshots(E, oc, tmp_path):
+    # Trace rows / snapshots (samplers.hpp:73-103,424-434): rows at record
+    # points, snapshots from burn-in on, the last one equal to the final
+    m = default_model()
+    w = golden_world("w1", m)
+    s = O.Sampler(steps_per_epoch=100, epochs=10, n_regions=4, seed=5, dynamic=1, rng_mode=1,
+                  record_every=300, burn_in_fraction=0.5)
+    ro = oc.run_chromatic(w, s, tape=False, rowlj=True)
+    eng = E.Engine(engine_model(m), w.signals)
+    eng.set_snapshot_capacity(10000, 64)
+    tr = eng.run_chromatic(engine_sampler(s, record_log_joint=True))
+    assert np.array_equal(tr.row_step, ro["row_step"])
+    assert np.array_equal(tr.row_count, ro["row_count"])
+    burn = int(0.5 * s.epochs * s.steps_per_epoch * s.n_regions)
+    want = [int(v) for v in ro["row_step"][1:] if v >= burn]
+    assert [sn.step for sn in tr.snapshots] == want
+    for sn, c in zip(tr.snapshots, [int(c) for st, c in zip(ro["row_step"][1:], ro["row_count"][1:])
+                                     if st >= burn]):
+        assert len(sn.ids) == c
+    last = tr.snapshots[-1]
+    assert np.array_equal(last.ids, ro["final"].ids) and np.array_equal(last.x, ro["final"].x)
+    tr.write_trace_csv(str(tmp_path / "trace.csv"))
+    tr.write_samples_csv(str(tmp_path / "samples.csv"))
+    lines = open(tmp_path / "samples.csv").read().splitlines()
+    assert lines[0] == "snapshot_id,event_id,x,t"
+    assert len(lines) == 1 + sum(len(sn.ids) for sn in tr.snapshots)
