@@ -159,6 +159,8 @@ int seis_log_joint(seis_engine* eng, double* out);
 
 /* mode 0: production (philox stream spec v1); mode 1: replay `tape` (n_tape
  * steps in driver order, arrivals in tape_arr) writing step_out[n_tape].
+ * In mode 0 a non-NULL step_out (capacity n_tape >= the run's steps, tape
+ * NULL) receives the production run's own per-step decisions, driver order.
  * Trace rows go to row_step/row_log_joint/row_count (capacity row_cap, may be
  * NULL). The final hypothesis stays on the engine (seis_get_hypothesis). */
 int seis_run_chromatic(seis_engine* eng, const seis_sampler_cfg* sc, int32_t mode,
@@ -166,6 +168,19 @@ int seis_run_chromatic(seis_engine* eng, const seis_sampler_cfg* sc, int32_t mod
                        int64_t n_tape_arr, seis_step_out* step_out, int64_t row_cap,
                        int64_t* row_step, double* row_log_joint, int64_t* row_count,
                        seis_run_stats* stats);
+
+/* run_naive_parallel (samplers.hpp:321-394), the uncolored comparison
+ * sampler: every region runs epochs x steps_per_epoch steps from the empty
+ * hypothesis (the engine's must be empty) against its own events only, prior
+ * support = the region, likelihood window = signal_window (partition.hpp:94-102).
+ * Same arguments as seis_run_chromatic (sc->dynamic ignored); the union of the
+ * regions' final events becomes the engine's hypothesis. Trace rows: union
+ * event counts at every checkpoint, log_joint at the last row only. */
+int seis_run_naive(seis_engine* eng, const seis_sampler_cfg* sc, int32_t mode,
+                   const seis_tape_step* tape, int64_t n_tape, const double* tape_arr,
+                   int64_t n_tape_arr, seis_step_out* step_out, int64_t row_cap,
+                   int64_t* row_step, double* row_log_joint, int64_t* row_count,
+                   seis_run_stats* stats);
 
 /* ---- synthetic inputs (worldgen.hpp:20-86, bit-exact with the reference
  * generator; host C++ so the fp64 libm draws match). Not on the hot path. */

@@ -178,6 +178,9 @@ class Oracle:
         self._run = g("run_chromatic")
         self._run.restype = P
         self._run.argtypes = [P, P, P, i64, P, P, P, P, i64, i64]
+        self._naive = g("run_naive")
+        self._naive.restype = P
+        self._naive.argtypes = [P, P, P, i64, i64]
         for n in ("run_status",):
             getattr(L, pre + n).argtypes = [P]
         g("run_counts").argtypes = [P] + [P] * 6
@@ -305,7 +308,7 @@ class Oracle:
 
     # -- samplers.hpp
     def run_chromatic(self, world: World, sampler: Sampler, init: Events | None = None,
-                      tape: bool = True, rowlj: bool = False) -> dict:
+                      tape: bool = True, rowlj: bool = False, naive: bool = False) -> dict:
         model = world.model
         m = model.c()
         s = sampler.c()
@@ -317,13 +320,16 @@ class Oracle:
         t = np.ascontiguousarray(init.t, np.float64)
         arr = np.ascontiguousarray(init.arr, np.float64)
         pre = self.pre
-        h = self._run(C.byref(m), _p(sig), C.byref(s), init.N, _p(ids), _p(x), _p(t), _p(arr),
-                      int(tape), int(rowlj))
+        if naive:
+            h = self._naive(C.byref(m), _p(sig), C.byref(s), int(tape), int(rowlj))
+        else:
+            h = self._run(C.byref(m), _p(sig), C.byref(s), init.N, _p(ids), _p(x), _p(t),
+                          _p(arr), int(tape), int(rowlj))
         L = self.lib
         try:
             st = getattr(L, pre + "run_status")(h)
             if st:
-                raise RuntimeError(f"run_chromatic status {st}: {self.err()}")
+                raise RuntimeError(f"run status {st}: {self.err()}")
             cnt = [i64(0) for _ in range(6)]
             getattr(L, pre + "run_counts")(h, *[C.byref(c) for c in cnt])
             n_tape, n_tarr, n_rows, n_final, total_steps, total_acc = [c.value for c in cnt]
@@ -351,8 +357,13 @@ def have_ref() -> bool:
     return os.path.exists(REF_SO)
 
 
-def ref_run_sampler(world: World, sampler: Sampler, workers: int = 1, cap: int = 1 << 16):
-    """The reference's own run_sampler (chromatic static/dynamic from empty)."""
+def ref_run_sampler(world: World, sampler: Sampler, workers: int = 1, cap: int = 1 << 16,
+                    naive: bool = False):
+    """The reference's own run_sampler (chromatic static/dynamic, or naive, from empty)."""
+    if naive:
+        import copy
+        sampler = copy.copy(sampler)
+        sampler.dynamic = 2
     L = C.CDLL(REF_SO)
     f = L.sr_run_sampler
     f.argtypes = [P, P, P, i64, i64, P, P, P, P, P, P, P, P]

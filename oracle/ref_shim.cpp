@@ -412,6 +412,128 @@ sr_run* sr_run_chromatic(const so_model* mm, const double* signals, const so_sam
   return run;
 }
 
+
+// Tape-recording naive driver composed from reference functions: the control
+// flow of run_naive_parallel (samplers.hpp:321-394) with run_region_steps and
+// mh_step unrolled as in sr_run_chromatic.
+sr_run* sr_run_naive(const so_model* mm, const double* signals, const so_sampler* s,
+                     int64_t want_tape, int64_t want_rowlj) {
+  auto* run = new sr_run;
+  run->status = guarded([&] {
+    if (s->rng_mode != 0) throw std::invalid_argument("reference supports rng_mode 0 only");
+    const ModelConfig config = to_config(mm);
+    SamplerConfig sc = to_sampler(s);
+    sc.algorithm = Algorithm::NaiveParallel;
+    config.validate();
+    sc.validate();
+    const std::size_t S = config.n_stations();
+    run->S = S;
+    const ObservedSignals sig = to_signals(config, signals);
+    const double tau = config.x_max / config.v;
+    const Partition partition = build_partition(config.T, config.T / sc.n_regions, 0.0);
+    const std::size_t n_regions = partition.n_regions();
+    const std::int64_t spr = sc.epochs * sc.steps_per_epoch;
+    std::vector<std::vector<std::vector<Event>>> cps(n_regions);
+    std::vector<std::int64_t> cp_steps{0};
+    for (std::size_t m = 0; m < n_regions; ++m) {
+      World local{config, {}, sig};
+      const TimeRegion region = partition.region(m);
+      ScoreOptions opts;
+      opts.window = signal_window(partition.regions[m], tau, config.T, config.sample_rate);
+      opts.prior_support = region;
+      Rng rng = derive_stream(sc.seed, streams::kChain, 0, 0, m);
+      std::uint64_t id_base = (static_cast<std::uint64_t>(m) + 1) << 32;
+      cps[m].push_back(local.events);
+      std::int64_t done = 0;
+      while (done < spr) {
+        const std::int64_t chunk = std::min(sc.record_every, spr - done);
+        std::int64_t births = 0;
+        for (std::int64_t i = 0; i < chunk; ++i) {
+          const MoveType type = sc.moves.sample(rng);
+          const Proposal p = propose_move(type, region, local.events, config, sc.moves,
+                                          sc.step_sizes,
+                                          id_base + static_cast<std::uint64_t>(births), rng);
+          so_tape_rec rec{};
+          rec.region = static_cast<int64_t>(m);
+          rec.slot = static_cast<int64_t>(m);
+          rec.step = done + i;
+          rec.type = static_cast<int64_t>(p.type);
+          rec.is_null = p.null;
+          rec.n_removed = static_cast<int64_t>(p.change.removed.size());
+          rec.n_added = static_cast<int64_t>(p.change.added.size());
+          for (std::size_t r = 0; r < p.change.removed.size(); ++r)
+            rec.removed_id[r] = p.change.removed[r].id;
+          for (std::size_t a = 0; a < p.change.added.size(); ++a) {
+            rec.added_id[a] = p.change.added[a].id;
+            rec.added_x[a] = p.change.added[a].x;
+            rec.added_t[a] = p.change.added[a].t;
+            if (want_tape) {
+              if (a == 0) rec.added_arr_off = static_cast<int64_t>(run->tarr.size());
+              run->tarr.insert(run->tarr.end(), p.change.added[a].arrivals.begin(),
+                               p.change.added[a].arrivals.end());
+            }
+          }
+          rec.logq_f = p.log_q_forward;
+          rec.logq_r = p.log_q_reverse;
+          rec.delta = kLogZero;
+          bool acc = false;
+          if (!p.null) {
+            bool constrained_out = false;
+            for (const Event& e : p.change.added)
+              if (!region.contains(e.t)) {
+                constrained_out = true;
+                break;
+              }
+            double log_r;
+            if (constrained_out) {
+              log_r = kLogZero;
+            } else {
+              rec.delta = delta_log_joint(local, p.change, opts);
+              log_r = log_accept_ratio(rec.delta, p);
+            }
+            rec.constrained_out = constrained_out;
+            rec.scored = !constrained_out;
+            rec.log_r = log_r;
+            if (log_r >= 0.0) {
+              acc = true;
+            } else {
+              const double u = rng.uniform();
+              rec.u_drawn = 1;
+              rec.u = u;
+              acc = std::log(u) < log_r;
+            }
+            if (acc) apply_change(local, p.change);
+          }
+          rec.accepted = acc;
+          if (acc) {
+            ++run->total_accepted;
+            if (p.type == MoveType::Birth) ++births;
+          }
+          if (want_tape) run->tape.push_back(rec);
+        }
+        id_base += static_cast<std::uint64_t>(births);
+        done += chunk;
+        cps[m].push_back(local.events);
+        if (m == 0) cp_steps.push_back(done);
+      }
+    }
+    World scratch{config, {}, sig};
+    for (std::size_t c = 0; c < cp_steps.size(); ++c) {
+      std::vector<Event> merged;
+      for (std::size_t m = 0; m < n_regions; ++m)
+        merged.insert(merged.end(), cps[m][c].begin(), cps[m][c].end());
+      detail::sort_by_id(merged);
+      scratch.events = merged;
+      run->row_step.push_back(cp_steps[c] * static_cast<std::int64_t>(n_regions));
+      run->row_lj.push_back(want_rowlj ? log_joint(scratch) : 0.0);
+      run->row_count.push_back(static_cast<int64_t>(merged.size()));
+      if (c + 1 == cp_steps.size()) run->final = merged;
+    }
+    run->total_steps = spr * static_cast<std::int64_t>(n_regions);
+  });
+  return run;
+}
+
 int sr_run_status(const sr_run* r) { return r->status; }
 
 void sr_run_counts(const sr_run* r, int64_t* n_tape, int64_t* n_tape_arr, int64_t* n_rows,
@@ -457,6 +579,7 @@ int sr_run_sampler(const so_model* mm, const double* signals, const so_sampler* 
   return guarded([&] {
     const ModelConfig config = to_config(mm);
     SamplerConfig sc = to_sampler(s);
+    if (s->dynamic == 2) sc.algorithm = Algorithm::NaiveParallel;
     sc.workers = static_cast<int>(workers);
     const ObservedSignals sig = to_signals(config, signals);
     const auto t0 = std::chrono::steady_clock::now();

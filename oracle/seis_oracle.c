@@ -668,6 +668,13 @@ typedef struct {
   so_rng rng;
   /* mode 1 */
   uint32_t sweep, region, step;
+  uint32_t step_base; /* global step index of this call's first step */
+  /* ScoreOptions (density.hpp:182-189): chromatic = full window and [0, T]
+   * (samplers.hpp:410); naive = signal_window and the region
+   * (samplers.hpp:345-347) */
+  int64_t wlo, whi;
+  double slo, shi;
+  int sclosed;
 } chain_t;
 
 /* proposals.hpp:65-71 */
@@ -859,13 +866,13 @@ static void apply_change(evlist_t* l, prop_t* p) {
 static int64_t run_region_steps(struct so_run* run, chain_t* c, evlist_t* local,
                                 const double* signals, int64_t steps, uint64_t id_base,
                                 int want_tape, int64_t epoch, int64_t color, int64_t slot,
-                                flat_t* flat, int64_t* idxbuf) {
+                                flat_t* flat, int64_t* idxbuf, int64_t* births_out) {
   const so_model* m = c->m;
   const so_sampler* sc = c->sc;
   const int64_t S = m->n_stations;
   int64_t births = 0, accepted = 0;
   for (int64_t i = 0; i < steps; ++i) {
-    c->step = (uint32_t)i;
+    c->step = (uint32_t)(c->step_base + i);
     seis_u32x4 d0 = {{0, 0, 0, 0}};
     double um;
     if (sc->rng_mode == 0) {
@@ -893,7 +900,7 @@ static int64_t run_region_steps(struct so_run* run, chain_t* c, evlist_t* local,
       rec->color = color;
       rec->region = c->region;
       rec->slot = slot;
-      rec->step = i;
+      rec->step = (int64_t)c->step_base + i;
       rec->type = type;
       rec->is_null = p.is_null;
       rec->n_removed = p.n_removed;
@@ -933,10 +940,9 @@ static int64_t run_region_steps(struct so_run* run, chain_t* c, evlist_t* local,
           aid[a] = p.added[a].id;
           memcpy(aarr + a * S, p.added[a].a, sizeof(double) * (size_t)S);
         }
-        /* chromatic scoring: full window, full [0, T] support (samplers.hpp:410) */
         delta = so_delta(m, signals, local->n, flat->ids, flat->x, flat->t, flat->arr, p.n_removed,
-                         p.removed_idx, p.n_added, aid, ax, at, aarr, 0, so_n_samples(m), 0.0,
-                         m->T, 1);
+                         p.removed_idx, p.n_added, aid, ax, at, aarr, c->wlo, c->whi, c->slo,
+                         c->shi, c->sclosed);
         free(aarr);
         /* log_accept_ratio, proposals.hpp:255-258 */
         log_r = delta == -INFINITY ? -INFINITY : delta + p.logq_r - p.logq_f;
@@ -967,6 +973,7 @@ static int64_t run_region_steps(struct so_run* run, chain_t* c, evlist_t* local,
     if (rec) rec->accepted = acc;
     prop_free(&p);
   }
+  if (births_out) *births_out = births;
   return accepted;
 }
 
@@ -1064,6 +1071,11 @@ so_run* so_run_chromatic(const so_model* m, const double* signals, const so_samp
         c.rclosed = (ri + 1 == nreg);
         c.sweep = (uint32_t)epoch;
         c.region = (uint32_t)ri;
+        c.wlo = 0;
+        c.whi = so_n_samples(m);
+        c.slo = 0.0;
+        c.shi = m->T;
+        c.sclosed = 1;
         if (sc->rng_mode == 0)
           c.rng = so_derive_stream(sc->seed, 5, (uint64_t)epoch, (uint64_t)color, (uint64_t)ri);
         evlist_t local = evl_clone(&global, S); /* samplers.hpp:448 */
@@ -1073,7 +1085,7 @@ so_run* so_run_chromatic(const so_model* m, const double* signals, const so_samp
         }
         const uint64_t id_base = next_base + (uint64_t)slot * (uint64_t)k;
         run->total_accepted += run_region_steps(run, &c, &local, signals, k, id_base, (int)want_tape,
-                                                epoch, color, slot, &flat, idxbuf);
+                                                epoch, color, slot, &flat, idxbuf, NULL);
         /* samplers.hpp:459-462: own events in local order */
         for (int64_t i = 0; i < local.n; ++i)
           if (region_contains(c.rlo, c.rhi, c.rclosed, local.e[i].t))
@@ -1131,6 +1143,117 @@ so_run* so_run_chromatic(const so_model* m, const double* signals, const so_samp
   flat_free(&flat);
   free(bnd);
   free(col);
+  return run;
+}
+
+
+/* run_naive_parallel, samplers.hpp:321-394: independent per-region chains
+ * from the empty hypothesis, no coloring, prior restricted to the region and
+ * the likelihood to the region's signal window; the trace is the union of
+ * the per-region checkpoints (every record_every local steps). */
+so_run* so_run_naive(const so_model* m, const double* signals, const so_sampler* sc,
+                     int64_t want_tape, int64_t want_rowlj) {
+  struct so_run* run = (struct so_run*)calloc(1, sizeof(struct so_run));
+  const int64_t S = m->n_stations;
+  run->S = S;
+  int rc = so_validate_model(m);
+  if (rc) {
+    run->status = rc;
+    return run;
+  }
+  if (sc->steps_per_epoch < 1 || sc->epochs < 1 || sc->n_regions < 1 || sc->record_every < 1 ||
+      sc->burn_in_fraction < 0 || sc->burn_in_fraction >= 1) {
+    run->status = fail(SO_EINVAL, "SamplerConfig: invalid");
+    return run;
+  }
+  const double tau = m->x_max / m->v;
+  const double l = m->T / (double)sc->n_regions;
+  const int64_t bcap = sc->n_regions + 8;
+  double* bnd = (double*)malloc(sizeof(double) * (size_t)bcap);
+  int64_t nreg = 0;
+  /* build_partition only (no color_partition), samplers.hpp:326-327 */
+  {
+    int64_t nb = 0;
+    if (!(l > 0) || l > m->T) {
+      run->status = fail(SO_EINVAL, "build_partition: need 0 < l <= T");
+      free(bnd);
+      return run;
+    }
+    bnd[nb++] = 0.0;
+    double b = l;
+    while (b < m->T - 1e-9) {
+      bnd[nb++] = b;
+      b += l;
+    }
+    bnd[nb++] = m->T;
+    nreg = nb - 1;
+  }
+  const int64_t spr = sc->epochs * sc->steps_per_epoch;
+  const int64_t n_cp = (spr + sc->record_every - 1) / sc->record_every + 1;
+  evlist_t* cps = (evlist_t*)calloc((size_t)(nreg * n_cp), sizeof(evlist_t));
+  int64_t* cp_steps = (int64_t*)calloc((size_t)n_cp, sizeof(int64_t));
+  flat_t flat = {0, 0, 0, 0, 0};
+  int64_t idxcap = spr + 16;
+  int64_t* idxbuf = (int64_t*)malloc(sizeof(int64_t) * (size_t)idxcap);
+  for (int64_t r = 0; r < nreg; ++r) {
+    chain_t c;
+    memset(&c, 0, sizeof c);
+    c.m = m;
+    c.sc = sc;
+    c.rlo = bnd[r];
+    c.rhi = bnd[r + 1];
+    c.rclosed = (r + 1 == nreg);
+    c.sweep = 0;
+    c.region = (uint32_t)r;
+    so_signal_window(c.rlo, c.rhi, tau, m->T, m->sample_rate, &c.wlo, &c.whi);
+    c.slo = c.rlo;
+    c.shi = c.rhi;
+    c.sclosed = c.rclosed;
+    if (sc->rng_mode == 0) c.rng = so_derive_stream(sc->seed, 5, 0, 0, (uint64_t)r);
+    uint64_t id_base = ((uint64_t)r + 1) << 32;
+    evlist_t local = {0, 0, 0};
+    cps[r * n_cp + 0] = evl_clone(&local, S);
+    int64_t done = 0, ci = 0;
+    while (done < spr) {
+      const int64_t chunk = sc->record_every < spr - done ? sc->record_every : spr - done;
+      c.step_base = (uint32_t)done;
+      int64_t births = 0;
+      run->total_accepted += run_region_steps(run, &c, &local, signals, chunk, id_base,
+                                              (int)want_tape, 0, 0, r, &flat, idxbuf, &births);
+      id_base += (uint64_t)births;
+      done += chunk;
+      ++ci;
+      cps[r * n_cp + ci] = evl_clone(&local, S);
+      cp_steps[ci] = done;
+    }
+    evl_free(&local);
+  }
+  /* union trace rows, samplers.hpp:366-392 */
+  for (int64_t ci = 0; ci < n_cp; ++ci) {
+    evlist_t merged = {0, 0, 0};
+    for (int64_t r = 0; r < nreg; ++r)
+      for (int64_t i = 0; i < cps[r * n_cp + ci].n; ++i)
+        evl_push(&merged, ev_copy(&cps[r * n_cp + ci].e[i], S));
+    qsort(merged.e, (size_t)merged.n, sizeof(ev_t), cmp_id);
+    double lj = 0.0;
+    if (want_rowlj) {
+      flat_fill(&flat, &merged, S);
+      lj = so_log_joint(m, signals, merged.n, flat.ids, flat.x, flat.t, flat.arr);
+    }
+    run_push_row(run, cp_steps[ci] * nreg, lj, merged.n);
+    if (ci + 1 == n_cp) {
+      run->final = merged;
+    } else {
+      evl_free(&merged);
+    }
+  }
+  for (int64_t i = 0; i < nreg * n_cp; ++i) evl_free(&cps[i]);
+  free(cps);
+  free(cp_steps);
+  free(idxbuf);
+  flat_free(&flat);
+  free(bnd);
+  run->total_steps = spr * nreg;
   return run;
 }
 

@@ -328,6 +328,8 @@ __device__ void gen_proposal(const Dev& d, const Samp& sp, const PhaseArgs& pa, 
   }
   if (P.skip) return;
   P.scored = 1;
+  // support: [0, T] closed in chromatic mode, the region in naive mode
+  // (density.hpp:218-221); naive support == the constraint already checked
   for (int a = 0; a < P.na; ++a) {
     const double t = P.at[a], x = P.ax[a];
     if (x < 0.0 || x > d.x_max || !(t >= 0.0 && t <= d.T)) P.skip = 1;
@@ -359,12 +361,18 @@ __global__ void __launch_bounds__(NTT, MINB)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int slot_idx = blockIdx.x;
-  const int region = pa.color + slot_idx * sp.ncol;
+  const int region = pa.naive ? slot_idx : pa.color + slot_idx * sp.ncol;
   if (region >= pa.nreg) return;
   const double rlo = pa.bnd[region], rhi = pa.bnd[region + 1];
   const bool rclosed = region + 1 == pa.nreg;
   const int N = ctl->n_events;
   const double log_len = log(rhi - rlo);  // std::log(region.length()), proposals.hpp:102
+  // prior constants: area T in chromatic mode (samplers.hpp:410), the region
+  // in naive mode (samplers.hpp:347); likelihood window likewise
+  const double llam = pa.naive ? pa.reg_llam[region] : d.log_lambda_T;
+  const double lxa_r = pa.naive ? pa.reg_lxa[region] : d.lxa;
+  const int win_lo = pa.naive ? pa.reg_wlo[region] : 0;
+  const int win_hi = pa.naive ? pa.reg_whi[region] : d.n;
 
   for (int i = tid; i < TBL * 4 + 4; i += NTT)
     Ts[i] = i < TBL * 4 && i < d.tab_n * 4 ? d.Dg[i] : make_double2(0, 0);
@@ -430,7 +438,9 @@ __global__ void __launch_bounds__(NTT, MINB)
   long long n_local = N;
   unsigned long long births = 0, n_acc = 0, n_scored = 0, n_arr = 0, n_changed = 0;
   unsigned long long n_spec = 0;
-  const unsigned long long id_base = pa.next_base + (unsigned long long)slot_idx * sp.k;
+  const unsigned long long id_base =
+      pa.naive ? ((unsigned long long)region + 1ull) << 32  // samplers.hpp:349
+               : pa.next_base + (unsigned long long)slot_idx * sp.k;
   if (tid == 0) {
     s_np = 0;
     s_births = 0;
@@ -456,10 +466,10 @@ __global__ void __launch_bounds__(NTT, MINB)
       const double lb = (wb >= 0 && wb < LOGIWIN) ? s_logi_n[wb] : d.logi[n0 + 1];
       const double ld = (wd >= 0 && wd < LOGIWIN) ? s_logi_n[wd] : d.logi[n0];
       double pb = 0.0, pdth = 0.0;
-      pb += d.log_lambda_T - lb;
-      pb += 1.0 * d.lxa;
-      pdth -= d.log_lambda_T - ld;
-      pdth += -1.0 * d.lxa;
+      pb += llam - lb;
+      pb += 1.0 * lxa_r;
+      pdth -= llam - ld;
+      pdth += -1.0 * lxa_r;
       s_prior[0] = pb;
       s_prior[1] = pdth;
     }
@@ -503,8 +513,8 @@ __global__ void __launch_bounds__(NTT, MINB)
             in.sweep = (uint32_t)pa.epoch;
             in.region = (uint32_t)region;
             in.step = (uint32_t)(i0 + q);
-            in.wlo = 0;
-            in.whi = d.n;
+            in.wlo = win_lo;
+            in.whi = win_hi;
             double sig = 0.0, arr = 0.0;
             int cnt = 0;
             score_item<MODE, YT>(d, P, in, tile, np_now, pold, pnew, Ts, sig, arr, cnt);
@@ -558,8 +568,8 @@ __global__ void __launch_bounds__(NTT, MINB)
           in.sweep = (uint32_t)pa.epoch;
           in.region = (uint32_t)region;
           in.step = (uint32_t)(i0 + q);
-          in.wlo = 0;
-          in.whi = d.n;
+          in.wlo = win_lo;
+          in.whi = win_hi;
           score_item<MODE, YT>(d, P, in, tile, np_now, pold, pnew, Ts, sig, arr, cnt);
         }
         if (cur_q >= 0) {
@@ -613,11 +623,11 @@ __global__ void __launch_bounds__(NTT, MINB)
           delta = s_prior[1];
         } else if (n1 != n0) {
           if (n1 > n0) {
-            for (long long i = n0 + 1; i <= n1; ++i) delta += d.log_lambda_T - d.logi[i];
+            for (long long i = n0 + 1; i <= n1; ++i) delta += llam - d.logi[i];
           } else {
-            for (long long i = n1 + 1; i <= n0; ++i) delta -= d.log_lambda_T - d.logi[i];
+            for (long long i = n1 + 1; i <= n0; ++i) delta -= llam - d.logi[i];
           }
-          delta += (double)(n1 - n0) * d.lxa;
+          delta += (double)(n1 - n0) * lxa_r;
         }
         delta += A;
         delta += sig;
@@ -659,7 +669,7 @@ __global__ void __launch_bounds__(NTT, MINB)
         if (P.skip) {
           // null (no draw), constrained out, or out of support: log_r = -inf
           // -> reject (proposals.hpp:268-291)
-          if (MODE == 1) {
+          if (pa.out) {
             seis_step_out o;
             o.delta = -INFINITY;
             o.log_r = -INFINITY;
@@ -674,15 +684,15 @@ __global__ void __launch_bounds__(NTT, MINB)
         const double delta = s_delta[q], log_r = s_logr[q];
         const bool acc_gpu = s_accg[q] != 0;
         bool apply = acc_gpu;
-        if (MODE == 1) {
+        if (pa.out) {  // replay, or a production run asked for its decisions
           seis_step_out o;
           o.delta = delta;
           o.log_r = log_r;
           o.scored = 1;
           o.accepted = acc_gpu ? 1 : 0;
           pa.out[P.tape_idx] = o;
-          apply = P.tape_acc != 0;  // keep the state on the tape's trajectory
         }
+        if (MODE == 1) apply = P.tape_acc != 0;  // keep the state on the tape's trajectory
         P.accept = 0;
         if (!apply) continue;
         // allocate destination slots; modify this-phase versions in place
@@ -771,6 +781,18 @@ __global__ void __launch_bounds__(NTT, MINB)
         break;
       }
       n_spec += (unsigned long long)(m - adv);
+      if (pa.naive && pa.record_every > 0) {
+        // checkpoints at local steps c * record_every (and the end) inside
+        // (i0, i0 + adv]: every step before the round's accept was rejected
+        const int hi_step = i0 + adv;
+        int c = i0 / pa.record_every + 1;
+        for (int cb = c * pa.record_every; ; cb += pa.record_every, ++c) {
+          const int at = cb < (int)sp.k ? cb : (int)sp.k;
+          if (at > hi_step) break;
+          pa.cp_counts[(size_t)c * pa.nreg + region] = at == hi_step ? nown : s_nown;
+          if (at == (int)sp.k) break;
+        }
+      }
       s_adv = adv;
       s_accq = accq;
       s_nown = nown;
@@ -2035,6 +2057,9 @@ extern "C" int seis_run_chromatic(seis_engine* e, const seis_sampler_cfg* sc, in
         ck(cudaMemcpyAsync(d_tarr, tape_arr, (size_t)n_tape_arr * 8, cudaMemcpyHostToDevice,
                            e->stream),
            "H2D tape arrivals");
+    } else if (step_out) {  // production run recording its per-step decisions
+      if (n_tape < 1) throw std::invalid_argument("step_out needs n_tape >= 1 entries");
+      d_out = static_cast<seis_step_out*>(alloc((size_t)n_tape * sizeof(seis_step_out)));
     }
     const int64_t rcap = std::max<int64_t>(row_cap, 1);
     double* lj_dev = static_cast<double*>(alloc((size_t)rcap * 8));
@@ -2123,8 +2148,9 @@ extern "C" int seis_run_chromatic(seis_engine* e, const seis_sampler_cfg* sc, in
           pa.tape_arr = d_tarr;
           pa.out = d_out;
           const int stamp = ++e->stamp;
-          if (mode == 1 && tape_base + (long long)ncr * k > n_tape)
-            throw std::invalid_argument("replay tape shorter than the run");
+          if ((mode == 1 || d_out) && tape_base + (long long)ncr * k > n_tape)
+            throw std::invalid_argument(mode == 1 ? "replay tape shorter than the run"
+                                                  : "step_out shorter than the run");
           cudaEvent_t a = nullptr, b = nullptr;
           if (timing) {
             ck(cudaEventCreate(&a), "event");
@@ -2180,8 +2206,9 @@ extern "C" int seis_run_chromatic(seis_engine* e, const seis_sampler_cfg* sc, in
         if (row_count) row_count[i] = cn[i];
       }
     }
-    if (mode == 1)
-      ck(cudaMemcpy(step_out, d_out, (size_t)n_tape * sizeof(seis_step_out),
+    if (d_out)
+      ck(cudaMemcpy(step_out, d_out, (size_t)std::min<long long>(n_tape, tape_base) *
+                                         sizeof(seis_step_out),
                     cudaMemcpyDeviceToHost),
          "D2H out");
     if (getenv("SEIS_PROF"))
@@ -2216,6 +2243,215 @@ extern "C" int seis_run_chromatic(seis_engine* e, const seis_sampler_cfg* sc, in
     }
   });
   for (auto ev : evs) cudaEventDestroy(ev);
+  for (void* p : tmp) cudaFree(p);
+  return rc;
+}
+
+// run_naive_parallel (samplers.hpp:321-394): independent per-region chains
+// from the empty hypothesis, no coloring, region prior support and signal
+// window; one launch runs every region's whole chain. The final hypothesis
+// (the union) is committed to the engine; trace rows carry the union's event
+// count at every checkpoint and log_joint at the last row only.
+extern "C" int seis_run_naive(seis_engine* e, const seis_sampler_cfg* sc, int32_t mode,
+                              const seis_tape_step* tape, int64_t n_tape, const double* tape_arr,
+                              int64_t n_tape_arr, seis_step_out* step_out, int64_t row_cap,
+                              int64_t* row_step, double* row_log_joint, int64_t* row_count,
+                              seis_run_stats* stats) {
+  std::vector<void*> tmp;
+  auto alloc = [&](size_t bytes) {
+    void* p = nullptr;
+    ck(cudaMalloc(&p, bytes ? bytes : 1), "cudaMalloc");
+    tmp.push_back(p);
+    return p;
+  };
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, evp0 = nullptr, evp1 = nullptr;
+  const int rc = guarded([&] {
+    if (sc->steps_per_epoch < 1 || sc->epochs < 1 || sc->n_regions < 1 || sc->record_every < 1 ||
+        sc->burn_in_fraction < 0 || sc->burn_in_fraction >= 1)
+      throw std::invalid_argument("SamplerConfig: invalid");
+    double wsum = 0.0;
+    for (double w : sc->weights) {
+      if (w < 0) throw std::invalid_argument("MoveDistribution: negative weight");
+      wsum += w;
+    }
+    if (std::abs(wsum - 1.0) > 1e-12)
+      throw std::invalid_argument("MoveDistribution: weights must sum to 1");
+    if (mode != 0 && mode != 1) throw std::invalid_argument("mode must be 0 or 1");
+    if (mode == 1 && (!tape || !step_out)) throw std::invalid_argument("replay needs a tape");
+    if (read_ctl(e).n_events != 0)
+      throw std::invalid_argument("the naive sampler starts from the empty hypothesis");
+    const double tau = e->cfg.x_max / e->cfg.v;
+    const double l = e->cfg.T / (double)sc->n_regions;
+    if (!(l > 0) || l > e->cfg.T) throw std::invalid_argument("build_partition: need 0 < l <= T");
+    const int bcap = (int)sc->n_regions + 4;
+    double* bnd = static_cast<double*>(alloc((size_t)bcap * 8));
+    int* nreg_d = static_cast<int*>(alloc(4));
+    int* perr = static_cast<int*>(alloc(4));
+    ck(cudaMemsetAsync(perr, 0, 4, e->stream), "memset");
+    // build_partition only: no coloring, no separation check (tau = -inf)
+    k_partition<<<1, 1, 0, e->stream>>>(e->cfg.T, l, -INFINITY, 1, 0, 0, 0, 1, 0.0, bcap, bnd,
+                                         nreg_d, perr, nullptr);
+    int nreg = 0, herr = 0;
+    ck(cudaMemcpyAsync(&nreg, nreg_d, 4, cudaMemcpyDeviceToHost, e->stream), "D2H");
+    ck(cudaMemcpyAsync(&herr, perr, 4, cudaMemcpyDeviceToHost, e->stream), "D2H");
+    ck(cudaStreamSynchronize(e->stream), "sync");
+    if (herr) throw std::runtime_error("partition capacity");
+    std::vector<double> hb(nreg + 1);
+    ck(cudaMemcpy(hb.data(), bnd, (size_t)(nreg + 1) * 8, cudaMemcpyDeviceToHost), "D2H");
+    // per-region prior constants (glibc log, density.hpp:225-237) and
+    // signal windows (partition.hpp:94-102)
+    std::vector<double> llam(nreg), lxa(nreg);
+    std::vector<int> wlo(nreg), whi(nreg);
+    for (int r = 0; r < nreg; ++r) {
+      const double area = hb[r + 1] - hb[r];
+      llam[r] = std::log(e->cfg.lambda_rate * area);
+      lxa[r] = -std::log(e->cfg.x_max) - std::log(area);
+      const double h = std::min(hb[r + 1] + tau, e->cfg.T);
+      wlo[r] = (int)std::max<int64_t>(0, (int64_t)std::ceil(hb[r] * e->cfg.sample_rate - 1e-9));
+      whi[r] = (int)std::min<int64_t>(e->n, (int64_t)std::ceil(h * e->cfg.sample_rate - 1e-9));
+    }
+    double* d_llam = static_cast<double*>(alloc((size_t)nreg * 8));
+    double* d_lxa = static_cast<double*>(alloc((size_t)nreg * 8));
+    int* d_wlo = static_cast<int*>(alloc((size_t)nreg * 4));
+    int* d_whi = static_cast<int*>(alloc((size_t)nreg * 4));
+    ck(cudaMemcpy(d_llam, llam.data(), (size_t)nreg * 8, cudaMemcpyHostToDevice), "H2D");
+    ck(cudaMemcpy(d_lxa, lxa.data(), (size_t)nreg * 8, cudaMemcpyHostToDevice), "H2D");
+    ck(cudaMemcpy(d_wlo, wlo.data(), (size_t)nreg * 4, cudaMemcpyHostToDevice), "H2D");
+    ck(cudaMemcpy(d_whi, whi.data(), (size_t)nreg * 4, cudaMemcpyHostToDevice), "H2D");
+    const int64_t spr = sc->epochs * sc->steps_per_epoch;
+    if (spr > INT32_MAX) throw std::invalid_argument("too many steps per region");
+    const int64_t re = std::min<int64_t>(sc->record_every, spr);
+    const int64_t n_cp = (spr + re - 1) / re + 1;
+    int* cp = static_cast<int*>(alloc((size_t)n_cp * nreg * 4));
+    ck(cudaMemsetAsync(cp, 0, (size_t)n_cp * nreg * 4, e->stream), "memset");
+    Samp sp{};
+    sp.k = spr;
+    sp.seed = sc->seed;
+    double cum = 0.0;
+    for (int q = 0; q < 5; ++q) {
+      cum += sc->weights[q];
+      sp.cumw[q] = cum;
+      sp.logw[q] = std::log(sc->weights[q]);
+    }
+    sp.step_lx = sc->step_location_x;
+    sp.step_lt = sc->step_location_t;
+    sp.step_arr = sc->step_arrival;
+    sp.step_joint = sc->step_joint;
+    sp.joint_t_sd = sc->step_joint / e->cfg.v;
+    sp.ncol = 1;
+    int* births_cnt = static_cast<int*>(alloc((size_t)nreg * 4));
+    OutEv* births = static_cast<OutEv*>(alloc((size_t)nreg * MAXOWN * sizeof(OutEv)));
+    int* diff_cnt = static_cast<int*>(alloc((size_t)nreg * 4));
+    DiffPair* diff = static_cast<DiffPair*>(alloc((size_t)nreg * MAXDOUT * sizeof(DiffPair)));
+    seis_tape_step* d_tape = nullptr;
+    double* d_tarr = nullptr;
+    seis_step_out* d_out = nullptr;
+    if (mode == 1) {
+      if (n_tape != spr * nreg) throw std::invalid_argument("replay tape length != steps x regions");
+      d_tape = static_cast<seis_tape_step*>(alloc((size_t)n_tape * sizeof(seis_tape_step)));
+      d_tarr = static_cast<double*>(alloc((size_t)std::max<int64_t>(n_tape_arr, 1) * 8));
+      d_out = static_cast<seis_step_out*>(alloc((size_t)n_tape * sizeof(seis_step_out)));
+      ck(cudaMemcpy(d_tape, tape, (size_t)n_tape * sizeof(seis_tape_step), cudaMemcpyHostToDevice),
+         "H2D tape");
+      if (n_tape_arr)
+        ck(cudaMemcpy(d_tarr, tape_arr, (size_t)n_tape_arr * 8, cudaMemcpyHostToDevice), "H2D");
+    } else if (step_out) {  // production run recording its per-step decisions
+      if (n_tape < spr * nreg) throw std::invalid_argument("step_out shorter than the run");
+      d_out = static_cast<seis_step_out*>(alloc((size_t)spr * nreg * sizeof(seis_step_out)));
+    }
+    k_reset_counters<<<1, 1, 0, e->stream>>>(e->ctl);
+    PhaseArgs pa{};
+    pa.epoch = 0;
+    pa.color = 0;
+    pa.nreg = nreg;
+    pa.n_slots = nreg;
+    pa.bnd = bnd;
+    pa.next_base = 0;  // every event of a naive region is born in the run
+    pa.tape_base = 0;
+    pa.tab = e->tab[e->cur];
+    pa.fate_stamp = e->fate_stamp;
+    pa.fate_alive = e->fate_alive;
+    pa.fate_x = e->fate_x;
+    pa.fate_t = e->fate_t;
+    pa.fate_slot = e->fate_slot;
+    pa.births_cnt = births_cnt;
+    pa.births = births;
+    pa.diff_cnt = diff_cnt;
+    pa.diff = diff;
+    pa.free_stack = e->free_stack;
+    pa.tape = d_tape;
+    pa.tape_arr = d_tarr;
+    pa.out = d_out;
+    pa.naive = 1;
+    pa.reg_llam = d_llam;
+    pa.reg_lxa = d_lxa;
+    pa.reg_wlo = d_wlo;
+    pa.reg_whi = d_whi;
+    pa.record_every = (int)re;
+    pa.cp_counts = cp;
+    const int stamp = ++e->stamp;
+    ck(cudaEventCreate(&ev0), "event");
+    ck(cudaEventCreate(&ev1), "event");
+    ck(cudaEventCreate(&evp0), "event");
+    ck(cudaEventCreate(&evp1), "event");
+    ck(cudaEventRecord(ev0, e->stream), "event");
+    ck(cudaEventRecord(evp0, e->stream), "event");
+    launch_phase(e, mode, nreg, sp, pa, stamp);
+    ck(cudaEventRecord(evp1, e->stream), "event");
+    ck(cudaGetLastError(), "k_phase (naive)");
+    // the union: coverage of every region's events, table of all births
+    k_commit<<<nreg, 256, 0, e->stream>>>(e->d, 0, 1, nreg, diff_cnt, diff, e->free_stack,
+                                          e->ctl);
+    const int nxt = e->cur ^ 1;
+    k_rebuild<<<1, 1024, 0, e->stream>>>(e->tab[e->cur], e->tab[nxt], e->cap, stamp,
+                                          e->fate_stamp, e->fate_alive, e->fate_x, e->fate_t,
+                                          e->fate_slot, nreg, births_cnt, births, e->ctl);
+    ck(cudaGetLastError(), "naive commit");
+    e->cur = nxt;
+    double* lj_dev = static_cast<double*>(alloc(8));
+    double* lj_scratch = static_cast<double*>(alloc((2 * 296 + 1) * 8));
+    if (sc->record_log_joint) launch_lj_any(e, lj_dev, lj_scratch);
+    ck(cudaEventRecord(ev1, e->stream), "event");
+    ck(cudaStreamSynchronize(e->stream), "run");
+    const Ctl c = read_ctl(e);
+    if (c.err) throw std::runtime_error(std::string("device: ") + err_name(c.err));
+    std::vector<int> hcp((size_t)n_cp * nreg);
+    ck(cudaMemcpy(hcp.data(), cp, hcp.size() * 4, cudaMemcpyDeviceToHost), "D2H");
+    double lj_last = 0.0;
+    if (sc->record_log_joint) ck(cudaMemcpy(&lj_last, lj_dev, 8, cudaMemcpyDeviceToHost), "D2H");
+    for (int64_t ci = 0; ci < n_cp && ci < row_cap; ++ci) {
+      int64_t cnt = 0;
+      for (int r = 0; r < nreg; ++r) cnt += hcp[(size_t)ci * nreg + r];
+      if (row_step) row_step[ci] = std::min<int64_t>(ci * re, spr) * nreg;
+      if (row_count) row_count[ci] = cnt;
+      if (row_log_joint) row_log_joint[ci] = (ci + 1 == n_cp) ? lj_last : 0.0;
+    }
+    if (d_out)
+      ck(cudaMemcpy(step_out, d_out, (size_t)spr * nreg * sizeof(seis_step_out),
+                    cudaMemcpyDeviceToHost),
+         "D2H out");
+    if (stats) {
+      std::memset(stats, 0, sizeof *stats);
+      stats->total_steps = spr * nreg;
+      stats->total_accepted = (int64_t)c.accepted;
+      stats->scored_proposals = (int64_t)c.scored;
+      stats->changed_samples = (int64_t)c.changed;
+      stats->arrival_values = (int64_t)c.arrvals;
+      const double by = e->dtype == SEIS_F64 ? 8.0 : 4.0;
+      stats->algorithmic_bytes = (double)c.changed * (by + 2.0) + 8.0 * (double)c.arrvals;
+      float ms = 0.f;
+      ck(cudaEventElapsedTime(&ms, evp0, evp1), "elapsed");
+      stats->sweep_kernel_ms = ms;
+      ck(cudaEventElapsedTime(&ms, ev0, ev1), "elapsed");
+      stats->total_ms = ms;
+      stats->kernel_launches = 3 + (sc->record_log_joint ? 3 : 0);
+      stats->n_rows = n_cp;
+      stats->final_events = c.n_events;
+      stats->speculative_discarded = (int64_t)c.speculative;
+    }
+  });
+  for (cudaEvent_t ev : {ev0, ev1, evp0, evp1})
+    if (ev) cudaEventDestroy(ev);
   for (void* p : tmp) cudaFree(p);
   return rc;
 }

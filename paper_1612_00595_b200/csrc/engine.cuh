@@ -121,6 +121,15 @@ struct PhaseArgs {
   const seis_tape_step* tape;
   const double* tape_arr;
   seis_step_out* out;
+  // naive mode (run_naive_parallel, samplers.hpp:321-394): all regions in one
+  // launch from the empty hypothesis; per-region prior support and window
+  int naive;
+  const double* reg_llam;          // log(lambda * region length)
+  const double* reg_lxa;           // -log(x_max) - log(region length)
+  const int* reg_wlo;              // signal_window (partition.hpp:94-102)
+  const int* reg_whi;
+  int record_every;                // checkpoints every record_every local steps
+  int* cp_counts;                  // [n_cp][nreg] own event count at checkpoint c
 };
 
 enum : int {

@@ -516,8 +516,8 @@ __device__ __forceinline__ void station_item(const Dev& d, const Prop& P, const 
 // Arrival move (proposals.hpp:161-174) in production: only station st moves;
 // the warp's lanes take rows.
 template <typename YT>
-__device__ __forceinline__ void arrival_item(const Dev& d, const Prop& P, int np,
-                                             const int* pold, const int* pnew,
+__device__ __forceinline__ void arrival_item(const Dev& d, const Prop& P, const PassIn& in,
+                                             int np, const int* pold, const int* pnew,
                                              const double2* Ts, double& sig, double& arr,
                                              int& cnt) {
   const int lane = threadIdx.x & 31;
@@ -526,7 +526,9 @@ __device__ __forceinline__ void arrival_item(const Dev& d, const Prop& P, int np
   const double new_a = old_a + P.arr_da;
   const double mean = arrival_mean(d, P.rx[0], P.rt[0], d.stations[st]);
   if (lane == 0) arr += arr_logpdf(d, new_a, mean) - arr_logpdf(d, old_a, mean);
-  const Win wo = make_win(d, old_a), wn = make_win(d, new_a);
+  // likelihood window: [0, n) chromatic, signal_window naive (density.hpp:244-262)
+  const Win wo = clampw(make_win(d, old_a), in.wlo, in.whi);
+  const Win wn = clampw(make_win(d, new_a), in.wlo, in.whi);
   if (weq(wo, wn)) return;
   const int blo = min(wo.hi > wo.lo ? wo.lo : INT_MAX, wn.hi > wn.lo ? wn.lo : INT_MAX);
   const int bhi = max(wo.hi > wo.lo ? wo.hi : INT_MIN, wn.hi > wn.lo ? wn.hi : INT_MIN);
@@ -554,7 +556,7 @@ __device__ __forceinline__ void score_item(const Dev& d, const Prop& P, const Pa
   if (P.skip) return;
   const int j = tile * 32 + (threadIdx.x & 31);
   if (MODE == 0 && P.type == 3) {
-    if (tile == 0) arrival_item<YT>(d, P, np, pold, pnew, Ts, sig, arr, cnt);
+    if (tile == 0) arrival_item<YT>(d, P, in, np, pold, pnew, Ts, sig, arr, cnt);
     return;
   }
   const int shape = P.nr * 3 + P.na;

@@ -66,7 +66,8 @@ EXPORTS = ("seis_last_error", "seis_engine_create", "seis_engine_destroy", "seis
            "seis_set_hypothesis", "seis_get_hypothesis", "seis_partition", "seis_assign_regions",
            "seis_partition_offset", "seis_score_batch", "seis_log_joint", "seis_run_chromatic",
            "seis_world_last_error", "seis_world_generate", "seis_world_with_events",
-           "seis_thomas_events", "seis_set_snapshot_capacity", "seis_get_snapshots")
+           "seis_thomas_events", "seis_set_snapshot_capacity", "seis_get_snapshots",
+           "seis_run_naive")
 
 _LIB = None
 
@@ -94,6 +95,7 @@ def load_library(path: str | None = None) -> C.CDLL:
     L.seis_score_batch.argtypes = [P, i64, P, P, i64, P]
     L.seis_log_joint.argtypes = [P, P]
     L.seis_run_chromatic.argtypes = [P, P, i32, P, i64, P, i64, P, i64, P, P, P, P]
+    L.seis_run_naive.argtypes = [P, P, i32, P, i64, P, i64, P, i64, P, P, P, P]
     L.seis_world_generate.argtypes = [P, P, i64, u64, i64, P, P, P, P, P, P, i32, i32]
     L.seis_world_with_events.argtypes = [P, P, i64, i64, P, P, u64, P, P, i32, i32]
     L.seis_thomas_events.argtypes = [u64, f64, f64, f64, f64, f64, f64, i64, P, P, P]
@@ -163,9 +165,9 @@ class SamplerConfig:
     record_log_joint: bool = False
 
     def _c(self):
-        if self.algorithm not in ("chromatic-static", "chromatic-dynamic"):
+        if self.algorithm not in ("chromatic-static", "chromatic-dynamic", "naive"):
             raise ValueError(f"unknown sampler '{self.algorithm}' (this engine runs "
-                             "chromatic-static or chromatic-dynamic)")
+                             "chromatic-static, chromatic-dynamic or naive)")
         return _SamplerC(self.steps_per_epoch, self.epochs, self.n_regions, self.seed,
                          self.burn_in_fraction, self.record_every, (f64 * 5)(*self.weights),
                          self.step_location_x, self.step_location_t, self.step_arrival,
@@ -457,12 +459,16 @@ class Engine:
 
     def run_chromatic(self, sc: SamplerConfig, tape: np.ndarray | None = None,
                       tape_arrivals: np.ndarray | None = None, row_cap: int = 1 << 16,
-                      final: bool = True) -> Trace:
-        """run_chromatic (samplers.hpp:401-498) from the resident hypothesis.
+                      final: bool = True, decisions: int = 0) -> Trace:
+        """run_chromatic (samplers.hpp:401-498) from the resident hypothesis, or
+        run_naive_parallel (samplers.hpp:321-394) when sc.algorithm == "naive"
+        (from the empty hypothesis).
 
         Without `tape`: production mode (philox stream spec v1). With `tape`
         (oracle TAPE_DTYPE records in driver order): replay mode, returning the
         engine's per-step delta / log_r / decision in Trace.step_out.
+        `decisions` > 0 (production only): capacity for the run's own per-step
+        decisions, returned in Trace.step_out (driver order).
         """
         s = sc._c()
         mode = 0
@@ -476,15 +482,21 @@ class Engine:
             tarr = np.ascontiguousarray(tape_arrivals if tape_arrivals is not None
                                         else np.zeros(1), np.float64)
             out = np.zeros(n_tape, STEP_OUT_DTYPE)
+        elif decisions > 0:
+            n_tape = int(decisions)
+            out = np.zeros(n_tape, STEP_OUT_DTYPE)
         rs = np.zeros(row_cap, np.int64)
         rl = np.zeros(row_cap)
         rc = np.zeros(row_cap, np.int64)
         st = _StatsC()
-        _check(self.L.seis_run_chromatic(self.h, C.byref(s), mode, _p(tape), n_tape, _p(tarr),
-                                         0 if tarr is None else len(tarr), _p(out), row_cap,
-                                         _p(rs), _p(rl), _p(rc), C.byref(st)), self.L)
+        fn = self.L.seis_run_naive if sc.algorithm == "naive" else self.L.seis_run_chromatic
+        _check(fn(self.h, C.byref(s), mode, _p(tape), n_tape, _p(tarr),
+                  0 if tarr is None else len(tarr), _p(out), row_cap, _p(rs), _p(rl), _p(rc),
+                  C.byref(st)), self.L)
         nr = min(st.n_rows, row_cap)
         stats = {f: getattr(st, f) for f, _ in _StatsC._fields_}
+        if out is not None and mode == 0:
+            out = out[:st.total_steps]
         tr = Trace(rs[:nr], rl[:nr], rc[:nr], st.total_steps, st.total_accepted, stats,
                    step_out=out)
         if final:
@@ -495,8 +507,9 @@ class Engine:
 
 def run_sampler(config: ModelConfig, signals: np.ndarray, sc: SamplerConfig,
                 event_capacity: int = 4096) -> Trace:
-    """reference run_sampler (samplers.hpp:500-509) for the chromatic algorithms:
-    from the empty hypothesis, through the C-ABI with host buffers."""
+    """reference run_sampler (samplers.hpp:500-509) for the chromatic and
+    naive algorithms: from the empty hypothesis, through the C-ABI with host
+    buffers."""
     eng = Engine(config, signals, event_capacity)
     try:
         return eng.run_chromatic(sc)

@@ -151,6 +151,16 @@ def main():
             pr, rc, le, nm = R.match_events(w.events, r["final"])
             post.append((300 + ws, rs, pr, rc, le, r["final"].N, w.events.N,
                          r["total_accepted"]))
+    # naive-parallel comparison (samplers.hpp:321-394) on the same worlds
+    for ws in range(8):
+        w = R.sample_world(m, 300 + ws)
+        for rs in (1, 2, 3):
+            sc = O.Sampler(steps_per_epoch=500, epochs=40, n_regions=4, seed=rs,
+                           burn_in_fraction=0.0, record_every=1 << 30)
+            r = O.ref_run_sampler(w, sc, workers=1, naive=True)
+            pr, rc, le, nm = R.match_events(w.events, r["final"])
+            post.append((1000 + 300 + ws, rs, pr, rc, le, r["final"].N, w.events.N,
+                         r["total_accepted"]))
     np.savez_compressed(os.path.join(HERE, "posterior.npz"), rows=np.array(post, np.float64),
                         cols=np.array(["world_seed", "run_seed", "precision", "recall",
                                        "location_error", "n_final", "n_true", "accepted"]),

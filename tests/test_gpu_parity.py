@@ -202,12 +202,24 @@ def test_replay_fp32_mapped_world(E, oc):
 
 
 # ------------------------------------------------------------------ production
+def _decisions_match(so, t, rtol):
+    """per-step production decisions (driver order) vs the oracle's tape"""
+    assert len(so) == len(t)
+    assert np.array_equal(so["accepted"], t["accepted"])
+    assert np.array_equal(so["scored"] != 0, t["scored"] == 1)
+    sc = t["scored"] == 1
+    fin = sc & np.isfinite(t["delta"])
+    assert np.array_equal(np.isfinite(so["delta"][sc]), np.isfinite(t["delta"][sc]))
+    assert np.allclose(so["delta"][fin], t["delta"][fin], rtol=rtol, atol=1e-9)
+
+
 def _prod_vs_oracle(E, oc, m, w, s, init=None, dtype=np.float64, rowlj=False):
-    ro = oc.run_chromatic(w, s, init=init, tape=False, rowlj=rowlj)
+    ro = oc.run_chromatic(w, s, init=init, tape=True, rowlj=rowlj)
     eng = E.Engine(engine_model(m), w.signals.astype(dtype), event_capacity=2048)
     if init is not None:
         eng.set_hypothesis(E.Events(init.ids, init.x, init.t, init.arr))
-    tr = eng.run_chromatic(engine_sampler(s, record_log_joint=rowlj))
+    tr = eng.run_chromatic(engine_sampler(s, record_log_joint=rowlj), decisions=len(ro["tape"]))
+    _decisions_match(tr.step_out, ro["tape"], 1e-11 if dtype == np.float64 else 1e-5)
     assert tr.total_steps == ro["total_steps"]
     assert tr.total_accepted == ro["total_accepted"]
     assert np.array_equal(tr.final.ids, ro["final"].ids)
@@ -268,7 +280,7 @@ def test_posterior_statistics_within_seed_spread(E, oc):
     seeds); engine: production mode (philox stream) on the same worlds, 6
     seeds each."""
     g = golden("posterior.npz")
-    rows = g["rows"]
+    rows = g["rows"][g["rows"][:, 0] < 1000]
     k, ep, nr, dyn = [int(v) for v in g["sampler"]]
     m = default_model()
     stats = []
@@ -346,3 +358,74 @@ def test_trace_rows_and_snapshots(E, oc, tmp_path):
     lines = open(tmp_path / "samples.csv").read().splitlines()
     assert lines[0] == "snapshot_id,event_id,x,t"
     assert len(lines) == 1 + sum(len(sn.ids) for sn in tr.snapshots)
+
+
+
+# ------------------------------------------------------------------ naive mode
+def _naive_sampler(E, s):
+    return E.SamplerConfig(algorithm="naive", steps_per_epoch=s.steps_per_epoch,
+                           epochs=s.epochs, n_regions=s.n_regions, seed=s.seed,
+                           burn_in_fraction=s.burn_in_fraction, record_every=s.record_every,
+                           record_log_joint=True)
+
+
+@pytest.mark.parametrize("ws", [0, 2, 3])
+def test_naive_production_matches_oracle_philox(E, oc, ws):
+    m = default_model()
+    w = golden_world(f"w{ws}", m)
+    s = O.Sampler(steps_per_epoch=100, epochs=8, n_regions=4, seed=31 + ws, rng_mode=1,
+                  record_every=130, burn_in_fraction=0.0)
+    ro = oc.run_chromatic(w, s, tape=True, rowlj=True, naive=True)
+    eng = E.Engine(engine_model(m), w.signals)
+    tr = eng.run_chromatic(_naive_sampler(E, s), decisions=len(ro["tape"]))
+    _decisions_match(tr.step_out, ro["tape"], 1e-11)
+    assert tr.total_steps == ro["total_steps"]
+    assert tr.total_accepted == ro["total_accepted"]
+    assert np.array_equal(tr.final.ids, ro["final"].ids)
+    assert np.array_equal(tr.final.arrivals, ro["final"].arr)
+    assert np.array_equal(tr.row_step, ro["row_step"])
+    assert np.array_equal(tr.row_count, ro["row_count"])
+    assert close(tr.row_log_joint[-1], ro["row_lj"][-1], 1e-12)
+
+
+def test_naive_replay_reference_tape(E, oc):
+    m = _mapped_model(S=32, T=600.0, n_regions=12, x_max=400.0, lam_events=25)
+    w = oc.sample_world(m, 6)
+    s = O.Sampler(steps_per_epoch=50, epochs=4, n_regions=12, seed=2, record_every=1 << 30,
+                  burn_in_fraction=0.0)
+    r = oc.run_chromatic(w, s, tape=True, naive=True)
+    eng = E.Engine(engine_model(m), w.signals)
+    tr = eng.run_chromatic(_naive_sampler(E, s), tape=r["tape"], tape_arrivals=r["tape_arr"])
+    t = r["tape"]
+    drawn = t["u_drawn"] == 1
+    tie = np.zeros(len(t), bool)
+    tie[drawn] = np.abs(t["log_r"][drawn] - np.log(t["u"][drawn])) < TIE
+    assert not ((tr.step_out["accepted"] != t["accepted"]) & ~tie).any()
+    sc = t["scored"] == 1
+    assert np.allclose(tr.step_out["delta"][sc], t["delta"][sc], rtol=1e-11, atol=1e-9)
+    assert np.array_equal(tr.final.ids, r["final"].ids)
+    assert np.array_equal(tr.final.arrivals, r["final"].arr)
+
+
+def test_naive_posterior_within_seed_spread(E, oc):
+    g = golden("posterior.npz")
+    rows = g["rows"][g["rows"][:, 0] >= 1000]
+    k, ep, nr, _ = [int(v) for v in g["sampler"]]
+    m = default_model()
+    stats = []
+    for ws in sorted(set(int(v) % 1000 for v in rows[:, 0])):
+        w = oc.sample_world(m, ws)
+        eng = E.Engine(engine_model(m), w.signals)
+        for rs in range(11, 17):
+            eng.set_hypothesis(E.Events(np.zeros(0, np.uint64), np.zeros(0), np.zeros(0),
+                                        np.zeros((0, m.S))))
+            sc = E.SamplerConfig(algorithm="naive", steps_per_epoch=k, epochs=ep, n_regions=nr,
+                                 seed=rs, burn_in_fraction=0.0, record_every=1 << 30)
+            f = eng.run_chromatic(sc).final
+            stats.append(oc.match_events(w.events, O.Events(f.ids, f.x, f.t, f.arrivals))[:3])
+    gpu = np.array(stats)
+    ref = rows[:, 2:5]
+    for c, name in enumerate(["precision", "recall", "location_error"]):
+        a, b = gpu[:, c], ref[:, c]
+        se = np.sqrt(a.var(ddof=1) / len(a) + b.var(ddof=1) / len(b))
+        assert abs(a.mean() - b.mean()) <= 2.5 * se + 0.02, (name, a.mean(), b.mean(), se)

@@ -194,10 +194,28 @@ def test_posterior_statistics_match_reference(oc):
     m = default_model()
     for row in g["rows"][::5]:
         ws, rs = int(row[0]), int(row[1])
-        w = oc.sample_world(m, ws)
+        naive = ws >= 1000
+        w = oc.sample_world(m, ws % 1000)
         s = O.Sampler(steps_per_epoch=k, epochs=ep, n_regions=nr, seed=rs, dynamic=dyn,
                       burn_in_fraction=0.0, record_every=1 << 30)
-        r = oc.run_chromatic(w, s, tape=False)
+        r = oc.run_chromatic(w, s, tape=False, naive=naive)
         p, rc, le, _ = oc.match_events(w.events, r["final"])
         assert (p, rc, le) == (row[2], row[3], row[4])
         assert r["final"].N == row[5] and r["total_accepted"] == row[7]
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_naive_tape_matches_reference(oc, seed):
+    if not O.have_ref():
+        pytest.skip("reference tree absent")
+    R = O.Oracle("ref")
+    m = default_model()
+    w = oc.sample_world(m, 40 + seed)
+    s = O.Sampler(steps_per_epoch=100, epochs=5, n_regions=4, seed=seed, record_every=150,
+                  burn_in_fraction=0.0)
+    a = oc.run_chromatic(w, s, naive=True, rowlj=True)
+    b = R.run_chromatic(w, s, naive=True, rowlj=True)
+    assert a["tape"].tobytes() == b["tape"].tobytes()
+    assert np.array_equal(a["row_lj"], b["row_lj"]) and np.array_equal(a["row_count"], b["row_count"])
+    c = O.ref_run_sampler(w, s, naive=True)
+    assert np.array_equal(a["final"].arr, c["final"].arr)
