@@ -270,7 +270,7 @@ def main():
     threads = os.cpu_count() or 1
     m, ev, sig = make_world(c, threads)
     cap = int(max(1024, ev.N * 2 + 256))
-    eng = E.Engine(m, sig, event_capacity=min(cap, 65000))
+    eng = E.Engine(m, sig, event_capacity=cap)
     truth = E.Events(ev.ids, ev.x, ev.t, ev.arrivals)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     seed0 = 1000 * rank

@@ -123,10 +123,18 @@ typedef struct {
 
 const char* seis_last_error(void);
 
+/* event_capacity (1 .. 2^22): live events the hypothesis may hold. Coverage
+ * counts stay uint16: a run that puts more than 65535 events over one
+ * (sample, station) fails with status 3 instead of wrapping. */
 int seis_engine_create(const seis_model_cfg* cfg, const double* stations, int64_t n_stations,
                        const void* signals /* [S][n] station-major, dtype */, int32_t dtype,
                        int64_t event_capacity, seis_engine** out);
 void seis_engine_destroy(seis_engine* eng);
+
+/* Arrival-version slots the engine allocated: min(2 * event_capacity + 2048,
+ * what fits in free HBM less 4 GiB), never below event_capacity. A phase needs
+ * the live events plus the phase-start versions it replaced. */
+int64_t seis_engine_pool_slots(const seis_engine* eng);
 
 /* Replace the signals (same shape/dtype) — one host->device copy. */
 int seis_upload_signals(seis_engine* eng, const void* signals);

@@ -130,7 +130,7 @@ __global__ void k_transpose(const YT* __restrict__ src, YT* __restrict__ dst, in
 }
 
 // coverage of every event of the table (variance_profile, density.hpp:112-129)
-__global__ void k_build_cov(Dev d, Table tab, const Ctl* ctl) {
+__global__ void k_build_cov(Dev d, Table tab, Ctl* ctl) {
   const int e = blockIdx.y;
   if (e >= ctl->n_events) return;
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
@@ -141,8 +141,13 @@ __global__ void k_build_cov(Dev d, Table tab, const Ctl* ctl) {
   const int lo = min(w0.lo < w0.hi ? w0.lo : INT_MAX, w1.lo < w1.hi ? w1.lo : INT_MAX);
   const int hi = max(w0.hi > w0.lo ? w0.hi : INT_MIN, w1.hi > w1.lo ? w1.hi : INT_MIN);
   for (int r = lo; r < hi; ++r) {
-    const unsigned inc = (unsigned)inw(r, w0) + ((unsigned)inw(r, w1) << 16);
-    if (inc) atomicAdd(d.cov + (size_t)r * d.P2 + p, inc);
+    const int i0 = inw(r, w0), i1 = inw(r, w1);
+    const unsigned inc = (unsigned)i0 + ((unsigned)i1 << 16);
+    if (inc) {
+      const unsigned old = atomicAdd(d.cov + (size_t)r * d.P2 + p, inc);
+      if ((old & 0xffffu) + i0 > 0xffffu || (old >> 16) + i1 > 0xffffu)
+        atomicExch(&ctl->err, ERR_COUNT_OVERFLOW);
+    }
   }
 }
 
@@ -499,6 +504,18 @@ __global__ void __launch_bounds__(NTT, MINB)
       // tile) proposal-major, which balances the warps better.
       if (T_per >= 4 * NWT) {
         for (int tile = warp; tile < T_per; tile += NWT) {
+          DiffW X;
+          long long tq = kProfItems ? clock64() : 0;
+          diff_windows(d, tile * 32 + lane, np_now, pold, pnew, X);
+          if (kProfItems) {
+            __syncwarp();
+            const long long now = clock64();
+            if (lane == 0) {
+              atomicAdd(&s_tprof[0][5], (unsigned long long)(now - tq));
+              atomicAdd(&s_tprof[1][5], 1ull);
+            }
+            tq = now;
+          }
 #pragma unroll 1
           for (int q = 0; q < m; ++q) {
             const Prop& P = prop[buf][q];
@@ -517,7 +534,7 @@ __global__ void __launch_bounds__(NTT, MINB)
             in.whi = win_hi;
             double sig = 0.0, arr = 0.0;
             int cnt = 0;
-            score_item<MODE, YT>(d, P, in, tile, np_now, pold, pnew, Ts, sig, arr, cnt);
+            score_item<MODE, YT>(d, P, in, tile, np_now, pold, pnew, &X, Ts, sig, arr, cnt);
             sig = warp_sum(sig);
             arr = warp_sum(arr);
             cnt = (int)__reduce_add_sync(0xffffffffu, (unsigned)cnt);
@@ -525,6 +542,14 @@ __global__ void __launch_bounds__(NTT, MINB)
               red_sig[warp][q] += sig;
               red_arr[warp][q] += arr;
               red_cnt[warp][q] += cnt;
+            }
+            if (kProfItems) {
+              const long long now = clock64();
+              if (lane == 0) {
+                atomicAdd(&s_tprof[0][P.type], (unsigned long long)(now - tq));
+                atomicAdd(&s_tprof[1][P.type], 1ull);
+              }
+              tq = now;
             }
           }
         }
@@ -570,7 +595,7 @@ __global__ void __launch_bounds__(NTT, MINB)
           in.step = (uint32_t)(i0 + q);
           in.wlo = win_lo;
           in.whi = win_hi;
-          score_item<MODE, YT>(d, P, in, tile, np_now, pold, pnew, Ts, sig, arr, cnt);
+          score_item<MODE, YT>(d, P, in, tile, np_now, pold, pnew, nullptr, Ts, sig, arr, cnt);
         }
         if (cur_q >= 0) {
           sig = warp_sum(sig);
@@ -959,8 +984,17 @@ __global__ void k_commit(Dev d, int color, int ncol, int nreg, const int* diff_c
           hi = max(hi, ws[k].hi);
         }
       for (int r = lo; r < hi; ++r) {
-        const int inc = (inw(r, n0) - inw(r, o0)) + (inw(r, n1) - inw(r, o1)) * 65536;
-        if (inc) atomicAdd(d.cov + (size_t)r * d.P2 + p, (unsigned)inc);
+        const int d0 = inw(r, n0) - inw(r, o0), d1 = inw(r, n1) - inw(r, o1);
+        const int inc = d0 + d1 * 65536;
+        if (inc) {
+          // true counts never go negative mid-commit (only counted start
+          // versions are removed), so the halves never borrow: a half that
+          // passes 0xffff is a real uint16 overflow
+          const unsigned old = atomicAdd(d.cov + (size_t)r * d.P2 + p, (unsigned)inc);
+          if ((d0 > 0 && (int)(old & 0xffffu) + d0 > 0xffff) ||
+              (d1 > 0 && (int)(old >> 16) + d1 > 0xffff))
+            atomicExch(&ctl->err, ERR_COUNT_OVERFLOW);
+        }
       }
     }
   }
@@ -1131,7 +1165,7 @@ __global__ void __launch_bounds__(NT, 1)
   int cnt = 0;
   const int T_per = (d.S_pad + 31) / 32;
   for (int t = warp; t < T_per; t += NW)
-    score_item<1, YT>(d, P, in, t, 0, nullptr, nullptr, Ts, sig, arr, cnt);
+    score_item<1, YT>(d, P, in, t, 0, nullptr, nullptr, nullptr, Ts, sig, arr, cnt);
   sig = warp_sum(sig);
   arr = warp_sum(arr);
   if (lane == 0) {
@@ -1368,6 +1402,7 @@ void validate_model(const seis_model_cfg* c, const double* st, int64_t S) {
 struct seis_engine {
   seis_model_cfg cfg{};
   int S = 0, S_pad = 0, P2 = 0, n = 0, dtype = 0, cap = 0;
+  int pool_slots = 0;  // arrival versions: live events + this phase's retired ones
   cudaStream_t stream = nullptr;
   Dev d{};
   double* stations = nullptr;
@@ -1465,9 +1500,10 @@ Ctl read_ctl(seis_engine* e) {
 const char* err_name(int e) {
   switch (e) {
     case ERR_OWN_OVERFLOW: return "a region exceeded the per-region event limit (64)";
-    case ERR_POOL_EXHAUSTED: return "event pool exhausted: raise event_capacity";
+    case ERR_POOL_EXHAUSTED: return "arrival pool exhausted (live events + replaced versions > pool slots): raise event_capacity";
     case ERR_TAPE_UNKNOWN_ID: return "replay tape names an event the region does not hold";
     case ERR_TABLE_OVERFLOW: return "event table overflow: raise event_capacity";
+    case ERR_COUNT_OVERFLOW: return "more than 65535 events cover one (sample, station): uint16 coverage count overflow";
     default: return "device error";
   }
 }
@@ -1496,7 +1532,7 @@ namespace {
 // config[2]): a chain's rounds slow down more than sharing an SM gains.
 template <typename YT, int MODE>
 void launch_phase_t(seis_engine* e, int ncr, const Samp& sp, const PhaseArgs& pa, int stamp) {
-  k_phase<YT, MODE, NT, 1><<<ncr, NT, kPhaseSmem, e->stream>>>(e->d, sp, pa, e->ctl, stamp);
+  k_phase<YT, MODE, NT, SEIS_MINB><<<ncr, NT, kPhaseSmem, e->stream>>>(e->d, sp, pa, e->ctl, stamp);
 }
 
 void launch_phase(seis_engine* e, int mode, int ncr, const Samp& sp, const PhaseArgs& pa,
@@ -1516,7 +1552,7 @@ void launch_phase(seis_engine* e, int mode, int ncr, const Samp& sp, const Phase
 
 template <typename YT, int MODE>
 void set_phase_attrs() {
-  ck(cudaFuncSetAttribute(k_phase<YT, MODE, NT, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  ck(cudaFuncSetAttribute(k_phase<YT, MODE, NT, SEIS_MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           kPhaseSmem),
      "smem attribute");
 }
@@ -1534,8 +1570,8 @@ int seis_engine_create(const seis_model_cfg* cfg, const double* stations, int64_
   const int rc = guarded([&] {
     validate_model(cfg, stations, n_stations);
     if (dtype != SEIS_F32 && dtype != SEIS_F64) throw std::invalid_argument("dtype must be F32 or F64");
-    if (event_capacity < 1 || event_capacity > 65000)
-      throw std::invalid_argument("event_capacity must be in [1, 65000] (uint16 coverage counts)");
+    if (event_capacity < 1 || event_capacity > kMaxEvents)
+      throw std::invalid_argument("event_capacity must be in [1, 4194304]");
     check_device();
     e = new seis_engine;
     e->cfg = *cfg;
@@ -1557,9 +1593,22 @@ int seis_engine_create(const seis_model_cfg* cfg, const double* stations, int64_
     ck(cudaMemset(e->y, 0, (size_t)(e->n + kRowPad) * e->S_pad * esz), "memset");
     e->cov = dalloc<uint32_t>((size_t)(e->n + kRowPad) * e->P2);
     ck(cudaMemset(e->cov, 0, (size_t)(e->n + kRowPad) * e->P2 * 4), "memset");
-    e->pool = dalloc<double>((size_t)e->cap * e->S_pad);
-    // per-count terms with glibc log, exactly as density.hpp:288-297
-    const int tab_n = e->cap + 8;
+    // arrival pool: a phase holds every live event plus the phase-start
+    // versions it replaced or killed (freed at the barrier) -> about twice
+    // the live events; bounded by what fits in HBM beside the other buffers
+    {
+      size_t free_b = 0, total_b = 0;
+      ck(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+      const size_t per = (size_t)e->S_pad * 8;
+      const size_t reserve = (size_t)4 << 30;
+      const size_t fit = free_b > reserve ? (free_b - reserve) / per : 0;
+      const size_t want = 2 * (size_t)e->cap + 2048;
+      e->pool_slots = (int)std::min<size_t>(want, std::max<size_t>(fit, (size_t)e->cap));
+    }
+    e->pool = dalloc<double>((size_t)e->pool_slots * e->S_pad);
+    // per-count terms with glibc log, exactly as density.hpp:288-297; counts
+    // are uint16 (<= 65535) plus at most 2 * MAXOWN in-phase own versions
+    const int tab_n = std::min(e->cap, 65535) + 2 * MAXOWN + 8;
     std::vector<double> L(tab_n), I(tab_n);
     for (int c = 0; c < tab_n; ++c) {
       const double var = cfg->var_noise + c * cfg->var_event;
@@ -1581,25 +1630,27 @@ int seis_engine_create(const seis_model_cfg* cfg, const double* stations, int64_
     e->Ig = dalloc<double>(tab_n);
     ck(cudaMemcpy(e->Lg, L.data(), tab_n * 8, cudaMemcpyHostToDevice), "H2D");
     ck(cudaMemcpy(e->Ig, I.data(), tab_n * 8, cudaMemcpyHostToDevice), "H2D");
-    e->h_logi.resize(tab_n);
-    e->h_logfact.resize(tab_n);
+    // log i and log i! for event counts: the live events plus a region's births
+    const int logi_n = e->cap + 2 * MAXOWN + 8;
+    e->h_logi.resize(logi_n);
+    e->h_logfact.resize(logi_n);
     double acc = 0.0;
-    for (int i = 0; i < tab_n; ++i) {
+    for (int i = 0; i < logi_n; ++i) {
       e->h_logi[i] = i > 0 ? std::log(static_cast<double>(i)) : -INFINITY;
       if (i >= 2) acc += std::log(static_cast<double>(i));  // log_factorial, density.hpp:21-25
       e->h_logfact[i] = acc;
     }
-    e->logi = dalloc<double>(tab_n);
-    e->logfact = dalloc<double>(tab_n);
-    ck(cudaMemcpy(e->logi, e->h_logi.data(), tab_n * 8, cudaMemcpyHostToDevice), "H2D");
-    ck(cudaMemcpy(e->logfact, e->h_logfact.data(), tab_n * 8, cudaMemcpyHostToDevice), "H2D");
+    e->logi = dalloc<double>(logi_n);
+    e->logfact = dalloc<double>(logi_n);
+    ck(cudaMemcpy(e->logi, e->h_logi.data(), logi_n * 8, cudaMemcpyHostToDevice), "H2D");
+    ck(cudaMemcpy(e->logfact, e->h_logfact.data(), logi_n * 8, cudaMemcpyHostToDevice), "H2D");
     for (auto& t : e->tab) {
       t.id = dalloc<unsigned long long>(e->cap);
       t.x = dalloc<double>(e->cap);
       t.t = dalloc<double>(e->cap);
       t.slot = dalloc<int>(e->cap);
     }
-    e->free_stack = dalloc<int>(e->cap);
+    e->free_stack = dalloc<int>(e->pool_slots);
     e->ctl = dalloc<Ctl>(1);
     e->fate_stamp = dalloc<int>(e->cap);
     ck(cudaMemset(e->fate_stamp, 0, e->cap * 4), "memset");
@@ -1633,8 +1684,8 @@ int seis_engine_create(const seis_model_cfg* cfg, const double* stations, int64_
     d.Dg = e->Dg;
     d.tab_n = tab_n;
     d.logi = e->logi;
-    d.logi_n = tab_n;
-    d.pool_cap = e->cap;
+    d.logi_n = logi_n;
+    d.pool_cap = e->pool_slots;
     set_phase_attrs<float, 0>();
     set_phase_attrs<float, 1>();
     set_phase_attrs<double, 0>();
@@ -1660,6 +1711,8 @@ int seis_engine_create(const seis_model_cfg* cfg, const double* stations, int64_
 
 void seis_engine_destroy(seis_engine* eng) { delete eng; }
 
+int64_t seis_engine_pool_slots(const seis_engine* eng) { return eng ? eng->pool_slots : 0; }
+
 int seis_upload_signals(seis_engine* e, const void* signals) {
   return guarded([&] { upload_signals(e, signals); });
 }
@@ -1676,7 +1729,7 @@ int seis_set_hypothesis(seis_engine* e, int64_t N, const uint64_t* ids, const do
     std::vector<unsigned long long> hid(N);
     std::vector<double> hx(N), ht(N);
     std::vector<long long> row(N);
-    std::vector<int> hs(N), fs(e->cap);
+    std::vector<int> hs(N), fs(e->pool_slots);
     for (int64_t i = 0; i < N; ++i) {
       const int64_t k = order[i];
       hid[i] = ids[k];
@@ -1685,9 +1738,9 @@ int seis_set_hypothesis(seis_engine* e, int64_t N, const uint64_t* ids, const do
       hs[i] = (int)i;
       row[i] = k;  // slot i holds input row k
     }
-    // free stack: slots N..cap-1 (top of stack = lowest)
+    // free stack: slots N..pool_slots-1 (top of stack = lowest)
     int nf = 0;
-    for (int s2 = e->cap - 1; s2 >= (int)N; --s2) fs[nf++] = s2;
+    for (int s2 = e->pool_slots - 1; s2 >= (int)N; --s2) fs[nf++] = s2;
     e->cur = 0;
     Table& tb = e->tab[0];
     if (N) {

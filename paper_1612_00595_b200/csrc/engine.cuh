@@ -29,12 +29,16 @@ constexpr int MSPEC = SEIS_MSPEC;  // speculative proposals evaluated per round
 #define SEIS_PROF_ITEMS 0
 #endif
 constexpr bool kProfItems = SEIS_PROF_ITEMS;
+#ifndef SEIS_MINB
+#define SEIS_MINB 1  // k_phase CTAs per SM the register budget is cut for
+#endif
 constexpr int NW = NT / 32;
 constexpr int MAXOWN = 64;       // events a region may hold during a phase
+constexpr int kMaxEvents = 1 << 22;  // event_capacity bound (table sizes; counts stay uint16)
 constexpr int MAXDIFF = 2 * MAXOWN;  // diff pairs a region may hold
 constexpr int MAXDOUT = 3 * MAXOWN;  // diff pairs + recycled slots per region
 constexpr int TBL = 512;         // coverage counts whose {dL, dI} rows live in smem
-constexpr int kRowPad = 16;      // zero rows appended to y and cov (unpredicated chunk loads)
+constexpr int kRowPad = 32;      // zero rows appended to y and cov (unpredicated chunk loads)
 constexpr int LOGIWIN = 1024;    // log(i) window around the phase-start event count
 constexpr int BANDMAX = 256;     // rows of the generic diff-correction scratch
 constexpr double kLog2Pi = 1.8378770664093454835606594728112;

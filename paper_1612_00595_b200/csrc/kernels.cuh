@@ -194,12 +194,15 @@ __device__ __forceinline__ void band(const Dev& d, int j, int blo, int bhi, cons
 // the lane's window changes, so the warp walks its common band row by row
 // (coalesced: one line per row for the 32 stations) with the lane's window
 // test as a predicate. cnt is the window length (computed by the caller).
-static_assert(kRowPad >= 8, "band1 loads RU <= 8 rows past the band");
+#ifndef SEIS_BAND_RU
+#define SEIS_BAND_RU 7
+#endif
+static_assert(kRowPad >= SEIS_BAND_RU, "band1 loads up to RU - 1 rows past the band");
 template <int SIGN, int ND, typename YT>
 __device__ __forceinline__ void band1(const Dev& d, int j, int blo, int bhi, Win W,
                                       const Wins<ND>& D, const int (&sg)[ND > 0 ? ND : 1],
                                       const double2* Ts, double& sig) {
-  constexpr int RU = sizeof(YT) == 4 ? 8 : 4;
+  constexpr int RU = sizeof(YT) == 4 ? SEIS_BAND_RU : 4;
   constexpr int code = SIGN > 0 ? 2 : 1;  // dc_code(+1) / dc_code(-1)
   const unsigned len = (unsigned)(W.hi - W.lo);
   const size_t stride = (size_t)d.S_pad;
@@ -365,6 +368,56 @@ __device__ __noinline__ void band_generic(const Dev& d, int j, bool v, int blo, 
   *out_cnt += cnt;
 }
 
+// Effective diff windows of the region's own changes at station j: (start,
+// current) version pairs whose windows coincide here (an arrival move
+// elsewhere) correct nothing. The same for every proposal of a round, so the
+// tile-major pass computes them once per tile. nwmax (warp max) > 4 sends the
+// station through band_generic, which walks the pairs itself.
+struct DiffW {
+  Wins<4> D;
+  int sg[4];
+  int nwmax;
+};
+
+__device__ __forceinline__ void diff_windows(const Dev& d, int j, int np, const int* pold,
+                                             const int* pnew, DiffW& X) {
+  const bool v = j < d.S;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    X.D.w[q] = empty_win();
+    X.sg[q] = 0;
+  }
+  int nw = 0;
+  for (int q = 0; q < np && v; ++q) {
+    const Win wo = pold[q] >= 0 ? make_win(d, d.pool[(size_t)pold[q] * d.S_pad + j]) : empty_win();
+    const Win wn = pnew[q] >= 0 ? make_win(d, d.pool[(size_t)pnew[q] * d.S_pad + j]) : empty_win();
+    if (weq(wo, wn)) continue;
+    if (wo.hi > wo.lo) {
+      if (nw < 4) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (k == nw) {
+            X.D.w[k] = wo;
+            X.sg[k] = -1;
+          }
+      }
+      ++nw;
+    }
+    if (wn.hi > wn.lo) {
+      if (nw < 4) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (k == nw) {
+            X.D.w[k] = wn;
+            X.sg[k] = 1;
+          }
+      }
+      ++nw;
+    }
+  }
+  X.nwmax = (int)__reduce_max_sync(0xffffffffu, (unsigned)nw);
+}
+
 // One station of one proposal (density.hpp:239-301): arrival densities of
 // the added/removed versions (arr += added - removed) and the per-sample
 // terms where the coverage changes (sig). Called by a whole warp
@@ -372,8 +425,8 @@ __device__ __noinline__ void band_generic(const Dev& d, int j, bool v, int blo, 
 template <int NR, int NA, typename YT>
 __device__ __forceinline__ void station_item(const Dev& d, const Prop& P, const PassIn& in,
                                              int j, int np, const int* pold, const int* pnew,
-                                             const double2* Ts, double& sig, double& arr,
-                                             int& cnt) {
+                                             const DiffW* Xp, const double2* Ts, double& sig,
+                                             double& arr, int& cnt) {
   const bool v = j < d.S;
   Wins<NR> R;
   Wins<NA> A;
@@ -439,44 +492,14 @@ __device__ __forceinline__ void station_item(const Dev& d, const Prop& P, const 
   const int blo = __reduce_min_sync(0xffffffffu, lo);
   const int bhi = __reduce_max_sync(0xffffffffu, hi);
   if (blo >= bhi) return;
-  // effective diff windows at this station: a (start, current) version pair
-  // whose windows coincide here (an arrival move elsewhere) corrects nothing
-  Wins<4> D;
-  int sg[4];
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    D.w[q] = empty_win();
-    sg[q] = 0;
-  }
-  int nw = 0;
-  for (int q = 0; q < np && v; ++q) {
-    const Win wo = pold[q] >= 0 ? make_win(d, d.pool[(size_t)pold[q] * d.S_pad + j]) : empty_win();
-    const Win wn = pnew[q] >= 0 ? make_win(d, d.pool[(size_t)pnew[q] * d.S_pad + j]) : empty_win();
-    if (weq(wo, wn)) continue;
-    if (wo.hi > wo.lo) {
-      if (nw < 4) {
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-          if (k == nw) {
-            D.w[k] = wo;
-            sg[k] = -1;
-          }
-      }
-      ++nw;
-    }
-    if (wn.hi > wn.lo) {
-      if (nw < 4) {
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-          if (k == nw) {
-            D.w[k] = wn;
-            sg[k] = 1;
-          }
-      }
-      ++nw;
-    }
-  }
-  const int nwmax = __reduce_max_sync(0xffffffffu, (unsigned)nw);
+  // the tile-major pass hands in the tile's diff windows; otherwise they are
+  // built here, only for stations the proposal changes
+  DiffW Xl;
+  if (!Xp) diff_windows(d, j, np, pold, pnew, Xl);
+  const DiffW& X = Xp ? *Xp : Xl;
+  const Wins<4>& D = X.D;
+  const int(&sg)[4] = X.sg;
+  const int nwmax = X.nwmax;
   if (nwmax == 0) {
     Wins<0> D0;
     int sg0[1];
@@ -551,8 +574,8 @@ __device__ __forceinline__ void arrival_item(const Dev& d, const Prop& P, const 
 template <int MODE, typename YT>
 __device__ __forceinline__ void score_item(const Dev& d, const Prop& P, const PassIn& in,
                                            int tile, int np, const int* pold,
-                                           const int* pnew, const double2* Ts, double& sig,
-                                           double& arr, int& cnt) {
+                                           const int* pnew, const DiffW* X, const double2* Ts,
+                                           double& sig, double& arr, int& cnt) {
   if (P.skip) return;
   const int j = tile * 32 + (threadIdx.x & 31);
   if (MODE == 0 && P.type == 3) {
@@ -561,13 +584,13 @@ __device__ __forceinline__ void score_item(const Dev& d, const Prop& P, const Pa
   }
   const int shape = P.nr * 3 + P.na;
   if (shape == 1)  // birth
-    station_item<0, 1, YT>(d, P, in, j, np, pold, pnew, Ts, sig, arr, cnt);
+    station_item<0, 1, YT>(d, P, in, j, np, pold, pnew, X, Ts, sig, arr, cnt);
   else if (shape == 3)  // death
-    station_item<1, 0, YT>(d, P, in, j, np, pold, pnew, Ts, sig, arr, cnt);
+    station_item<1, 0, YT>(d, P, in, j, np, pold, pnew, X, Ts, sig, arr, cnt);
   else if (shape == 4)  // location / arrival
-    station_item<1, 1, YT>(d, P, in, j, np, pold, pnew, Ts, sig, arr, cnt);
+    station_item<1, 1, YT>(d, P, in, j, np, pold, pnew, X, Ts, sig, arr, cnt);
   else  // joint pair, and any other change of <= 2 removed / 2 added events
-    station_item<2, 2, YT>(d, P, in, j, np, pold, pnew, Ts, sig, arr, cnt);
+    station_item<2, 2, YT>(d, P, in, j, np, pold, pnew, X, Ts, sig, arr, cnt);
 }
 
 }  // namespace seis

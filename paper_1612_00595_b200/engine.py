@@ -67,7 +67,7 @@ EXPORTS = ("seis_last_error", "seis_engine_create", "seis_engine_destroy", "seis
            "seis_partition_offset", "seis_score_batch", "seis_log_joint", "seis_run_chromatic",
            "seis_world_last_error", "seis_world_generate", "seis_world_with_events",
            "seis_thomas_events", "seis_set_snapshot_capacity", "seis_get_snapshots",
-           "seis_run_naive")
+           "seis_run_naive", "seis_engine_pool_slots")
 
 _LIB = None
 
@@ -86,6 +86,8 @@ def load_library(path: str | None = None) -> C.CDLL:
     L.seis_world_last_error.restype = C.c_char_p
     L.seis_engine_create.argtypes = [P, P, i64, P, i32, i64, P]
     L.seis_engine_destroy.argtypes = [P]
+    L.seis_engine_pool_slots.argtypes = [P]
+    L.seis_engine_pool_slots.restype = C.c_int64
     L.seis_upload_signals.argtypes = [P, P]
     L.seis_set_hypothesis.argtypes = [P, i64, P, P, P, P]
     L.seis_get_hypothesis.argtypes = [P, i64, P, P, P, P, P]
@@ -361,6 +363,7 @@ class Engine:
                                          event_capacity, C.byref(h)), self.L)
         self.h = h
         self.capacity = event_capacity
+        self.pool_slots = int(self.L.seis_engine_pool_slots(h))
 
     def close(self):
         if getattr(self, "h", None):
