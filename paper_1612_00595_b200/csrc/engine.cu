@@ -115,7 +115,7 @@ __global__ void k_region_of(const double* b, int n, int64_t m, const double* t, 
 // ----------------------------------------------------------------- signals
 template <typename YT>
 __global__ void k_transpose(const YT* __restrict__ src, YT* __restrict__ dst, int S, int S_pad,
-                            int n) {
+                            int n, int rows) {
   __shared__ YT tile[32][33];
   const int s0 = blockIdx.x * 32, j0 = blockIdx.y * 32;
   for (int k = threadIdx.y; k < 32; k += blockDim.y) {
@@ -125,7 +125,7 @@ __global__ void k_transpose(const YT* __restrict__ src, YT* __restrict__ dst, in
   __syncthreads();
   for (int k = threadIdx.y; k < 32; k += blockDim.y) {
     const int s = s0 + k, j = j0 + threadIdx.x;
-    if (s < n && j < S_pad) dst[(size_t)s * S_pad + j] = tile[threadIdx.x][k];
+    if (s < n && j < S_pad) dst[yix(rows, s, j)] = tile[threadIdx.x][k];
   }
 }
 
@@ -144,7 +144,7 @@ __global__ void k_build_cov(Dev d, Table tab, Ctl* ctl) {
     const int i0 = inw(r, w0), i1 = inw(r, w1);
     const unsigned inc = (unsigned)i0 + ((unsigned)i1 << 16);
     if (inc) {
-      const unsigned old = atomicAdd(d.cov + (size_t)r * d.P2 + p, inc);
+      const unsigned old = atomicAdd(d.cov + pix(d.rows, r, p), inc);
       if ((old & 0xffffu) + i0 > 0xffffu || (old >> 16) + i1 > 0xffffu)
         atomicExch(&ctl->err, ERR_COUNT_OVERFLOW);
     }
@@ -352,15 +352,20 @@ __global__ void __launch_bounds__(NTT, MINB)
   __shared__ int lfree[MAXOWN];
   __shared__ Prop prop[2][MSPEC];
   __shared__ double red_sig[NWT][MSPEC], red_arr[NWT][MSPEC];
+
   __shared__ int red_cnt[NWT][MSPEC];
   __shared__ int s_w[NWT];
   __shared__ int s_nown, s_np, s_abort, s_tmp, s_adv, s_accq;
   __shared__ unsigned long long s_births;
-  __shared__ unsigned long long s_tprof[2][8];
   __shared__ double s_delta[MSPEC], s_logr[MSPEC], s_prior[2];
   __shared__ int s_item;
   __shared__ double s_logi_k[MAXOWN + 2];   // log(i), i <= MAXOWN + 1 (proposal terms)
-  extern __shared__ double s_logi_n[];       // [LOGIWIN] log(i), i in [N - LOGIWIN/2, N + LOGIWIN/2)
+  // dynamic: [LOGIWIN] log(i), i in [N - LOGIWIN/2, N + LOGIWIN/2), then the
+  // per-lane partial sums of the tile-major pass
+  extern __shared__ double s_logi_n[];
+  double(*acc_sig)[NTT] = reinterpret_cast<double(*)[NTT]>(s_logi_n + LOGIWIN);
+  double(*acc_arr)[NTT] = reinterpret_cast<double(*)[NTT]>(s_logi_n + LOGIWIN + MSPEC * NTT);
+  int(*acc_cnt)[NTT] = reinterpret_cast<int(*)[NTT]>(s_logi_n + LOGIWIN + 2 * MSPEC * NTT);
   __shared__ int s_accg[MSPEC], s_cnt[MSPEC];
   __shared__ long long s_nlocal;
 
@@ -391,7 +396,7 @@ __global__ void __launch_bounds__(NTT, MINB)
     s_nown = 0;
     s_abort = 0;
   }
-  if (tid < 16) s_tprof[tid >> 3][tid & 7] = 0ull;
+  if (tid < 16) s_tprof[tid >> 3][tid & 7] = 0ull;  // kernels.cuh
   __syncthreads();
   // own events: table entries (id order) inside the region
   // (events_in_region, proposals.hpp:65-71, on the local copy of samplers.hpp:448)
@@ -439,10 +444,33 @@ __global__ void __launch_bounds__(NTT, MINB)
   }
   const int nstart = s_nown;
   // thread-0 chain state (mirrored in shared memory for the generators)
-  int nown = nstart, np = 0, nlfree = 0;
-  long long n_local = N;
-  unsigned long long births = 0, n_acc = 0, n_scored = 0, n_arr = 0, n_changed = 0;
-  unsigned long long n_spec = 0;
+  // thread-0 chain state lives in shared memory: registers are allocated for
+  // every thread, and the scoring passes need them more
+  __shared__ struct {
+    long long n_local, tc, tprof[6];
+    unsigned long long births, n_acc, n_scored, n_arr, n_changed, n_spec;
+    int nown, np, nlfree;
+  } z;
+  int& nown = z.nown;
+  int& np = z.np;
+  int& nlfree = z.nlfree;
+  long long& n_local = z.n_local;
+  unsigned long long& births = z.births;
+  unsigned long long& n_acc = z.n_acc;
+  unsigned long long& n_scored = z.n_scored;
+  unsigned long long& n_arr = z.n_arr;
+  unsigned long long& n_changed = z.n_changed;
+  unsigned long long& n_spec = z.n_spec;
+  long long(&tprof)[6] = z.tprof;
+  long long& tc = z.tc;
+  if (tid == 0) {
+    nown = nstart;
+    np = nlfree = 0;
+    n_local = N;
+    births = n_acc = n_scored = n_arr = n_changed = n_spec = 0;
+    for (int q = 0; q < 6; ++q) tprof[q] = 0;
+    tc = clock64();
+  }
   const unsigned long long id_base =
       pa.naive ? ((unsigned long long)region + 1ull) << 32  // samplers.hpp:349
                : pa.next_base + (unsigned long long)slot_idx * sp.k;
@@ -453,8 +481,6 @@ __global__ void __launch_bounds__(NTT, MINB)
   }
   const int T_per = (d.S_pad + 31) / 32;  // tiles of 32 stations
   int round = 0;
-  long long tprof[6] = {0, 0, 0, 0, 0, 0};
-  long long tc = clock64();
   for (int i0 = 0; i0 < (int)sp.k; ++round) {
     const int m = min(MSPEC, (int)sp.k - i0);
     const int buf = round & 1;
@@ -488,6 +514,12 @@ __global__ void __launch_bounds__(NTT, MINB)
       red_sig[warp][lane] = 0.0;
       red_arr[warp][lane] = 0.0;
       red_cnt[warp][lane] = 0;
+    }
+#pragma unroll
+    for (int q = 0; q < MSPEC; ++q) {
+      acc_sig[q][tid] = 0.0;
+      acc_arr[q][tid] = 0.0;
+      acc_cnt[q][tid] = 0;
     }
     __syncthreads();  // S1: proposals ready
     if (tid == 0) {
@@ -535,14 +567,10 @@ __global__ void __launch_bounds__(NTT, MINB)
             double sig = 0.0, arr = 0.0;
             int cnt = 0;
             score_item<MODE, YT>(d, P, in, tile, np_now, pold, pnew, &X, Ts, sig, arr, cnt);
-            sig = warp_sum(sig);
-            arr = warp_sum(arr);
-            cnt = (int)__reduce_add_sync(0xffffffffu, (unsigned)cnt);
-            if (lane == 0) {
-              red_sig[warp][q] += sig;
-              red_arr[warp][q] += arr;
-              red_cnt[warp][q] += cnt;
-            }
+            // per-lane partial sums; the warp reduces them once per round
+            acc_sig[q][tid] += sig;
+            acc_arr[q][tid] += arr;
+            acc_cnt[q][tid] += cnt;
             if (kProfItems) {
               const long long now = clock64();
               if (lane == 0) {
@@ -551,6 +579,16 @@ __global__ void __launch_bounds__(NTT, MINB)
               }
               tq = now;
             }
+          }
+        }
+        for (int q = 0; q < m; ++q) {
+          const double sg = warp_sum(acc_sig[q][tid]);
+          const double ar = warp_sum(acc_arr[q][tid]);
+          const int cn = (int)__reduce_add_sync(0xffffffffu, (unsigned)acc_cnt[q][tid]);
+          if (lane == 0) {
+            red_sig[warp][q] = sg;
+            red_arr[warp][q] = ar;
+            red_cnt[warp][q] = cn;
           }
         }
       } else {
@@ -990,7 +1028,7 @@ __global__ void k_commit(Dev d, int color, int ncol, int nreg, const int* diff_c
           // true counts never go negative mid-commit (only counted start
           // versions are removed), so the halves never borrow: a half that
           // passes 0xffff is a real uint16 overflow
-          const unsigned old = atomicAdd(d.cov + (size_t)r * d.P2 + p, (unsigned)inc);
+          const unsigned old = atomicAdd(d.cov + pix(d.rows, r, p), (unsigned)inc);
           if ((d0 > 0 && (int)(old & 0xffffu) + d0 > 0xffff) ||
               (d1 > 0 && (int)(old >> 16) + d1 > 0xffff))
             atomicExch(&ctl->err, ERR_COUNT_OVERFLOW);
@@ -1191,11 +1229,14 @@ __global__ void k_lj_signal(const Dev d, double* part) {
   __shared__ double sred[32];
   using T2 = typename Y2<YT>::T;
   const T2* y2 = reinterpret_cast<const T2*>(d.y);
-  const size_t total = (size_t)d.n * d.P2;
+  const size_t total = (size_t)d.rows * d.P2;  // station tiles incl. pad rows
   double acc = 0.0;
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
        i += (size_t)gridDim.x * blockDim.x) {
-    const int p = (int)(i % d.P2);
+    const size_t q = i >> 4;
+    const int r = (int)(q % (size_t)d.rows);
+    if (r >= d.n) continue;
+    const int p = (int)((q / (size_t)d.rows) * 16 + (i & 15));
     const uint32_t w = d.cov[i];
     const T2 yy = y2[i];
     if (2 * p < d.S) {
@@ -1325,7 +1366,9 @@ using namespace seis;
 namespace {
 
 thread_local std::string g_err;
-constexpr int kPhaseSmem = LOGIWIN * (int)sizeof(double);  // dynamic: the log(i) window
+// dynamic: the log(i) window + per-lane partial sums (2 double + 1 int per
+// speculative slot and thread)
+constexpr int kPhaseSmem = LOGIWIN * (int)sizeof(double) + MSPEC * NT * (2 * 8 + 4);
 
 int fail(int code, const std::string& m) {
   g_err = m;
@@ -1480,11 +1523,11 @@ void upload_signals(seis_engine* e, const void* signals) {
   if (e->dtype == SEIS_F64)
     k_transpose<double><<<grid, block, 0, e->stream>>>(static_cast<const double*>(tmp),
                                                        static_cast<double*>(e->y), e->S,
-                                                       e->S_pad, e->n);
+                                                       e->S_pad, e->n, e->n + kRowPad);
   else
     k_transpose<float><<<grid, block, 0, e->stream>>>(static_cast<const float*>(tmp),
                                                       static_cast<float*>(e->y), e->S, e->S_pad,
-                                                      e->n);
+                                                      e->n, e->n + kRowPad);
   ck(cudaGetLastError(), "k_transpose");
   ck(cudaStreamSynchronize(e->stream), "sync");
   cudaFree(tmp);
@@ -1661,6 +1704,7 @@ int seis_engine_create(const seis_model_cfg* cfg, const double* stations, int64_
     Dev& d = e->d;
     d.S = e->S;
     d.S_pad = e->S_pad;
+    d.rows = e->n + kRowPad;
     d.P2 = e->P2;
     d.n = e->n;
     d.rate = cfg->sample_rate;
@@ -1766,7 +1810,7 @@ int seis_set_hypothesis(seis_engine* e, int64_t N, const uint64_t* ids, const do
     c.n_events = (int)N;
     c.free_top = nf;
     ck(cudaMemcpy(e->ctl, &c, sizeof c, cudaMemcpyHostToDevice), "H2D");
-    ck(cudaMemsetAsync(e->cov, 0, (size_t)e->n * e->P2 * 4, e->stream), "memset");
+    ck(cudaMemsetAsync(e->cov, 0, (size_t)(e->n + kRowPad) * e->P2 * 4, e->stream), "memset");
     if (N) {
       dim3 grid((e->P2 + 127) / 128, (unsigned)N);
       k_build_cov<<<grid, 128, 0, e->stream>>>(e->d, tb, e->ctl);
@@ -2268,7 +2312,7 @@ extern "C" int seis_run_chromatic(seis_engine* e, const seis_sampler_cfg* sc, in
       fprintf(stderr, "[seis prof] cycles: gen %llu items %llu decide %llu (parallel part %llu) writeback %llu rounds %llu\n",
               c.prof[0], c.prof[1], c.prof[2], c.prof[5], c.prof[3], c.prof[4]);
     if (getenv("SEIS_PROF"))
-      for (int q = 0; q < 6; ++q)
+      for (int q = 0; q < 8; ++q)
         fprintf(stderr, "[seis prof] type %d: items %llu warp-cycles/item %.0f\n", q,
                 c.tprof[1][q], c.tprof[1][q] ? (double)c.tprof[0][q] / c.tprof[1][q] : 0.0);
     if (stats) {

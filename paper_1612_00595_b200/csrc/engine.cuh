@@ -47,15 +47,23 @@ struct Win {
   int lo, hi;
 };
 
+// Signal and count layout ("station tiles"): the 32 stations of tile
+// b = j >> 5 keep their rows contiguous, element (r, j) at
+// ((j >> 5) * rows + r) * 32 + (j & 31) with rows = n + kRowPad. One row of a
+// tile is one 128-byte line of y (fp32) / 64-byte line of counts, so a warp
+// walking a station tile's rows reads coalesced lines at compile-time offsets.
+// Counts are uint16; two neighbouring stations share a uint32 word (the
+// commit's packed atomics): pair p = j >> 1 at ((p >> 4) * rows + r) * 16 + (p & 15).
 struct Dev {
   int S, S_pad, P2, n;
+  int rows;                        // n + kRowPad
   double rate, t_s, v, sigma, x_max, T;
   double c0_arr, twovar_arr;       // log_gaussian constants for sigma_arrival
   double log_lambda_T, lxa;        // log(lambda T), -log(x_max) - log(T)
   double log_xmax;
   const double* stations;          // [S_pad]
-  const void* y;                   // [n][S_pad]
-  uint32_t* cov;                   // [n][P2]
+  const void* y;                   // [S_pad / 32][rows][32] (station tiles)
+  uint32_t* cov;                   // [S_pad / 32][rows][16] uint16 pairs
   double* pool;                    // [P][S_pad]
   const double* Lg;                // [tab_n] -0.5 (log 2pi + log var_c)
   const double* Ig;                // [tab_n] 0.5 / var_c
@@ -153,6 +161,14 @@ __device__ __forceinline__ Win make_win(const Dev& d, double a) {
   w.lo = min(max(__double2int_ru(a * d.rate), 0), d.n);
   w.hi = min(max(__double2int_ru((a + d.t_s) * d.rate), 0), d.n);
   return w;
+}
+
+// element (r, j) of y / uint16 counts; uint32 count pair (r, p = j >> 1)
+__host__ __device__ __forceinline__ size_t yix(int rows, int r, int j) {
+  return ((size_t)(j >> 5) * rows + r) * 32 + (j & 31);
+}
+__host__ __device__ __forceinline__ size_t pix(int rows, int r, int p) {
+  return ((size_t)(p >> 4) * rows + r) * 16 + (p & 15);
 }
 
 __device__ __forceinline__ int inw(int r, Win w) {

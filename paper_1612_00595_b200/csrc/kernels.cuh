@@ -28,6 +28,9 @@ struct Y2<double> {
   using T = double2;
 };
 
+// per-item cycle counters of the profiling build (SEIS_PROF_ITEMS=1)
+__shared__ unsigned long long s_tprof[2][8];
+
 // Proposal descriptor (one per speculative slot, double-buffered by round).
 struct Prop {
   int type, skip, scored, nr, na, bad;
@@ -122,13 +125,13 @@ __device__ __forceinline__ void band(const Dev& d, int j, int blo, int bhi, cons
                                      const int (&sg)[ND > 0 ? ND : 1], const double2* Ts,
                                      double& sig, int& cnt) {
   constexpr int RU = 4;
-  const int stride = d.S_pad;
-  const YT* __restrict__ y = reinterpret_cast<const YT*>(d.y);
-  const uint16_t* __restrict__ c16 = reinterpret_cast<const uint16_t*>(d.cov);
+  constexpr int stride = 32;  // next row of the station tile
+  const YT* __restrict__ y = reinterpret_cast<const YT*>(d.y) + yix(d.rows, 0, j);
+  const uint16_t* __restrict__ c16 = reinterpret_cast<const uint16_t*>(d.cov) + yix(d.rows, 0, j);
   double s_loc = 0.0;
   int c_loc = 0;
   bool big = false;
-  int off = blo * stride + j;
+  int off = blo * stride;
   for (int r0 = blo; r0 < bhi; r0 += RU, off += RU * stride) {
     int dc[RU];
 #pragma unroll
@@ -177,7 +180,7 @@ __device__ __forceinline__ void band(const Dev& d, int j, int blo, int bhi, cons
 #pragma unroll
       for (int q = 0; q < NR; ++q) dcv -= inw(r, R.w[q]);
       if (dcv) {
-        const int o = r * stride + j;
+        const int o = r * stride;
         int cc = (int)__ldg(c16 + o);
 #pragma unroll
         for (int q = 0; q < ND; ++q) cc += sg[q] * inw(r, D.w[q]);
@@ -191,60 +194,110 @@ __device__ __forceinline__ void band(const Dev& d, int j, int blo, int bhi, cons
 }
 
 // Dense single-window moves (birth: SIGN +1, death: SIGN -1): every row of
-// the lane's window changes, so the warp walks its common band row by row
-// (coalesced: one line per row for the 32 stations) with the lane's window
-// test as a predicate. cnt is the window length (computed by the caller).
+// the lane's window changes. Each lane walks its own window down its station
+// tile (rows 32 elements apart: compile-time load offsets, one 128-byte line
+// per row for the warp when the lanes' windows align, as they do under the
+// reference's geometry); the warp runs the longest window's trip count and
+// rows past a lane's window index the zero row of the table. cnt is the
+// window length (computed by the caller).
 #ifndef SEIS_BAND_RU
 #define SEIS_BAND_RU 7
 #endif
-static_assert(kRowPad >= SEIS_BAND_RU, "band1 loads up to RU - 1 rows past the band");
+#ifndef SEIS_BAND_PIPE
+#define SEIS_BAND_PIPE 0
+#endif
+static_assert(kRowPad >= SEIS_BAND_RU, "band1 reads up to RU - 1 rows past the longest window");
 template <int SIGN, int ND, typename YT>
-__device__ __forceinline__ void band1(const Dev& d, int j, int blo, int bhi, Win W,
-                                      const Wins<ND>& D, const int (&sg)[ND > 0 ? ND : 1],
-                                      const double2* Ts, double& sig) {
+__device__ __forceinline__ void band1(const Dev& d, int j, Win W, const Wins<ND>& D,
+                                      const int (&sg)[ND > 0 ? ND : 1], const double2* Ts,
+                                      double& sig) {
   constexpr int RU = sizeof(YT) == 4 ? SEIS_BAND_RU : 4;
   constexpr int code = SIGN > 0 ? 2 : 1;  // dc_code(+1) / dc_code(-1)
-  const unsigned len = (unsigned)(W.hi - W.lo);
-  const size_t stride = (size_t)d.S_pad;
-  const YT* __restrict__ yp = reinterpret_cast<const YT*>(d.y) + (size_t)blo * stride + j;
+  const int len = W.hi - W.lo;
+  const int trips = (int)__reduce_max_sync(0xffffffffu, (unsigned)len);
+  // the walk covers rows [base, base + ceil(trips / RU) * RU) of the tile;
+  // base = W.lo unless that would run past the pad rows
+  const int span = (trips + RU - 1) / RU * RU;
+  const int base = min(W.lo, d.rows - span);
+  const int sh = W.lo - base;
+  const YT* __restrict__ yp = reinterpret_cast<const YT*>(d.y) + yix(d.rows, base, j);
   const uint16_t* __restrict__ cp =
-      reinterpret_cast<const uint16_t*>(d.cov) + (size_t)blo * stride + j;
+      reinterpret_cast<const uint16_t*>(d.cov) + yix(d.rows, base, j);
   double s = 0.0;
   int mx = 0;
-  // every lane loads every band row (the band's sectors are shared by the
-  // warp's 32 stations anyway); rows outside the lane's window index the zero
-  // row of the table
-  for (int r0 = blo; r0 < bhi; r0 += RU) {
-    int c[RU];
-    YT yv[RU];
-#pragma unroll
-    for (int k = 0; k < RU; ++k) {  // rows up to bhi + RU - 1 <= n + kRowPad exist
-      c[k] = (int)__ldg(cp);
-      yv[k] = __ldg(yp);
-      cp += stride;
-      yp += stride;
-    }
+  auto consume = [&](const int (&c)[RU], const YT (&yv)[RU], int i0) {
 #pragma unroll
     for (int k = 0; k < RU; ++k) {
       int cc = c[k];
 #pragma unroll
-      for (int q = 0; q < ND; ++q) cc += sg[q] * inw(r0 + k, D.w[q]);
+      for (int q = 0; q < ND; ++q) cc += sg[q] * inw(base + i0 + k, D.w[q]);
       mx = max(mx, cc);
-      const bool in = (unsigned)(r0 + k - W.lo) < len;
+      const bool in = (unsigned)(i0 + k - sh) < (unsigned)len;
       const int idx = in ? min(cc, TBL - 3) * 4 + code : TBL * 4;
       const double2 e = Ts[idx];
       const double yy = (double)yv[k];
       s += fma(-(yy * yy), e.y, e.x);
     }
+  };
+#if SEIS_BAND_PIPE
+  // two row batches in flight: the next batch's loads are issued before the
+  // current batch is consumed
+  int ca[RU], cb[RU];
+  YT ya[RU], yb[RU];
+#pragma unroll
+  for (int k = 0; k < RU; ++k) {
+    ca[k] = (int)__ldg(cp + k * 32);
+    ya[k] = __ldg(yp + k * 32);
   }
+  for (int i0 = 0;;) {
+    if (i0 + RU < trips) {
+#pragma unroll
+      for (int k = 0; k < RU; ++k) {
+        cb[k] = (int)__ldg(cp + (RU + k) * 32);
+        yb[k] = __ldg(yp + (RU + k) * 32);
+      }
+    }
+    consume(ca, ya, i0);
+    cp += RU * 32;
+    yp += RU * 32;
+    i0 += RU;
+    if (i0 >= trips) break;
+    if (i0 + RU < trips) {
+#pragma unroll
+      for (int k = 0; k < RU; ++k) {
+        ca[k] = (int)__ldg(cp + (RU + k) * 32);
+        ya[k] = __ldg(yp + (RU + k) * 32);
+      }
+    }
+    consume(cb, yb, i0);
+    cp += RU * 32;
+    yp += RU * 32;
+    i0 += RU;
+    if (i0 >= trips) break;
+  }
+#else
+  for (int i0 = 0; i0 < trips; i0 += RU) {
+    int c[RU];
+    YT yv[RU];
+#pragma unroll
+    for (int k = 0; k < RU; ++k) {
+      c[k] = (int)__ldg(cp + k * 32);
+      yv[k] = __ldg(yp + k * 32);
+    }
+    cp += RU * 32;
+    yp += RU * 32;
+    consume(c, yv, i0);
+  }
+#endif
   if (__any_sync(0xffffffffu, mx >= TBL - 3)) {
     s = 0.0;  // slow exact pass with the global table
+    const YT* y0 = reinterpret_cast<const YT*>(d.y) + yix(d.rows, 0, j);
+    const uint16_t* c0 = reinterpret_cast<const uint16_t*>(d.cov) + yix(d.rows, 0, j);
     for (int r = W.lo; r < W.hi; ++r) {
-      const size_t o = (size_t)r * stride + j;
-      int cc = (int)__ldg(reinterpret_cast<const uint16_t*>(d.cov) + o);
+      int cc = (int)__ldg(c0 + r * 32);
 #pragma unroll
       for (int q = 0; q < ND; ++q) cc += sg[q] * inw(r, D.w[q]);
-      s += term(d, Ts, (double)__ldg(reinterpret_cast<const YT*>(d.y) + o), cc, SIGN);
+      s += term(d, Ts, (double)__ldg(y0 + r * 32), cc, SIGN);
     }
   }
   sig += s;
@@ -277,9 +330,9 @@ __device__ __forceinline__ void edges(const Dev& d, int j, Win A0, Win R0, const
   }
   const int total = n1 + n2;
   const int trips = __reduce_max_sync(0xffffffffu, (unsigned)total);
-  const int stride = d.S_pad;
-  const YT* __restrict__ y = reinterpret_cast<const YT*>(d.y) + j;
-  const uint16_t* __restrict__ c16 = reinterpret_cast<const uint16_t*>(d.cov) + j;
+  constexpr int stride = 32;  // next row of the station tile
+  const YT* __restrict__ y = reinterpret_cast<const YT*>(d.y) + yix(d.rows, 0, j);
+  const uint16_t* __restrict__ c16 = reinterpret_cast<const uint16_t*>(d.cov) + yix(d.rows, 0, j);
   double s_loc = 0.0;
   int c_loc = 0;
   bool big = false;
@@ -333,7 +386,7 @@ __device__ __forceinline__ void edges(const Dev& d, int j, Win A0, Win R0, const
 // Many effective diff windows at a station (> 4): the correction of the band
 // rows is accumulated in a per-thread scratch column first (rare).
 template <int NR, int NA, typename YT>
-__device__ __noinline__ void band_generic(const Dev& d, int j, bool v, int blo, int bhi,
+__device__ __forceinline__ void band_generic(const Dev& d, int j, bool v, int blo, int bhi,
                                           const Wins<NR> R, const Wins<NA> A, int np,
                                           const int* pold, const int* pnew,
                                           const double2* Ts, double* out_sig, int* out_cnt) {
@@ -357,7 +410,7 @@ __device__ __noinline__ void band_generic(const Dev& d, int j, bool v, int blo, 
       for (int q = 0; q < NA; ++q) dc += inw(r, A.w[q]);
       for (int q = 0; q < NR; ++q) dc -= inw(r, R.w[q]);
       if (dc) {
-        const size_t off = (size_t)r * d.S_pad + j;
+        const size_t off = yix(d.rows, r, j);
         const int co = (int)__ldg(c16 + off) + corr[r - c0];
         sig += term(d, Ts, (double)__ldg(y + off), co, dc);
         ++cnt;
@@ -427,6 +480,7 @@ __device__ __forceinline__ void station_item(const Dev& d, const Prop& P, const 
                                              int j, int np, const int* pold, const int* pnew,
                                              const DiffW* Xp, const double2* Ts, double& sig,
                                              double& arr, int& cnt) {
+  const long long t_item = kProfItems ? clock64() : 0;
   const bool v = j < d.S;
   Wins<NR> R;
   Wins<NA> A;
@@ -500,12 +554,21 @@ __device__ __forceinline__ void station_item(const Dev& d, const Prop& P, const 
   const Wins<4>& D = X.D;
   const int(&sg)[4] = X.sg;
   const int nwmax = X.nwmax;
+  long long t_band = 0;
+  if (kProfItems && NR + NA == 1) {
+    __syncwarp();
+    t_band = clock64();
+    if ((threadIdx.x & 31) == 0) {
+      atomicAdd(&s_tprof[0][6], (unsigned long long)(t_band - t_item));
+      atomicAdd(&s_tprof[1][6], 1ull);
+    }
+  }
   if (nwmax == 0) {
     Wins<0> D0;
     int sg0[1];
     if (NR + NA == 1) {
       const Win W = NA ? A.w[0] : R.w[0];
-      band1<NA ? 1 : -1, 0, YT>(d, j, blo, bhi, W, D0, sg0, Ts, sig);
+      band1<NA ? 1 : -1, 0, YT>(d, j, W, D0, sg0, Ts, sig);
       cnt += W.hi - W.lo;
     }
     else if (NR == 1 && NA == 1 && P.nr == 1 && P.na == 1)
@@ -522,7 +585,7 @@ __device__ __forceinline__ void station_item(const Dev& d, const Prop& P, const 
     }
     if (NR + NA == 1) {
       const Win W = NA ? A.w[0] : R.w[0];
-      band1<NA ? 1 : -1, 2, YT>(d, j, blo, bhi, W, D2, sg2, Ts, sig);
+      band1<NA ? 1 : -1, 2, YT>(d, j, W, D2, sg2, Ts, sig);
       cnt += W.hi - W.lo;
     }
     else if (NR == 1 && NA == 1 && P.nr == 1 && P.na == 1)
@@ -533,6 +596,13 @@ __device__ __forceinline__ void station_item(const Dev& d, const Prop& P, const 
     band<NR, NA, 4, YT>(d, j, blo, bhi, R, A, D, sg, Ts, sig, cnt);
   } else {
     band_generic<NR, NA, YT>(d, j, v, blo, bhi, R, A, np, pold, pnew, Ts, &sig, &cnt);
+  }
+  if (kProfItems && NR + NA == 1) {
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) {
+      atomicAdd(&s_tprof[0][7], (unsigned long long)(clock64() - t_band));
+      atomicAdd(&s_tprof[1][7], 1ull);
+    }
   }
 }
 
@@ -560,12 +630,12 @@ __device__ __forceinline__ void arrival_item(const Dev& d, const Prop& P, const 
   for (int r = blo + lane; r < bhi; r += 32) {
     const int dc = inw(r, wn) - inw(r, wo);
     if (!dc) continue;
-    int co = (int)c16[(size_t)r * d.S_pad + st];
+    int co = (int)c16[yix(d.rows, r, st)];
     for (int q = 0; q < np; ++q) {
       if (pold[q] >= 0) co -= inw(r, make_win(d, d.pool[(size_t)pold[q] * d.S_pad + st]));
       if (pnew[q] >= 0) co += inw(r, make_win(d, d.pool[(size_t)pnew[q] * d.S_pad + st]));
     }
-    sig += term(d, Ts, (double)y[(size_t)r * d.S_pad + st], co, dc);
+    sig += term(d, Ts, (double)y[yix(d.rows, r, st)], co, dc);
     ++cnt;
   }
 }
@@ -589,8 +659,10 @@ __device__ __forceinline__ void score_item(const Dev& d, const Prop& P, const Pa
     station_item<1, 0, YT>(d, P, in, j, np, pold, pnew, X, Ts, sig, arr, cnt);
   else if (shape == 4)  // location / arrival
     station_item<1, 1, YT>(d, P, in, j, np, pold, pnew, X, Ts, sig, arr, cnt);
+#ifndef SEIS_EXP_NOJOINT
   else  // joint pair, and any other change of <= 2 removed / 2 added events
     station_item<2, 2, YT>(d, P, in, j, np, pold, pnew, X, Ts, sig, arr, cnt);
+#endif
 }
 
 }  // namespace seis
