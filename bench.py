@@ -256,8 +256,15 @@ def main():
     ap.add_argument("--ref-seconds", type=float, default=6.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--k", type=int, default=0,
+                    help="override steps per region per sweep (configs 3/4: the mapped k "
+                         "drives the hypothesis past HBM, see DESIGN.md)")
+    ap.add_argument("--capacity", type=int, default=0, help="event capacity (default 2N + 256)")
     args = ap.parse_args()
-    c = CONFIGS[args.config]
+    c = dict(CONFIGS[args.config])
+    if args.k:
+        c["k_mapped"] = c["k"]
+        c["k"] = args.k
     ws, rank, local, dist = dist_init()
     if args.impl == "reference":
         return run_reference(args, c, ws, rank, dist)
@@ -269,7 +276,7 @@ def main():
     torch.cuda.set_device(local)
     threads = os.cpu_count() or 1
     m, ev, sig = make_world(c, threads)
-    cap = int(max(1024, ev.N * 2 + 256))
+    cap = args.capacity or int(max(1024, ev.N * 2 + 256))
     eng = E.Engine(m, sig, event_capacity=cap)
     truth = E.Events(ev.ids, ev.x, ev.t, ev.arrivals)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
@@ -302,6 +309,7 @@ def main():
             acc["arrvals"] += st["arrival_values"]
             acc["accepted"] += st["total_accepted"]
             acc["spec"] += st["speculative_discarded"]
+            acc["final_events"] = st["final_events"]
     torch.cuda.synchronize()
     barrier(dist)
     t_max = reduce_max(dist, acc["total_ms"])
@@ -322,7 +330,9 @@ def main():
                    "sweeps_per_s": ws * args.steps / (t_max / 1e3),
                    "scored_proposals_per_s": reduce_sum(dist, acc["scored"]) / (t_max / 1e3),
                    "events": int(ev.N), "stations": c["S"], "regions": c["n_regions"],
-                   "k": c["k"], "l2": "flushed between timed sweeps (256 MiB write)",
+                   "k": c["k"], **({"k_mapped": c["k_mapped"]} if "k_mapped" in c else {}),
+                   "final_events": int(acc.get("final_events", 0)),
+                   "l2": "flushed between timed sweeps (256 MiB write)",
                    "sweep_kernel_ms_per_step": acc["sweep_ms"] / args.steps,
                    "acceptance": acc["accepted"] / max(1, acc["steps"]),
                    "speculative_discarded_frac": acc["spec"] / max(1, acc["steps"])},

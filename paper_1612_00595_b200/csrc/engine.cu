@@ -1320,12 +1320,14 @@ __global__ void k_gather_arrivals(const double* pool, const int* slot, int S, in
     out[(size_t)e * S + j] = pool[(size_t)slot[e] * S_pad + j];
 }
 
-__global__ void k_scatter_arrivals(const double* in, const long long* row_of_slot, int S,
-                                   int S_pad, int n, double* pool) {
-  const int slot = blockIdx.y;
-  const double* src = in + (size_t)row_of_slot[slot] * S;
+// input rows [0, gridDim.y) of a chunk -> their pool slots
+__global__ void k_scatter_arrivals(const double* in, const int* slot_of_row, int S, int S_pad,
+                                   double* pool) {
+  const int row = blockIdx.y;
+  const double* src = in + (size_t)row * S;
+  double* dst = pool + (size_t)slot_of_row[row] * S_pad;
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < S_pad; j += gridDim.x * blockDim.x)
-    pool[(size_t)slot * S_pad + j] = j < S ? src[j] : 0.0;
+    dst[j] = j < S ? src[j] : 0.0;
 }
 
 // Trace snapshot (samplers.hpp:430-433): append the event table to the arena
@@ -1643,12 +1645,20 @@ int seis_engine_create(const seis_model_cfg* cfg, const double* stations, int64_
       size_t free_b = 0, total_b = 0;
       ck(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
       const size_t per = (size_t)e->S_pad * 8;
-      const size_t reserve = (size_t)4 << 30;
+      // leave room for the tables, the per-launch scratch and other users
+      const size_t reserve = std::max<size_t>((size_t)6 << 30, total_b / 16);
       const size_t fit = free_b > reserve ? (free_b - reserve) / per : 0;
       const size_t want = 2 * (size_t)e->cap + 2048;
-      e->pool_slots = (int)std::min<size_t>(want, std::max<size_t>(fit, (size_t)e->cap));
+      size_t slots = std::min<size_t>(want, std::max<size_t>(fit, (size_t)e->cap));
+      void* p = nullptr;
+      while (cudaMalloc(&p, slots * per) != cudaSuccess) {
+        (void)cudaGetLastError();
+        if (slots <= (size_t)e->cap) throw std::runtime_error("cudaMalloc: arrival pool out of memory");
+        slots = std::max<size_t>((size_t)e->cap, slots - slots / 8);
+      }
+      e->pool_slots = (int)slots;
+      e->pool = static_cast<double*>(p);
     }
-    e->pool = dalloc<double>((size_t)e->pool_slots * e->S_pad);
     // per-count terms with glibc log, exactly as density.hpp:288-297; counts
     // are uint16 (<= 65535) plus at most 2 * MAXOWN in-phase own versions
     const int tab_n = std::min(e->cap, 65535) + 2 * MAXOWN + 8;
@@ -1792,18 +1802,29 @@ int seis_set_hypothesis(seis_engine* e, int64_t N, const uint64_t* ids, const do
       ck(cudaMemcpy(tb.x, hx.data(), N * 8, cudaMemcpyHostToDevice), "H2D");
       ck(cudaMemcpy(tb.t, ht.data(), N * 8, cudaMemcpyHostToDevice), "H2D");
       ck(cudaMemcpy(tb.slot, hs.data(), N * 4, cudaMemcpyHostToDevice), "H2D");
-      double* raw = dalloc<double>((size_t)N * e->S);
-      long long* drow = dalloc<long long>(N);
-      ck(cudaMemcpyAsync(raw, arrivals, (size_t)N * e->S * 8, cudaMemcpyHostToDevice, e->stream),
-         "H2D arrivals");
-      ck(cudaMemcpyAsync(drow, row.data(), (size_t)N * 8, cudaMemcpyHostToDevice, e->stream),
+      // arrivals in chunks of input rows (<= 512 MiB staging), each row
+      // scattered to its slot
+      std::vector<int> slot_of_row(N);
+      for (int64_t i = 0; i < N; ++i) slot_of_row[row[i]] = (int)i;
+      const int64_t chunk =
+          std::max<int64_t>(1, std::min<int64_t>(N, ((int64_t)512 << 20) / ((int64_t)e->S * 8)));
+      double* raw = dalloc<double>((size_t)chunk * e->S);
+      int* dslot = dalloc<int>(N);
+      ck(cudaMemcpyAsync(dslot, slot_of_row.data(), (size_t)N * 4, cudaMemcpyHostToDevice,
+                         e->stream),
          "H2D");
-      dim3 grid((unsigned)std::min(64, (e->S_pad + 255) / 256), (unsigned)N);
-      k_scatter_arrivals<<<grid, 256, 0, e->stream>>>(raw, drow, e->S, e->S_pad, (int)N, e->pool);
-      ck(cudaGetLastError(), "k_scatter_arrivals");
+      for (int64_t r0 = 0; r0 < N; r0 += chunk) {
+        const int64_t nr = std::min(chunk, N - r0);
+        ck(cudaMemcpyAsync(raw, arrivals + (size_t)r0 * e->S, (size_t)nr * e->S * 8,
+                           cudaMemcpyHostToDevice, e->stream),
+           "H2D arrivals");
+        dim3 grid((unsigned)std::min(64, (e->S_pad + 255) / 256), (unsigned)nr);
+        k_scatter_arrivals<<<grid, 256, 0, e->stream>>>(raw, dslot + r0, e->S, e->S_pad, e->pool);
+        ck(cudaGetLastError(), "k_scatter_arrivals");
+      }
       ck(cudaStreamSynchronize(e->stream), "sync");
       cudaFree(raw);
-      cudaFree(drow);
+      cudaFree(dslot);
     }
     if (nf) ck(cudaMemcpy(e->free_stack, fs.data(), (size_t)nf * 4, cudaMemcpyHostToDevice), "H2D");
     Ctl c{};
@@ -1831,13 +1852,20 @@ int seis_get_hypothesis(seis_engine* e, int64_t cap, int64_t* n, uint64_t* ids, 
     ck(cudaMemcpy(ids, tb.id, m * 8, cudaMemcpyDeviceToHost), "D2H");
     ck(cudaMemcpy(x, tb.x, m * 8, cudaMemcpyDeviceToHost), "D2H");
     ck(cudaMemcpy(t, tb.t, m * 8, cudaMemcpyDeviceToHost), "D2H");
-    if (arrivals) {
-      double* buf = dalloc<double>((size_t)m * e->S);
-      dim3 grid((unsigned)std::min(64, (e->S + 255) / 256), (unsigned)m);
-      k_gather_arrivals<<<grid, 256, 0, e->stream>>>(e->pool, tb.slot, e->S, e->S_pad, (int)m, buf);
-      ck(cudaGetLastError(), "k_gather_arrivals");
-      ck(cudaMemcpyAsync(arrivals, buf, (size_t)m * e->S * 8, cudaMemcpyDeviceToHost, e->stream),
-         "D2H arrivals");
+    if (arrivals) {  // in chunks of <= 512 MiB
+      const int64_t chunk =
+          std::max<int64_t>(1, std::min<int64_t>(m, ((int64_t)512 << 20) / ((int64_t)e->S * 8)));
+      double* buf = dalloc<double>((size_t)chunk * e->S);
+      for (int64_t r0 = 0; r0 < m; r0 += chunk) {
+        const int64_t nr = std::min(chunk, m - r0);
+        dim3 grid((unsigned)std::min(64, (e->S + 255) / 256), (unsigned)nr);
+        k_gather_arrivals<<<grid, 256, 0, e->stream>>>(e->pool, tb.slot + r0, e->S, e->S_pad,
+                                                       (int)nr, buf);
+        ck(cudaGetLastError(), "k_gather_arrivals");
+        ck(cudaMemcpyAsync(arrivals + (size_t)r0 * e->S, buf, (size_t)nr * e->S * 8,
+                           cudaMemcpyDeviceToHost, e->stream),
+           "D2H arrivals");
+      }
       ck(cudaStreamSynchronize(e->stream), "sync");
       cudaFree(buf);
     }

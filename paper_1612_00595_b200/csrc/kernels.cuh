@@ -659,10 +659,8 @@ __device__ __forceinline__ void score_item(const Dev& d, const Prop& P, const Pa
     station_item<1, 0, YT>(d, P, in, j, np, pold, pnew, X, Ts, sig, arr, cnt);
   else if (shape == 4)  // location / arrival
     station_item<1, 1, YT>(d, P, in, j, np, pold, pnew, X, Ts, sig, arr, cnt);
-#ifndef SEIS_EXP_NOJOINT
   else  // joint pair, and any other change of <= 2 removed / 2 added events
     station_item<2, 2, YT>(d, P, in, j, np, pold, pnew, X, Ts, sig, arr, cnt);
-#endif
 }
 
 }  // namespace seis
