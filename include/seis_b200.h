@@ -205,6 +205,31 @@ int seis_thomas_events(uint64_t seed, double x_max, double T, double parent_mean
                        double child_mean, double sx, double st, int64_t cap, int64_t* n,
                        double* cx, double* ct);
 
+/* ---- evaluation bridge (evaluation.hpp:51-171): greedy event matching and
+ * the percentile bootstrap, host C++, bit-exact with the reference. Feeds on
+ * seis_get_hypothesis / seis_get_snapshots output. Errors: status 2 with the
+ * message in seis_eval_last_error(). Not on the hot path. */
+typedef struct {
+  double precision, recall, location_error;
+  int64_t n_true, n_inferred, n_matched;
+} seis_match_report;
+
+typedef struct {
+  double mean, lo, hi, level;
+  int32_t resamples;
+} seis_ci;
+
+const char* seis_eval_last_error(void);
+/* pair_* (capacity min(n_true, n_inf), may be NULL): matched pairs in truth
+ * (t, x) order. */
+int seis_match_events(int64_t n_true, const uint64_t* true_id, const double* true_x,
+                      const double* true_t, int64_t n_inf, const uint64_t* inf_id,
+                      const double* inf_x, const double* inf_t, double threshold,
+                      seis_match_report* report, uint64_t* pair_true_id,
+                      uint64_t* pair_inf_id, double* pair_dist);
+int seis_bootstrap_ci(const double* values, int64_t n, double level, int32_t resamples,
+                      uint64_t seed, seis_ci* out);
+
 #ifdef __cplusplus
 }
 #endif

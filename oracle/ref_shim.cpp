@@ -667,4 +667,16 @@ int sr_match_events(int64_t nt, const uint64_t* tid, const double* tx, const dou
   });
 }
 
+int sr_bootstrap_ci(const double* values, int64_t n, double level, int32_t resamples,
+                    uint64_t seed, double* out) {
+  return guarded([&] {
+    const std::vector<double> v(values, values + n);
+    const BootstrapCI ci = bootstrap_ci(v, level, resamples, seed);
+    out[0] = ci.mean;
+    out[1] = ci.lo;
+    out[2] = ci.hi;
+    out[3] = ci.level;
+  });
+}
+
 }  // extern "C"

@@ -17,7 +17,8 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(LIBDIR, "libseis_b200.so")
-SOURCES = [os.path.join(CSRC, "engine.cu"), os.path.join(CSRC, "worldgen.cpp")]
+SOURCES = [os.path.join(CSRC, "engine.cu"), os.path.join(CSRC, "worldgen.cpp"),
+           os.path.join(CSRC, "evaluation.cpp")]
 DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("engine.cuh", "kernels.cuh")] + [
     os.path.join(ROOT, "include", f) for f in ("seis_b200.h", "seis_philox.h")]
 

@@ -67,7 +67,8 @@ EXPORTS = ("seis_last_error", "seis_engine_create", "seis_engine_destroy", "seis
            "seis_partition_offset", "seis_score_batch", "seis_log_joint", "seis_run_chromatic",
            "seis_world_last_error", "seis_world_generate", "seis_world_with_events",
            "seis_thomas_events", "seis_set_snapshot_capacity", "seis_get_snapshots",
-           "seis_run_naive", "seis_engine_pool_slots")
+           "seis_run_naive", "seis_engine_pool_slots", "seis_eval_last_error",
+           "seis_match_events", "seis_bootstrap_ci")
 
 _LIB = None
 
@@ -101,6 +102,9 @@ def load_library(path: str | None = None) -> C.CDLL:
     L.seis_world_generate.argtypes = [P, P, i64, u64, i64, P, P, P, P, P, P, i32, i32]
     L.seis_world_with_events.argtypes = [P, P, i64, i64, P, P, u64, P, P, i32, i32]
     L.seis_thomas_events.argtypes = [u64, f64, f64, f64, f64, f64, f64, i64, P, P, P]
+    L.seis_eval_last_error.restype = C.c_char_p
+    L.seis_match_events.argtypes = [i64, P, P, P, i64, P, P, P, f64, P, P, P, P]
+    L.seis_bootstrap_ci.argtypes = [P, i64, f64, i32, u64, P]
     L.seis_set_snapshot_capacity.argtypes = [P, i64, i64]
     L.seis_get_snapshots.argtypes = [P, i64, P, P, P, i64, P, P, P]
     if path == _build.LIB:
@@ -339,6 +343,93 @@ def thomas_events(seed, x_max, T, parent_mean, child_mean, sx, st, cap=1 << 22):
     if rc:
         raise RuntimeError(L.seis_world_last_error().decode())
     return cx[:n.value].copy(), ct[:n.value].copy()
+
+
+# ---------------------------------------------------------------- evaluation
+class _MatchC(C.Structure):
+    _fields_ = [("precision", f64), ("recall", f64), ("location_error", f64),
+                ("n_true", i64), ("n_inferred", i64), ("n_matched", i64)]
+
+
+class _CIC(C.Structure):
+    _fields_ = [("mean", f64), ("lo", f64), ("hi", f64), ("level", f64), ("resamples", i32)]
+
+
+@dataclass
+class MatchReport:
+    """reference MatchReport (evaluation.hpp:35-43); pairs in truth (t, x) order."""
+    precision: float
+    recall: float
+    location_error: float
+    n_true: int
+    n_inferred: int
+    n_matched: int
+    pair_true_id: np.ndarray
+    pair_inferred_id: np.ndarray
+    pair_distance: np.ndarray
+
+
+@dataclass
+class BootstrapCI:
+    """reference BootstrapCI (evaluation.hpp:128-134)."""
+    mean: float
+    lo: float
+    hi: float
+    level: float
+    resamples: int
+
+
+def _points(ev):
+    ids = np.ascontiguousarray(ev.ids, np.uint64)
+    return ids, np.ascontiguousarray(ev.x, np.float64), np.ascontiguousarray(ev.t, np.float64)
+
+
+def _eval_check(rc, L):
+    if rc == 2:
+        raise ValueError(L.seis_eval_last_error().decode())
+    if rc:
+        raise RuntimeError(L.seis_eval_last_error().decode())
+
+
+def match_events(true_events, inferred_events, threshold: float = 12.0) -> MatchReport:
+    """match_events (evaluation.hpp:51-105): greedy nearest matching in (x, t),
+    pairs within `threshold` in both |dt| and |dx|. Accepts anything with
+    ids/x/t (Events, Snapshot)."""
+    L = load_library()
+    ti, tx, tt = _points(true_events)
+    ii, ix, it = _points(inferred_events)
+    k = max(1, min(len(ti), len(ii)))
+    pt, pi, pd = np.zeros(k, np.uint64), np.zeros(k, np.uint64), np.zeros(k)
+    r = _MatchC()
+    _eval_check(L.seis_match_events(len(ti), _p(ti), _p(tx), _p(tt), len(ii), _p(ii), _p(ix),
+                                    _p(it), float(threshold), C.byref(r), _p(pt), _p(pi),
+                                    _p(pd)), L)
+    m = r.n_matched
+    return MatchReport(r.precision, r.recall, r.location_error, r.n_true, r.n_inferred, m,
+                       pt[:m].copy(), pi[:m].copy(), pd[:m].copy())
+
+
+def metric_trace(snapshots, true_events, threshold: float = 12.0) -> list:
+    """metric_trace (evaluation.hpp:115-126): (snapshot id, precision, recall,
+    location error) per snapshot (no wall-clock column, see Trace)."""
+    if not snapshots:
+        raise ValueError("metric_trace: no snapshots")
+    out = []
+    for sn in snapshots:
+        r = match_events(true_events, sn, threshold)
+        out.append((sn.id, r.precision, r.recall, r.location_error))
+    return out
+
+
+def bootstrap_ci(values, level: float = 0.95, resamples: int = 1000, seed: int = 0) -> BootstrapCI:
+    """bootstrap_ci (evaluation.hpp:136-169): percentile bootstrap of the mean
+    on the reference's kBootstrap stream (bit-exact)."""
+    L = load_library()
+    v = np.ascontiguousarray(values, np.float64)
+    out = _CIC()
+    _eval_check(L.seis_bootstrap_ci(_p(v), len(v), float(level), int(resamples), int(seed),
+                                    C.byref(out)), L)
+    return BootstrapCI(out.mean, out.lo, out.hi, out.level, out.resamples)
 
 
 class Engine:

@@ -4,6 +4,7 @@ import re
 import os
 
 import numpy as np
+import pytest
 
 from oracle import oracle as O
 from tests.helpers import default_model, engine_model, golden_world, wide_model
@@ -68,3 +69,34 @@ def test_engine_fails_loudly_without_gpu(built):
         assert "CUDA" in str(e) or "device" in str(e)
     else:
         raise AssertionError("engine constructed without a GPU")
+
+
+def test_evaluation_bridge_bit_exact_vs_reference(built):
+    """match_events / bootstrap_ci (evaluation.hpp:51-171) through the C-ABI
+    against the reference's own outputs (tests/golden/make_golden_eval.py)."""
+    import paper_1612_00595_b200 as E
+    from tests.helpers import golden
+    g = golden("eval.npz")
+    for i, (thr, pr, rc, le, nm) in enumerate(g["match"]):
+        T = E.Events(g[f"m{i}_ti"], g[f"m{i}_tx"], g[f"m{i}_tt"], np.zeros((len(g[f"m{i}_ti"]), 1)))
+        I = E.Events(g[f"m{i}_ii"], g[f"m{i}_ix"], g[f"m{i}_it"], np.zeros((len(g[f"m{i}_ii"]), 1)))
+        r = E.match_events(T, I, thr)
+        assert (r.precision, r.recall, r.location_error, r.n_matched) == (pr, rc, le, int(nm)), i
+        assert r.n_true == len(T.ids) and r.n_inferred == len(I.ids)
+        assert len(set(r.pair_inferred_id.tolist())) == r.n_matched  # degrees <= 1
+        if r.n_matched:
+            assert abs(r.pair_distance.mean() - r.location_error) <= 1e-12 * max(1.0, le)
+    for i, row in enumerate(g["boot"]):
+        level, res = row[0], int(row[1])
+        ci = E.bootstrap_ci(g[f"b{i}_v"], level, res, int(g["boot_seed"][i]))
+        assert (ci.mean, ci.lo, ci.hi, ci.level) == tuple(row[3:7]), i
+    with pytest.raises(ValueError):
+        E.bootstrap_ci([], 0.95, 10, 0)
+    with pytest.raises(ValueError):
+        E.bootstrap_ci([1.0], 1.5, 10, 0)
+    with pytest.raises(ValueError):
+        E.match_events(T, I, 0.0)
+    # vacuous conventions (evaluation.hpp:46-49)
+    empty = E.Events(np.zeros(0, np.uint64), np.zeros(0), np.zeros(0), np.zeros((0, 1)))
+    r = E.match_events(empty, empty)
+    assert (r.precision, r.recall, r.location_error) == (1.0, 1.0, 0.0)
