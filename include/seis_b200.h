@@ -177,6 +177,18 @@ int seis_run_chromatic(seis_engine* eng, const seis_sampler_cfg* sc, int32_t mod
                        int64_t* row_step, double* row_log_joint, int64_t* row_count,
                        seis_run_stats* stats);
 
+/* run_serial (samplers.hpp:282-315): plain MH over [0, T] (no region
+ * constraint, full window, area T), epochs x steps_per_epoch steps from the
+ * resident hypothesis (the reference starts empty), a trace row + snapshot
+ * after every record_every steps. Same arguments as seis_run_chromatic
+ * (n_regions, dynamic ignored); production draws follow the philox spec with
+ * sweep = region = 0 and the chain step as the step counter. */
+int seis_run_serial(seis_engine* eng, const seis_sampler_cfg* sc, int32_t mode,
+                    const seis_tape_step* tape, int64_t n_tape, const double* tape_arr,
+                    int64_t n_tape_arr, seis_step_out* step_out, int64_t row_cap,
+                    int64_t* row_step, double* row_log_joint, int64_t* row_count,
+                    seis_run_stats* stats);
+
 /* run_naive_parallel (samplers.hpp:321-394), the uncolored comparison
  * sampler: every region runs epochs x steps_per_epoch steps from the empty
  * hypothesis (the engine's must be empty) against its own events only, prior

@@ -181,6 +181,9 @@ class Oracle:
         self._naive = g("run_naive")
         self._naive.restype = P
         self._naive.argtypes = [P, P, P, i64, i64]
+        self._serial = g("run_serial")
+        self._serial.restype = P
+        self._serial.argtypes = [P, P, P, i64, i64]
         for n in ("run_status",):
             getattr(L, pre + n).argtypes = [P]
         g("run_counts").argtypes = [P] + [P] * 6
@@ -308,7 +311,8 @@ class Oracle:
 
     # -- samplers.hpp
     def run_chromatic(self, world: World, sampler: Sampler, init: Events | None = None,
-                      tape: bool = True, rowlj: bool = False, naive: bool = False) -> dict:
+                      tape: bool = True, rowlj: bool = False, naive: bool = False,
+                      serial: bool = False) -> dict:
         model = world.model
         m = model.c()
         s = sampler.c()
@@ -322,6 +326,8 @@ class Oracle:
         pre = self.pre
         if naive:
             h = self._naive(C.byref(m), _p(sig), C.byref(s), int(tape), int(rowlj))
+        elif serial:
+            h = self._serial(C.byref(m), _p(sig), C.byref(s), int(tape), int(rowlj))
         else:
             h = self._run(C.byref(m), _p(sig), C.byref(s), init.N, _p(ids), _p(x), _p(t),
                           _p(arr), int(tape), int(rowlj))
@@ -358,12 +364,13 @@ def have_ref() -> bool:
 
 
 def ref_run_sampler(world: World, sampler: Sampler, workers: int = 1, cap: int = 1 << 16,
-                    naive: bool = False):
-    """The reference's own run_sampler (chromatic static/dynamic, or naive, from empty)."""
-    if naive:
+                    naive: bool = False, serial: bool = False):
+    """The reference's own run_sampler (chromatic static/dynamic, naive or
+    serial, from empty)."""
+    if naive or serial:
         import copy
         sampler = copy.copy(sampler)
-        sampler.dynamic = 2
+        sampler.dynamic = 2 if naive else 3
     L = C.CDLL(REF_SO)
     f = L.sr_run_sampler
     f.argtypes = [P, P, P, i64, i64, P, P, P, P, P, P, P, P]

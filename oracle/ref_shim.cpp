@@ -534,6 +534,95 @@ sr_run* sr_run_naive(const so_model* mm, const double* signals, const so_sampler
   return run;
 }
 
+// run_serial (samplers.hpp:282-315) with every step taped (mh_step without a
+// constraint, proposals.hpp:265-293).
+sr_run* sr_run_serial(const so_model* mm, const double* signals, const so_sampler* s,
+                      int64_t want_tape, int64_t want_rowlj) {
+  auto* run = new sr_run;
+  run->status = guarded([&] {
+    if (s->rng_mode != 0) throw std::invalid_argument("reference supports rng_mode 0 only");
+    const ModelConfig config = to_config(mm);
+    SamplerConfig sc = to_sampler(s);
+    sc.algorithm = Algorithm::Serial;
+    config.validate();
+    sc.validate();
+    run->S = config.n_stations();
+    const ObservedSignals sig = to_signals(config, signals);
+    World world{config, {}, sig};
+    const TimeRegion region = config.full_region();
+    const ScoreOptions opts = default_score_options(config);
+    const std::int64_t total = sc.epochs * sc.steps_per_epoch;
+    Rng rng = derive_stream(sc.seed, streams::kChain, 0, 0, 0);
+    run->row_step.push_back(0);
+    run->row_lj.push_back(want_rowlj ? log_joint(world) : 0.0);
+    run->row_count.push_back(0);
+    std::uint64_t id_base = 0;
+    std::int64_t done = 0;
+    while (done < total) {
+      const std::int64_t chunk = std::min(sc.record_every, total - done);
+      std::int64_t births = 0;
+      for (std::int64_t i = 0; i < chunk; ++i) {
+        const MoveType type = sc.moves.sample(rng);
+        const Proposal p = propose_move(type, region, world.events, config, sc.moves,
+                                        sc.step_sizes, id_base + static_cast<std::uint64_t>(births),
+                                        rng);
+        so_tape_rec rec{};
+        rec.step = done + i;
+        rec.type = static_cast<int64_t>(p.type);
+        rec.is_null = p.null;
+        rec.n_removed = static_cast<int64_t>(p.change.removed.size());
+        rec.n_added = static_cast<int64_t>(p.change.added.size());
+        for (std::size_t r = 0; r < p.change.removed.size(); ++r)
+          rec.removed_id[r] = p.change.removed[r].id;
+        for (std::size_t a = 0; a < p.change.added.size(); ++a) {
+          rec.added_id[a] = p.change.added[a].id;
+          rec.added_x[a] = p.change.added[a].x;
+          rec.added_t[a] = p.change.added[a].t;
+          if (want_tape) {
+            if (a == 0) rec.added_arr_off = static_cast<int64_t>(run->tarr.size());
+            run->tarr.insert(run->tarr.end(), p.change.added[a].arrivals.begin(),
+                             p.change.added[a].arrivals.end());
+          }
+        }
+        rec.logq_f = p.log_q_forward;
+        rec.logq_r = p.log_q_reverse;
+        rec.delta = kLogZero;
+        bool acc = false;
+        if (!p.null) {
+          rec.delta = delta_log_joint(world, p.change, opts);
+          const double log_r = log_accept_ratio(rec.delta, p);
+          rec.scored = 1;
+          rec.log_r = log_r;
+          if (log_r >= 0.0) {
+            acc = true;
+          } else {
+            const double u = rng.uniform();
+            rec.u_drawn = 1;
+            rec.u = u;
+            acc = std::log(u) < log_r;
+          }
+          if (acc) apply_change(world, p.change);
+        }
+        rec.accepted = acc;
+        if (acc) {
+          ++run->total_accepted;
+          if (p.type == MoveType::Birth) ++births;
+        }
+        if (want_tape) run->tape.push_back(rec);
+      }
+      id_base += static_cast<std::uint64_t>(births);
+      done += chunk;
+      run->row_step.push_back(done);
+      run->row_lj.push_back(want_rowlj ? log_joint(world) : 0.0);
+      run->row_count.push_back(static_cast<int64_t>(world.events.size()));
+    }
+    run->final = world.events;
+    detail::sort_by_id(run->final);
+    run->total_steps = total;
+  });
+  return run;
+}
+
 int sr_run_status(const sr_run* r) { return r->status; }
 
 void sr_run_counts(const sr_run* r, int64_t* n_tape, int64_t* n_tape_arr, int64_t* n_rows,
@@ -580,6 +669,7 @@ int sr_run_sampler(const so_model* mm, const double* signals, const so_sampler* 
     const ModelConfig config = to_config(mm);
     SamplerConfig sc = to_sampler(s);
     if (s->dynamic == 2) sc.algorithm = Algorithm::NaiveParallel;
+    if (s->dynamic == 3) sc.algorithm = Algorithm::Serial;
     sc.workers = static_cast<int>(workers);
     const ObservedSignals sig = to_signals(config, signals);
     const auto t0 = std::chrono::steady_clock::now();

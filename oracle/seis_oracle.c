@@ -675,6 +675,7 @@ typedef struct {
   int64_t wlo, whi;
   double slo, shi;
   int sclosed;
+  int unconstrained; /* run_serial: no region constraint (samplers.hpp:300) */
 } chain_t;
 
 /* proposals.hpp:65-71 */
@@ -920,7 +921,7 @@ static int64_t run_region_steps(struct so_run* run, chain_t* c, evlist_t* local,
     int acc = 0;
     if (!p.is_null) {
       int constrained_out = 0;
-      for (int a = 0; a < p.n_added; ++a)
+      for (int a = 0; a < p.n_added && !c->unconstrained; ++a)
         if (!region_contains(c->rlo, c->rhi, c->rclosed, p.added[a].t)) {
           constrained_out = 1;
           break;
@@ -1376,4 +1377,71 @@ int so_match_events(int64_t nt, const uint64_t* tid, const double* tx, const dou
   free(I);
   free(taken);
   return SO_OK;
+}
+
+
+/* run_serial, samplers.hpp:282-315: one chain over config.full_region()
+ * without the region constraint, default ScoreOptions (full window, [0, T]),
+ * stream derive_stream(seed, kChain, 0, 0, 0) in rng_mode 0 and philox
+ * (sweep 0, region 0, chain step) in rng_mode 1; a trace row after every
+ * record_every steps. The final list is returned sorted by id (the engine's
+ * order; the reference keeps list order, a permutation of it). */
+so_run* so_run_serial(const so_model* m, const double* signals, const so_sampler* sc,
+                      int64_t want_tape, int64_t want_rowlj) {
+  struct so_run* run = (struct so_run*)calloc(1, sizeof(struct so_run));
+  const int64_t S = m->n_stations;
+  run->S = S;
+  int rc = so_validate_model(m);
+  if (rc) {
+    run->status = rc;
+    return run;
+  }
+  if (sc->steps_per_epoch < 1 || sc->epochs < 1 || sc->n_regions < 1 || sc->record_every < 1 ||
+      sc->burn_in_fraction < 0 || sc->burn_in_fraction >= 1) {
+    run->status = fail(SO_EINVAL, "SamplerConfig: invalid");
+    return run;
+  }
+  chain_t c;
+  memset(&c, 0, sizeof c);
+  c.m = m;
+  c.sc = sc;
+  c.rlo = 0.0;
+  c.rhi = m->T;
+  c.rclosed = 1;
+  c.unconstrained = 1;
+  c.wlo = 0;
+  c.whi = so_n_samples(m);
+  c.slo = 0.0;
+  c.shi = m->T;
+  c.sclosed = 1;
+  if (sc->rng_mode == 0) c.rng = so_derive_stream(sc->seed, 5, 0, 0, 0);
+  const int64_t total = sc->epochs * sc->steps_per_epoch;
+  flat_t flat = {0, 0, 0, 0, 0};
+  int64_t* idxbuf = (int64_t*)malloc(sizeof(int64_t) * (size_t)(total + 16));
+  evlist_t local = {0, 0, 0};
+  uint64_t id_base = 0;
+  int64_t done = 0;
+  run_push_row(run, 0, 0.0, 0); /* log_joint(empty world) */
+  if (want_rowlj) run->row_lj[0] = so_log_joint(m, signals, 0, NULL, NULL, NULL, NULL);
+  while (done < total) {
+    const int64_t chunk = sc->record_every < total - done ? sc->record_every : total - done;
+    c.step_base = (uint32_t)done;
+    int64_t births = 0;
+    run->total_accepted += run_region_steps(run, &c, &local, signals, chunk, id_base,
+                                            (int)want_tape, 0, 0, 0, &flat, idxbuf, &births);
+    id_base += (uint64_t)births;
+    done += chunk;
+    double lj = 0.0;
+    if (want_rowlj) {
+      flat_fill(&flat, &local, S);
+      lj = so_log_joint(m, signals, local.n, flat.ids, flat.x, flat.t, flat.arr);
+    }
+    run_push_row(run, done, lj, local.n);
+  }
+  qsort(local.e, (size_t)local.n, sizeof(ev_t), cmp_id);
+  run->final = local;
+  run->total_steps = total;
+  free(idxbuf);
+  flat_free(&flat);
+  return run;
 }

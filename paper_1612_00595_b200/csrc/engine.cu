@@ -325,12 +325,13 @@ __device__ void gen_proposal(const Dev& d, const Samp& sp, const PhaseArgs& pa, 
     P.rx[q] = e.x;
     P.rt[q] = e.t;
   }
-  // mh_step constraint (proposals.hpp:269-282), then delta_log_joint's
-  // support check (density.hpp:218-221)
-  for (int a = 0; a < P.na; ++a) {
-    const double t = P.at[a];
-    if (!(t >= rlo && (t < rhi || (rclosed && t == rhi)))) P.skip = 1;
-  }
+  // mh_step constraint (proposals.hpp:269-282; none in run_serial,
+  // samplers.hpp:300), then delta_log_joint's support check (density.hpp:218-221)
+  if (!pa.serial)
+    for (int a = 0; a < P.na; ++a) {
+      const double t = P.at[a];
+      if (!(t >= rlo && (t < rhi || (rclosed && t == rhi)))) P.skip = 1;
+    }
   if (P.skip) return;
   P.scored = 1;
   // support: [0, T] closed in chromatic mode, the region in naive mode
@@ -442,6 +443,25 @@ __global__ void __launch_bounds__(NTT, MINB)
     if (tid == 0) atomicExch(&ctl->err, ERR_OWN_OVERFLOW);
     return;
   }
+  // run_serial keeps the chain's list order (erase + push_back) across its
+  // chunks (samplers.hpp:299-303); the table is in id order, so the previous
+  // chunk's order is restored here
+  if (pa.order_io && tid == 0) {
+    const long long cnt = (long long)pa.order_io[0];
+    if (cnt >= 0 && cnt == s_nown) {
+      for (int i = 0; i < cnt; ++i) {
+        const unsigned long long want = pa.order_io[1 + i];
+        int f = i;
+        while (f < s_nown && own[f].id != want) ++f;
+        if (f < s_nown && f != i) {
+          const OwnEv tmp = own[f];
+          own[f] = own[i];
+          own[i] = tmp;
+        }
+      }
+    }
+  }
+  __syncthreads();
   const int nstart = s_nown;
   // thread-0 chain state (mirrored in shared memory for the generators)
   // thread-0 chain state lives in shared memory: registers are allocated for
@@ -507,8 +527,9 @@ __global__ void __launch_bounds__(NTT, MINB)
     if (warp < m && lane == 0) {  // one lane per warp: move types do not diverge
       const int step = i0 + warp;
       gen_proposal<MODE>(d, sp, pa, prop[buf][warp], own, s_nown, region, rlo, rhi, rclosed,
-                         step, pa.tape_base + (long long)slot_idx * sp.k + step,
-                         id_base + s_births, &ctl->err);
+                         (int)(pa.step_base + step),
+                         pa.tape_base + (long long)slot_idx * sp.k + step, id_base + s_births,
+                         &ctl->err);
     }
     if (lane < MSPEC) {
       red_sig[warp][lane] = 0.0;
@@ -561,7 +582,7 @@ __global__ void __launch_bounds__(NTT, MINB)
             in.seed = sp.seed;
             in.sweep = (uint32_t)pa.epoch;
             in.region = (uint32_t)region;
-            in.step = (uint32_t)(i0 + q);
+            in.step = (uint32_t)(pa.step_base + i0 + q);
             in.wlo = win_lo;
             in.whi = win_hi;
             double sig = 0.0, arr = 0.0;
@@ -630,7 +651,7 @@ __global__ void __launch_bounds__(NTT, MINB)
           in.seed = sp.seed;
           in.sweep = (uint32_t)pa.epoch;
           in.region = (uint32_t)region;
-          in.step = (uint32_t)(i0 + q);
+          in.step = (uint32_t)(pa.step_base + i0 + q);
           in.wlo = win_lo;
           in.whi = win_hi;
           score_item<MODE, YT>(d, P, in, tile, np_now, pold, pnew, nullptr, Ts, sig, arr, cnt);
@@ -875,7 +896,7 @@ __global__ void __launch_bounds__(NTT, MINB)
     if (accq >= 0) {
       // write the accepted version's arrivals (recomputed exactly as scored)
       const Prop& P = prop[buf][accq];
-      const int step = i0 + accq;
+      const int step = (int)(pa.step_base + i0 + accq);  // chain step (philox counter)
       double2* pool2 = reinterpret_cast<double2*>(d.pool);
       const double2* st2 = reinterpret_cast<const double2*>(d.stations);
       if (MODE == 0 && P.type == 3) {
@@ -960,6 +981,11 @@ __global__ void __launch_bounds__(NTT, MINB)
         bo[q] = e;
       }
     pa.births_cnt[slot_idx] = nb;
+    if (pa.births_total) pa.births_total[slot_idx] = (int)births;
+    if (pa.order_io) {
+      pa.order_io[0] = (unsigned long long)nown;
+      for (int j = 0; j < nown; ++j) pa.order_io[1 + j] = own[j].id;
+    }
     // coverage diff for the commit, then this-phase versions that died (sign
     // 0): k_commit returns those slots to the pool, after every CTA of this
     // phase has stopped popping from it
@@ -2078,12 +2104,14 @@ int seis_log_joint(seis_engine* e, double* out) {
 
 }  // extern "C"
 
-extern "C" int seis_run_chromatic(seis_engine* e, const seis_sampler_cfg* sc, int32_t mode,
-                                  const seis_tape_step* tape, int64_t n_tape,
-                                  const double* tape_arr, int64_t n_tape_arr,
-                                  seis_step_out* step_out, int64_t row_cap, int64_t* row_step,
-                                  double* row_log_joint, int64_t* row_count,
-                                  seis_run_stats* stats) {
+// The chromatic driver (run_chromatic, samplers.hpp:401-498) and, with
+// serial = true, run_serial (samplers.hpp:282-315): one region [0, T], no
+// constraint, chunks of record_every steps.
+static int run_driver(seis_engine* e, const seis_sampler_cfg* sc, int32_t mode,
+                      const seis_tape_step* tape, int64_t n_tape, const double* tape_arr,
+                      int64_t n_tape_arr, seis_step_out* step_out, int64_t row_cap,
+                      int64_t* row_step, double* row_log_joint, int64_t* row_count,
+                      seis_run_stats* stats, bool serial) {
   std::vector<void*> tmp;
   std::vector<cudaEvent_t> evs;
   auto alloc = [&](size_t bytes) {
@@ -2114,10 +2142,12 @@ extern "C" int seis_run_chromatic(seis_engine* e, const seis_sampler_cfg* sc, in
     if (mode == 1 && (!tape || !step_out)) throw std::invalid_argument("replay needs a tape");
     // run_chromatic setup (samplers.hpp:405-407)
     const double tau = e->cfg.x_max / e->cfg.v;
-    const double l = e->cfg.T / (double)sc->n_regions;
+    const double l = serial ? e->cfg.T : e->cfg.T / (double)sc->n_regions;
     if (l > e->cfg.T) throw std::invalid_argument("build_partition: need 0 < l <= T");
-    int ncol;
-    if (l >= tau)
+    int ncol = 1;
+    if (serial)
+      ncol = 1;
+    else if (l >= tau)
       ncol = 2;
     else if (l >= tau / 2)
       ncol = 3;
@@ -2143,12 +2173,16 @@ extern "C" int seis_run_chromatic(seis_engine* e, const seis_sampler_cfg* sc, in
     const int bcap = (int)sc->n_regions + 4;
     // every epoch's partition up front (one thread per epoch), so the timed
     // region holds no host round trip
-    const int64_t n_ep = sc->dynamic ? sc->epochs : 1;
+    const int64_t n_ep = (sc->dynamic && !serial) ? sc->epochs : 1;
     double* bnd = static_cast<double*>(alloc((size_t)n_ep * bcap * 8));
     int* nreg_d = static_cast<int*>(alloc((size_t)n_ep * 4));
     int* perr = static_cast<int*>(alloc(4));
     std::vector<int> h_nreg(n_ep);
-    {
+    if (serial) {  // config.full_region() (model.hpp:109)
+      const double hb[2] = {0.0, e->cfg.T};
+      ck(cudaMemcpy(bnd, hb, sizeof hb, cudaMemcpyHostToDevice), "H2D");
+      h_nreg[0] = 1;
+    } else {
       ck(cudaMemsetAsync(perr, 0, 4, e->stream), "memset");
       k_partition<<<(unsigned)((n_ep + 63) / 64), 64, 0, e->stream>>>(
           e->cfg.T, l, tau, ncol, sc->dynamic ? 1 : 0, sc->seed, 0, (int)n_ep, 0.0, bcap, bnd,
@@ -2163,8 +2197,16 @@ extern "C" int seis_run_chromatic(seis_engine* e, const seis_sampler_cfg* sc, in
       if (herr == 1) throw std::logic_error("color_partition: separation invariant violated");
       if (herr == 2) throw std::runtime_error("partition capacity");
     }
-    const int n_slots = (int)((sc->n_regions + 1 + ncol - 1) / ncol) + 1;
+    const int n_slots = serial ? 1 : (int)((sc->n_regions + 1 + ncol - 1) / ncol) + 1;
     int* births_cnt = static_cast<int*>(alloc((size_t)n_slots * 4));
+    int* births_total = static_cast<int*>(alloc((size_t)n_slots * 4));
+    // serial: the chain's list order between chunks ([0] = count, -1 = none yet)
+    unsigned long long* order_io = nullptr;
+    if (serial) {
+      order_io = static_cast<unsigned long long*>(alloc((MAXOWN + 1) * 8));
+      const unsigned long long none = ~0ull;
+      ck(cudaMemcpy(order_io, &none, 8, cudaMemcpyHostToDevice), "H2D");
+    }
     OutEv* births = static_cast<OutEv*>(alloc((size_t)n_slots * MAXOWN * sizeof(OutEv)));
     int* diff_cnt = static_cast<int*>(alloc((size_t)n_slots * 4));
     DiffPair* diff = static_cast<DiffPair*>(alloc((size_t)n_slots * MAXDOUT * sizeof(DiffPair)));
@@ -2208,7 +2250,7 @@ extern "C" int seis_run_chromatic(seis_engine* e, const seis_sampler_cfg* sc, in
     int64_t n_rows = 0;
     std::vector<int64_t> h_row_step;
     // snapshots at record points once executed >= burn (samplers.hpp:411-413,430-433)
-    const int64_t planned = sc->epochs * sc->steps_per_epoch * sc->n_regions;
+    const int64_t planned = sc->epochs * sc->steps_per_epoch * (serial ? 1 : sc->n_regions);
     const int64_t burn = (int64_t)(sc->burn_in_fraction * (double)planned);
     e->snap_steps.clear();
     if (e->snap_cap > 0) {
@@ -2241,69 +2283,97 @@ extern "C" int seis_run_chromatic(seis_engine* e, const seis_sampler_cfg* sc, in
     record_row(0);
     int64_t executed = 0, last_recorded = 0;
     long long tape_base = 0;
-    const int64_t k = sc->steps_per_epoch;
-    {
+    // one color phase: ncr same-colored regions x kk steps, then the barrier
+    auto run_phase = [&](int epoch, int color, int nreg, int ncr, const double* bndp, int64_t kk,
+                         long long step_base) {
+      PhaseArgs pa{};
+      pa.epoch = epoch;
+      pa.color = color;
+      pa.nreg = nreg;
+      pa.n_slots = ncr;
+      pa.bnd = bndp;
+      pa.next_base = next_base;
+      pa.tape_base = tape_base;
+      pa.tab = e->tab[e->cur];
+      pa.fate_stamp = e->fate_stamp;
+      pa.fate_alive = e->fate_alive;
+      pa.fate_x = e->fate_x;
+      pa.fate_t = e->fate_t;
+      pa.fate_slot = e->fate_slot;
+      pa.births_cnt = births_cnt;
+      pa.births = births;
+      pa.diff_cnt = diff_cnt;
+      pa.diff = diff;
+      pa.free_stack = e->free_stack;
+      pa.tape = d_tape;
+      pa.tape_arr = d_tarr;
+      pa.out = d_out;
+      pa.serial = serial ? 1 : 0;
+      pa.step_base = step_base;
+      pa.births_total = births_total;
+      pa.order_io = serial ? order_io : nullptr;
+      Samp spk = sp;
+      spk.k = kk;
+      const int stamp = ++e->stamp;
+      if ((mode == 1 || d_out) && tape_base + (long long)ncr * kk > n_tape)
+        throw std::invalid_argument(mode == 1 ? "replay tape shorter than the run"
+                                              : "step_out shorter than the run");
+      cudaEvent_t a = nullptr, b = nullptr;
+      if (timing) {
+        ck(cudaEventCreate(&a), "event");
+        ck(cudaEventCreate(&b), "event");
+        evs.push_back(a);
+        evs.push_back(b);
+        ck(cudaEventRecord(a, e->stream), "event");
+      }
+      launch_phase(e, mode, ncr, spk, pa, stamp);
+      if (timing) {
+        ck(cudaEventRecord(b, e->stream), "event");
+        phase_ev.emplace_back(a, b);
+      }
+      ck(cudaGetLastError(), "k_phase");
+      k_commit<<<ncr, 256, 0, e->stream>>>(e->d, color, std::max(ncol, 1), nreg, diff_cnt, diff,
+                                             e->free_stack, e->ctl);
+      ck(cudaGetLastError(), "k_commit");
+      const int nxt = e->cur ^ 1;
+      k_rebuild<<<1, 1024, 0, e->stream>>>(e->tab[e->cur], e->tab[nxt], e->cap, stamp,
+                                            e->fate_stamp, e->fate_alive, e->fate_x, e->fate_t,
+                                            e->fate_slot, ncr, births_cnt, births, e->ctl);
+      ck(cudaGetLastError(), "k_rebuild");
+      launches += 3;
+      e->cur = nxt;
+      tape_base += (long long)ncr * kk;
+      executed += (int64_t)ncr * kk;
+      if (serial) {
+        // run_serial: id_base += births (samplers.hpp:302-303); births are the
+        // chain's accepted births alive or not, counted by the kernel
+        int nb = 0;
+        ck(cudaMemcpyAsync(&nb, births_total, 4, cudaMemcpyDeviceToHost, e->stream), "D2H");
+        ck(cudaStreamSynchronize(e->stream), "sync");
+        next_base += (unsigned long long)nb;
+      } else {
+        next_base += (unsigned long long)ncr * (unsigned long long)kk;
+      }
+    };
+    if (serial) {
+      // run_serial (samplers.hpp:294-313): chunks of record_every steps, a
+      // trace row (and snapshot past burn-in) after every chunk
+      const int64_t total = sc->epochs * sc->steps_per_epoch;
+      while (executed < total) {
+        const int64_t chunk = std::min<int64_t>(sc->record_every, total - executed);
+        run_phase(0, 0, 1, 1, bnd, chunk, (long long)executed);
+        last_recorded = executed;
+        record_row(executed);
+      }
+    } else {
+      const int64_t k = sc->steps_per_epoch;
       for (int64_t i = 0; i < sc->epochs; ++i) {
-        const int epoch = (int)i;
         const int64_t pi = sc->dynamic ? i : 0;
         const int nreg = h_nreg[pi];
         for (int color = 0; color < ncol; ++color) {
           const int ncr = nreg > color ? (nreg - color + ncol - 1) / ncol : 0;
           if (ncr == 0) continue;
-          PhaseArgs pa{};
-          pa.epoch = epoch;
-          pa.color = color;
-          pa.nreg = nreg;
-          pa.n_slots = ncr;
-          pa.bnd = bnd + (size_t)pi * bcap;
-          pa.next_base = next_base;
-          pa.tape_base = tape_base;
-          pa.tab = e->tab[e->cur];
-          pa.fate_stamp = e->fate_stamp;
-          pa.fate_alive = e->fate_alive;
-          pa.fate_x = e->fate_x;
-          pa.fate_t = e->fate_t;
-          pa.fate_slot = e->fate_slot;
-          pa.births_cnt = births_cnt;
-          pa.births = births;
-          pa.diff_cnt = diff_cnt;
-          pa.diff = diff;
-          pa.free_stack = e->free_stack;
-          pa.tape = d_tape;
-          pa.tape_arr = d_tarr;
-          pa.out = d_out;
-          const int stamp = ++e->stamp;
-          if ((mode == 1 || d_out) && tape_base + (long long)ncr * k > n_tape)
-            throw std::invalid_argument(mode == 1 ? "replay tape shorter than the run"
-                                                  : "step_out shorter than the run");
-          cudaEvent_t a = nullptr, b = nullptr;
-          if (timing) {
-            ck(cudaEventCreate(&a), "event");
-            ck(cudaEventCreate(&b), "event");
-            evs.push_back(a);
-            evs.push_back(b);
-            ck(cudaEventRecord(a, e->stream), "event");
-          }
-          launch_phase(e, mode, ncr, sp, pa, stamp);
-          if (timing) {
-            ck(cudaEventRecord(b, e->stream), "event");
-            phase_ev.emplace_back(a, b);
-          }
-          ck(cudaGetLastError(), "k_phase");
-          k_commit<<<ncr, 256, 0, e->stream>>>(e->d, color, ncol, nreg, diff_cnt, diff,
-                                                 e->free_stack, e->ctl);
-          ck(cudaGetLastError(), "k_commit");
-          const int nxt = e->cur ^ 1;
-          k_rebuild<<<1, 1024, 0, e->stream>>>(e->tab[e->cur], e->tab[nxt], e->cap, stamp,
-                                                e->fate_stamp, e->fate_alive, e->fate_x,
-                                                e->fate_t, e->fate_slot, ncr, births_cnt,
-                                                births, e->ctl);
-          ck(cudaGetLastError(), "k_rebuild");
-          launches += 3;
-          e->cur = nxt;
-          next_base += (unsigned long long)ncr * (unsigned long long)k;
-          tape_base += (long long)ncr * k;
-          executed += (int64_t)ncr * k;
+          run_phase((int)i, color, nreg, ncr, bnd + (size_t)pi * bcap, k, 0);
           // record(false), samplers.hpp:424-434
           if (executed - last_recorded >= sc->record_every) {
             last_recorded = executed;
@@ -2370,6 +2440,25 @@ extern "C" int seis_run_chromatic(seis_engine* e, const seis_sampler_cfg* sc, in
   for (auto ev : evs) cudaEventDestroy(ev);
   for (void* p : tmp) cudaFree(p);
   return rc;
+}
+
+extern "C" int seis_run_chromatic(seis_engine* e, const seis_sampler_cfg* sc, int32_t mode,
+                                  const seis_tape_step* tape, int64_t n_tape,
+                                  const double* tape_arr, int64_t n_tape_arr,
+                                  seis_step_out* step_out, int64_t row_cap, int64_t* row_step,
+                                  double* row_log_joint, int64_t* row_count,
+                                  seis_run_stats* stats) {
+  return run_driver(e, sc, mode, tape, n_tape, tape_arr, n_tape_arr, step_out, row_cap, row_step,
+                    row_log_joint, row_count, stats, false);
+}
+
+extern "C" int seis_run_serial(seis_engine* e, const seis_sampler_cfg* sc, int32_t mode,
+                               const seis_tape_step* tape, int64_t n_tape, const double* tape_arr,
+                               int64_t n_tape_arr, seis_step_out* step_out, int64_t row_cap,
+                               int64_t* row_step, double* row_log_joint, int64_t* row_count,
+                               seis_run_stats* stats) {
+  return run_driver(e, sc, mode, tape, n_tape, tape_arr, n_tape_arr, step_out, row_cap, row_step,
+                    row_log_joint, row_count, stats, true);
 }
 
 // run_naive_parallel (samplers.hpp:321-394): independent per-region chains

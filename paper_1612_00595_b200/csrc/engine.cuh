@@ -142,6 +142,12 @@ struct PhaseArgs {
   const int* reg_whi;
   int record_every;                // checkpoints every record_every local steps
   int* cp_counts;                  // [n_cp][nreg] own event count at checkpoint c
+  // serial mode (run_serial, samplers.hpp:282-315): one chain over [0, T]
+  // without the region constraint, run in chunks of record_every steps
+  int serial;
+  long long step_base;             // chain step of this launch's first step
+  int* births_total;               // [n_slots] accepted births of the phase (may be null)
+  unsigned long long* order_io;    // serial: [0] count, [1..] ids in list order (may be null)
 };
 
 enum : int {

@@ -67,7 +67,7 @@ EXPORTS = ("seis_last_error", "seis_engine_create", "seis_engine_destroy", "seis
            "seis_partition_offset", "seis_score_batch", "seis_log_joint", "seis_run_chromatic",
            "seis_world_last_error", "seis_world_generate", "seis_world_with_events",
            "seis_thomas_events", "seis_set_snapshot_capacity", "seis_get_snapshots",
-           "seis_run_naive", "seis_engine_pool_slots", "seis_eval_last_error",
+           "seis_run_naive", "seis_run_serial", "seis_engine_pool_slots", "seis_eval_last_error",
            "seis_match_events", "seis_bootstrap_ci")
 
 _LIB = None
@@ -99,6 +99,7 @@ def load_library(path: str | None = None) -> C.CDLL:
     L.seis_log_joint.argtypes = [P, P]
     L.seis_run_chromatic.argtypes = [P, P, i32, P, i64, P, i64, P, i64, P, P, P, P]
     L.seis_run_naive.argtypes = [P, P, i32, P, i64, P, i64, P, i64, P, P, P, P]
+    L.seis_run_serial.argtypes = [P, P, i32, P, i64, P, i64, P, i64, P, P, P, P]
     L.seis_world_generate.argtypes = [P, P, i64, u64, i64, P, P, P, P, P, P, i32, i32]
     L.seis_world_with_events.argtypes = [P, P, i64, i64, P, P, u64, P, P, i32, i32]
     L.seis_thomas_events.argtypes = [u64, f64, f64, f64, f64, f64, f64, i64, P, P, P]
@@ -171,9 +172,9 @@ class SamplerConfig:
     record_log_joint: bool = False
 
     def _c(self):
-        if self.algorithm not in ("chromatic-static", "chromatic-dynamic", "naive"):
+        if self.algorithm not in ("chromatic-static", "chromatic-dynamic", "naive", "serial"):
             raise ValueError(f"unknown sampler '{self.algorithm}' (this engine runs "
-                             "chromatic-static, chromatic-dynamic or naive)")
+                             "chromatic-static, chromatic-dynamic, naive or serial)")
         return _SamplerC(self.steps_per_epoch, self.epochs, self.n_regions, self.seed,
                          self.burn_in_fraction, self.record_every, (f64 * 5)(*self.weights),
                          self.step_location_x, self.step_location_t, self.step_arrival,
@@ -554,7 +555,8 @@ class Engine:
     def run_chromatic(self, sc: SamplerConfig, tape: np.ndarray | None = None,
                       tape_arrivals: np.ndarray | None = None, row_cap: int = 1 << 16,
                       final: bool = True, decisions: int = 0) -> Trace:
-        """run_chromatic (samplers.hpp:401-498) from the resident hypothesis, or
+        """run_chromatic (samplers.hpp:401-498) from the resident hypothesis;
+        run_serial (samplers.hpp:282-315) when sc.algorithm == "serial"; or
         run_naive_parallel (samplers.hpp:321-394) when sc.algorithm == "naive"
         (from the empty hypothesis).
 
@@ -583,7 +585,8 @@ class Engine:
         rl = np.zeros(row_cap)
         rc = np.zeros(row_cap, np.int64)
         st = _StatsC()
-        fn = self.L.seis_run_naive if sc.algorithm == "naive" else self.L.seis_run_chromatic
+        fn = {"naive": self.L.seis_run_naive,
+              "serial": self.L.seis_run_serial}.get(sc.algorithm, self.L.seis_run_chromatic)
         _check(fn(self.h, C.byref(s), mode, _p(tape), n_tape, _p(tarr),
                   0 if tarr is None else len(tarr), _p(out), row_cap, _p(rs), _p(rl), _p(rc),
                   C.byref(st)), self.L)
@@ -601,9 +604,9 @@ class Engine:
 
 def run_sampler(config: ModelConfig, signals: np.ndarray, sc: SamplerConfig,
                 event_capacity: int = 4096) -> Trace:
-    """reference run_sampler (samplers.hpp:500-509) for the chromatic and
-    naive algorithms: from the empty hypothesis, through the C-ABI with host
-    buffers."""
+    """reference run_sampler (samplers.hpp:500-509) for every algorithm
+    (serial, naive, chromatic static/dynamic): from the empty hypothesis,
+    through the C-ABI with host buffers."""
     eng = Engine(config, signals, event_capacity)
     try:
         return eng.run_chromatic(sc)

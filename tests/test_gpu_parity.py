@@ -429,3 +429,55 @@ def test_naive_posterior_within_seed_spread(E, oc):
         a, b = gpu[:, c], ref[:, c]
         se = np.sqrt(a.var(ddof=1) / len(a) + b.var(ddof=1) / len(b))
         assert abs(a.mean() - b.mean()) <= 2.5 * se + 0.02, (name, a.mean(), b.mean(), se)
+
+
+# ------------------------------------------------------------------ serial mode
+def _serial_sampler(E, s, record_log_joint=True):
+    return E.SamplerConfig(algorithm="serial", steps_per_epoch=s.steps_per_epoch,
+                           epochs=s.epochs, n_regions=s.n_regions, seed=s.seed,
+                           burn_in_fraction=s.burn_in_fraction, record_every=s.record_every,
+                           record_log_joint=record_log_joint)
+
+
+def test_serial_replay_reference_tape(E, oc):
+    """run_serial (samplers.hpp:282-315) replayed from the oracle's tape, which
+    test_oracle pins bit-exact to the reference's."""
+    m = default_model()
+    w = golden_world("w1", m)
+    s = O.Sampler(steps_per_epoch=200, epochs=3, n_regions=4, seed=9, record_every=170,
+                  burn_in_fraction=0.0)
+    r = oc.run_chromatic(w, s, tape=True, serial=True, rowlj=True)
+    eng = E.Engine(engine_model(m), w.signals)
+    tr = eng.run_chromatic(_serial_sampler(E, s), tape=r["tape"], tape_arrivals=r["tape_arr"])
+    t = r["tape"]
+    assert np.array_equal(tr.step_out["scored"], t["scored"])
+    drawn = t["u_drawn"] == 1
+    tie = np.zeros(len(t), bool)
+    tie[drawn] = np.abs(t["log_r"][drawn] - np.log(t["u"][drawn])) < TIE
+    assert not ((tr.step_out["accepted"] != t["accepted"]) & ~tie).any()
+    sc = (t["scored"] == 1) & np.isfinite(t["delta"])
+    assert np.allclose(tr.step_out["delta"][sc], t["delta"][sc], rtol=1e-11, atol=1e-9)
+    assert np.array_equal(tr.final.ids, r["final"].ids)
+    assert np.array_equal(tr.final.arrivals, r["final"].arr)
+    assert np.array_equal(tr.row_step, r["row_step"]) and np.array_equal(tr.row_count, r["row_count"])
+    assert np.allclose(tr.row_log_joint, r["row_lj"], rtol=1e-12, atol=1e-8)
+
+
+@pytest.mark.parametrize("ws", [0, 3])
+def test_serial_production_matches_oracle_philox(E, oc, ws):
+    m = default_model()
+    w = golden_world(f"w{ws}", m)
+    s = O.Sampler(steps_per_epoch=250, epochs=4, n_regions=4, seed=41 + ws, rng_mode=1,
+                  record_every=300, burn_in_fraction=0.5)
+    ro = oc.run_chromatic(w, s, tape=True, rowlj=True, serial=True)
+    eng = E.Engine(engine_model(m), w.signals)
+    eng.set_snapshot_capacity(1 << 14, 16)
+    tr = eng.run_chromatic(_serial_sampler(E, s), decisions=len(ro["tape"]))
+    _decisions_match(tr.step_out, ro["tape"], 1e-11)
+    assert tr.total_steps == ro["total_steps"] and tr.total_accepted == ro["total_accepted"]
+    assert np.array_equal(tr.final.ids, ro["final"].ids)
+    assert np.array_equal(tr.final.arrivals, ro["final"].arr)
+    assert np.array_equal(tr.row_step, ro["row_step"]) and np.array_equal(tr.row_count, ro["row_count"])
+    assert np.allclose(tr.row_log_joint, ro["row_lj"], rtol=1e-12, atol=1e-8)
+    # snapshots at every record point past burn-in (samplers.hpp:309-312)
+    assert [sn.step for sn in tr.snapshots] == [int(v) for v in ro["row_step"][1:] if v >= 500]

@@ -219,3 +219,28 @@ def test_naive_tape_matches_reference(oc, seed):
     assert np.array_equal(a["row_lj"], b["row_lj"]) and np.array_equal(a["row_count"], b["row_count"])
     c = O.ref_run_sampler(w, s, naive=True)
     assert np.array_equal(a["final"].arr, c["final"].arr)
+
+
+@pytest.mark.parametrize("seed", [0, 5])
+def test_serial_tape_matches_reference(oc, seed):
+    """run_serial (samplers.hpp:282-315): the oracle's tape, rows and final
+    hypothesis bit-identical to the reference's, which also matches the
+    reference's own run_sampler(Serial)."""
+    if not O.have_ref():
+        pytest.skip("reference tree absent")
+    R = O.Oracle("ref")
+    m = default_model()
+    w = oc.sample_world(m, 60 + seed)
+    s = O.Sampler(steps_per_epoch=150, epochs=4, n_regions=4, seed=seed, record_every=110,
+                  burn_in_fraction=0.0)
+    a = oc.run_chromatic(w, s, serial=True, rowlj=True)
+    b = R.run_chromatic(w, s, serial=True, rowlj=True)
+    assert a["tape"].tobytes() == b["tape"].tobytes()
+    assert np.array_equal(a["tape_arr"], b["tape_arr"])
+    assert np.array_equal(a["row_step"], b["row_step"]) and np.array_equal(a["row_count"], b["row_count"])
+    assert np.array_equal(a["row_lj"], b["row_lj"])
+    assert a["total_accepted"] == b["total_accepted"]
+    c = O.ref_run_sampler(w, s, serial=True)
+    order = np.argsort(c["final"].ids)
+    assert np.array_equal(a["final"].ids, c["final"].ids[order])
+    assert np.array_equal(a["final"].arr, c["final"].arr[order])
