@@ -367,6 +367,8 @@ __global__ void __launch_bounds__(NTT, MINB)
   double(*acc_sig)[NTT] = reinterpret_cast<double(*)[NTT]>(s_logi_n + LOGIWIN);
   double(*acc_arr)[NTT] = reinterpret_cast<double(*)[NTT]>(s_logi_n + LOGIWIN + MSPEC * NTT);
   int(*acc_cnt)[NTT] = reinterpret_cast<int(*)[NTT]>(s_logi_n + LOGIWIN + 2 * MSPEC * NTT);
+  DiffS* dcache =
+      reinterpret_cast<DiffS*>(s_logi_n + LOGIWIN + 2 * MSPEC * NTT + MSPEC * NTT / 2);
   __shared__ int s_accg[MSPEC], s_cnt[MSPEC];
   __shared__ long long s_nlocal;
 
@@ -548,6 +550,13 @@ __global__ void __launch_bounds__(NTT, MINB)
       tprof[0] += now - tc;
       tc = now;
     }
+    const bool use_dcache = (d.S_pad + 31) / 32 < 4 * NWT && d.S_pad <= kDiffCache && d.n < 65535;
+    if (use_dcache && s_np > 0) {
+      // the round's diff windows per station, once for every proposal's items
+      const int np_c = s_np;
+      for (int j = tid; j < d.S_pad; j += NTT) diff_station(d, j, np_c, pold, pnew, dcache[j]);
+      __syncthreads();
+    }
     {
       const int np_now = s_np;
       // Two item orders. Many tiles per warp (configs 2-4): one item = one
@@ -654,7 +663,17 @@ __global__ void __launch_bounds__(NTT, MINB)
           in.step = (uint32_t)(pa.step_base + i0 + q);
           in.wlo = win_lo;
           in.whi = win_hi;
-          score_item<MODE, YT>(d, P, in, tile, np_now, pold, pnew, nullptr, Ts, sig, arr, cnt);
+          DiffW X;
+          const DiffW* Xp = nullptr;
+          if (use_dcache) {
+            if (np_now > 0) {
+              diff_from_cache(dcache[tile * 32 + lane], X);
+            } else {
+              X.nwmax = 0;
+            }
+            Xp = &X;
+          }
+          score_item<MODE, YT>(d, P, in, tile, np_now, pold, pnew, Xp, Ts, sig, arr, cnt);
         }
         if (cur_q >= 0) {
           sig = warp_sum(sig);
@@ -1396,7 +1415,8 @@ namespace {
 thread_local std::string g_err;
 // dynamic: the log(i) window + per-lane partial sums (2 double + 1 int per
 // speculative slot and thread)
-constexpr int kPhaseSmem = LOGIWIN * (int)sizeof(double) + MSPEC * NT * (2 * 8 + 4);
+constexpr int kPhaseSmem = LOGIWIN * (int)sizeof(double) + MSPEC * NT * (2 * 8 + 4) +
+                           kDiffCache * (int)sizeof(DiffS);
 
 int fail(int code, const std::string& m) {
   g_err = m;

@@ -38,6 +38,7 @@ constexpr int kMaxEvents = 1 << 22;  // event_capacity bound (table sizes; count
 constexpr int MAXDIFF = 2 * MAXOWN;  // diff pairs a region may hold
 constexpr int MAXDOUT = 3 * MAXOWN;  // diff pairs + recycled slots per region
 constexpr int TBL = 512;         // coverage counts whose {dL, dI} rows live in smem
+constexpr int kDiffCache = 2048;  // stations whose round diff windows k_phase caches in smem
 constexpr int kRowPad = 32;      // zero rows appended to y and cov (unpredicated chunk loads)
 constexpr int LOGIWIN = 1024;    // log(i) window around the phase-start event count
 constexpr int BANDMAX = 256;     // rows of the generic diff-correction scratch

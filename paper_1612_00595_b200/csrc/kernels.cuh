@@ -201,7 +201,7 @@ __device__ __forceinline__ void band(const Dev& d, int j, int blo, int bhi, cons
 // rows past a lane's window index the zero row of the table. cnt is the
 // window length (computed by the caller).
 #ifndef SEIS_BAND_RU
-#define SEIS_BAND_RU 7
+#define SEIS_BAND_RU 21
 #endif
 #ifndef SEIS_BAND_PIPE
 #define SEIS_BAND_PIPE 0
@@ -432,43 +432,91 @@ struct DiffW {
   int nwmax;
 };
 
+// Walk the region's (start, current) pairs at station j with each batch of
+// four pairs' pool loads issued together; first four effective windows kept.
+__device__ __forceinline__ int diff_collect(const Dev& d, int j, int np, const int* pold,
+                                            const int* pnew, Win (&w)[4], int (&sg)[4]) {
+  int nw = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    w[k] = empty_win();
+    sg[k] = 0;
+  }
+  if (j >= d.S) return 0;
+  for (int q0 = 0; q0 < np; q0 += 4) {
+    double vo[4], vn[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int q = q0 + k;
+      const int so = q < np ? pold[q] : -1, sn = q < np ? pnew[q] : -1;
+      vo[k] = so >= 0 ? __ldg(d.pool + (size_t)so * d.S_pad + j) : 0.0;
+      vn[k] = sn >= 0 ? __ldg(d.pool + (size_t)sn * d.S_pad + j) : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int q = q0 + k;
+      if (q >= np) break;
+      const Win wo = pold[q] >= 0 ? make_win(d, vo[k]) : empty_win();
+      const Win wn = pnew[q] >= 0 ? make_win(d, vn[k]) : empty_win();
+      if (weq(wo, wn)) continue;
+      if (wo.hi > wo.lo) {
+#pragma unroll
+        for (int m = 0; m < 4; ++m)
+          if (m == nw) {
+            w[m] = wo;
+            sg[m] = -1;
+          }
+        ++nw;
+      }
+      if (wn.hi > wn.lo) {
+#pragma unroll
+        for (int m = 0; m < 4; ++m)
+          if (m == nw) {
+            w[m] = wn;
+            sg[m] = 1;
+          }
+        ++nw;
+      }
+    }
+  }
+  return nw;
+}
+
 __device__ __forceinline__ void diff_windows(const Dev& d, int j, int np, const int* pold,
                                              const int* pnew, DiffW& X) {
-  const bool v = j < d.S;
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    X.D.w[q] = empty_win();
-    X.sg[q] = 0;
-  }
-  int nw = 0;
-  for (int q = 0; q < np && v; ++q) {
-    const Win wo = pold[q] >= 0 ? make_win(d, d.pool[(size_t)pold[q] * d.S_pad + j]) : empty_win();
-    const Win wn = pnew[q] >= 0 ? make_win(d, d.pool[(size_t)pnew[q] * d.S_pad + j]) : empty_win();
-    if (weq(wo, wn)) continue;
-    if (wo.hi > wo.lo) {
-      if (nw < 4) {
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-          if (k == nw) {
-            X.D.w[k] = wo;
-            X.sg[k] = -1;
-          }
-      }
-      ++nw;
-    }
-    if (wn.hi > wn.lo) {
-      if (nw < 4) {
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-          if (k == nw) {
-            X.D.w[k] = wn;
-            X.sg[k] = 1;
-          }
-      }
-      ++nw;
-    }
-  }
+  const int nw = diff_collect(d, j, np, pold, pnew, X.D.w, X.sg);
   X.nwmax = (int)__reduce_max_sync(0xffffffffu, (unsigned)nw);
+}
+
+// Per-station diff windows cached in shared memory for a round (the
+// proposal-major pass, few stations): windows as uint16 (n < 65535).
+struct DiffS {
+  uint16_t lo[4], hi[4];
+  int8_t sg[4];
+  int n;
+};
+
+__device__ __forceinline__ void diff_station(const Dev& d, int j, int np, const int* pold,
+                                             const int* pnew, DiffS& o) {
+  Win w[4];
+  int sg[4];
+  o.n = diff_collect(d, j, np, pold, pnew, w, sg);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    o.lo[k] = (uint16_t)w[k].lo;
+    o.hi[k] = (uint16_t)w[k].hi;
+    o.sg[k] = (int8_t)sg[k];
+  }
+}
+
+__device__ __forceinline__ void diff_from_cache(const DiffS& c, DiffW& X) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    X.D.w[k].lo = c.lo[k];
+    X.D.w[k].hi = c.hi[k];
+    X.sg[k] = c.sg[k];
+  }
+  X.nwmax = (int)__reduce_max_sync(0xffffffffu, (unsigned)c.n);
 }
 
 // One station of one proposal (density.hpp:239-301): arrival densities of
