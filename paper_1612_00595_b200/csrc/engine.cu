@@ -131,22 +131,22 @@ __global__ void k_transpose(const YT* __restrict__ src, YT* __restrict__ dst, in
 
 // coverage of every event of the table (variance_profile, density.hpp:112-129)
 __global__ void k_build_cov(Dev d, Table tab, Ctl* ctl) {
-  const int e = blockIdx.y;
-  if (e >= ctl->n_events) return;
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= d.P2) return;
-  const double2 a = reinterpret_cast<const double2*>(d.pool)[(size_t)tab.slot[e] * d.P2 + p];
-  const Win w0 = 2 * p < d.S ? make_win(d, a.x) : empty_win();
-  const Win w1 = 2 * p + 1 < d.S ? make_win(d, a.y) : empty_win();
-  const int lo = min(w0.lo < w0.hi ? w0.lo : INT_MAX, w1.lo < w1.hi ? w1.lo : INT_MAX);
-  const int hi = max(w0.hi > w0.lo ? w0.hi : INT_MIN, w1.hi > w1.lo ? w1.hi : INT_MIN);
-  for (int r = lo; r < hi; ++r) {
-    const int i0 = inw(r, w0), i1 = inw(r, w1);
-    const unsigned inc = (unsigned)i0 + ((unsigned)i1 << 16);
-    if (inc) {
-      const unsigned old = atomicAdd(d.cov + pix(d.rows, r, p), inc);
-      if ((old & 0xffffu) + i0 > 0xffffu || (old >> 16) + i1 > 0xffffu)
-        atomicExch(&ctl->err, ERR_COUNT_OVERFLOW);
+  for (int e = blockIdx.y; e < ctl->n_events; e += gridDim.y) {
+    const double2 a = reinterpret_cast<const double2*>(d.pool)[(size_t)tab.slot[e] * d.P2 + p];
+    const Win w0 = 2 * p < d.S ? make_win(d, a.x) : empty_win();
+    const Win w1 = 2 * p + 1 < d.S ? make_win(d, a.y) : empty_win();
+    const int lo = min(w0.lo < w0.hi ? w0.lo : INT_MAX, w1.lo < w1.hi ? w1.lo : INT_MAX);
+    const int hi = max(w0.hi > w0.lo ? w0.hi : INT_MIN, w1.hi > w1.lo ? w1.hi : INT_MIN);
+    for (int r = lo; r < hi; ++r) {
+      const int i0 = inw(r, w0), i1 = inw(r, w1);
+      const unsigned inc = (unsigned)i0 + ((unsigned)i1 << 16);
+      if (inc) {
+        const unsigned old = atomicAdd(d.cov + pix(d.rows, r, p), inc);
+        if ((old & 0xffffu) + i0 > 0xffffu || (old >> 16) + i1 > 0xffffu)
+          set_err(ctl, ERR_COUNT_OVERFLOW);
+      }
     }
   }
 }
@@ -374,6 +374,11 @@ __global__ void __launch_bounds__(NTT, MINB)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int slot_idx = blockIdx.x;
+  if (tid == 0) {  // a CTA that stops on an error leaves nothing for the barrier
+    pa.births_cnt[slot_idx] = 0;
+    pa.diff_cnt[slot_idx] = 0;
+    if (pa.births_total) pa.births_total[slot_idx] = 0;
+  }
   const int region = pa.naive ? slot_idx : pa.color + slot_idx * sp.ncol;
   if (region >= pa.nreg) return;
   const double rlo = pa.bnd[region], rhi = pa.bnd[region + 1];
@@ -442,7 +447,7 @@ __global__ void __launch_bounds__(NTT, MINB)
     __syncthreads();
   }
   if (s_nown > MAXOWN) {
-    if (tid == 0) atomicExch(&ctl->err, ERR_OWN_OVERFLOW);
+    if (tid == 0) set_err(ctl, ERR_OWN_OVERFLOW);
     return;
   }
   // run_serial keeps the chain's list order (erase + push_back) across its
@@ -763,7 +768,7 @@ __global__ void __launch_bounds__(NTT, MINB)
       for (int q = 0; q < m; ++q) {
         Prop& P = prop[buf][q];
         if (MODE == 1 && P.bad) {
-          atomicExch(&ctl->err, ERR_TAPE_UNKNOWN_ID);
+          set_err(ctl, ERR_TAPE_UNKNOWN_ID);
           s_abort = 1;
           adv = q + 1;
           break;
@@ -811,7 +816,7 @@ __global__ void __launch_bounds__(NTT, MINB)
             } else {
               const int top = atomicSub(&ctl->free_top, 1) - 1;
               if (top < 0) {
-                atomicExch(&ctl->err, ERR_POOL_EXHAUSTED);
+                set_err(ctl, ERR_POOL_EXHAUSTED);
                 ok = false;
                 break;
               }
@@ -820,7 +825,7 @@ __global__ void __launch_bounds__(NTT, MINB)
           }
         }
         if (ok && P.na >= 1 && nown - P.nr + P.na > MAXOWN) {
-          atomicExch(&ctl->err, ERR_OWN_OVERFLOW);
+          set_err(ctl, ERR_OWN_OVERFLOW);
           ok = false;
         }
         if (!ok) {
@@ -1076,7 +1081,7 @@ __global__ void k_commit(Dev d, int color, int ncol, int nreg, const int* diff_c
           const unsigned old = atomicAdd(d.cov + pix(d.rows, r, p), (unsigned)inc);
           if ((d0 > 0 && (int)(old & 0xffffu) + d0 > 0xffff) ||
               (d1 > 0 && (int)(old >> 16) + d1 > 0xffff))
-            atomicExch(&ctl->err, ERR_COUNT_OVERFLOW);
+            set_err(ctl, ERR_COUNT_OVERFLOW);
         }
       }
     }
@@ -1169,7 +1174,7 @@ __global__ void __launch_bounds__(1024) k_rebuild(Table in, Table out, int cap, 
     base += tot;
   }
   if (threadIdx.x == 0) {
-    if (base > cap) atomicExch(&ctl->err, ERR_TABLE_OVERFLOW);
+    if (base > cap) set_err(ctl, ERR_TABLE_OVERFLOW);
     ctl->n_events = min(base, cap);
   }
 }
@@ -1819,7 +1824,8 @@ int seis_upload_signals(seis_engine* e, const void* signals) {
 
 int seis_set_hypothesis(seis_engine* e, int64_t N, const uint64_t* ids, const double* x,
                         const double* t, const double* arrivals) {
-  return guarded([&] {
+  bool cov_failed = false;
+  const int rc = guarded([&] {
     if (N < 0 || N > e->cap) throw std::invalid_argument("hypothesis larger than event_capacity");
     std::vector<int64_t> order(N);
     for (int64_t i = 0; i < N; ++i) order[i] = i;
@@ -1852,8 +1858,8 @@ int seis_set_hypothesis(seis_engine* e, int64_t N, const uint64_t* ids, const do
       // scattered to its slot
       std::vector<int> slot_of_row(N);
       for (int64_t i = 0; i < N; ++i) slot_of_row[row[i]] = (int)i;
-      const int64_t chunk =
-          std::max<int64_t>(1, std::min<int64_t>(N, ((int64_t)512 << 20) / ((int64_t)e->S * 8)));
+      const int64_t chunk = std::max<int64_t>(
+          1, std::min<int64_t>({N, ((int64_t)512 << 20) / ((int64_t)e->S * 8), 65535}));
       double* raw = dalloc<double>((size_t)chunk * e->S);
       int* dslot = dalloc<int>(N);
       ck(cudaMemcpyAsync(dslot, slot_of_row.data(), (size_t)N * 4, cudaMemcpyHostToDevice,
@@ -1879,12 +1885,23 @@ int seis_set_hypothesis(seis_engine* e, int64_t N, const uint64_t* ids, const do
     ck(cudaMemcpy(e->ctl, &c, sizeof c, cudaMemcpyHostToDevice), "H2D");
     ck(cudaMemsetAsync(e->cov, 0, (size_t)(e->n + kRowPad) * e->P2 * 4, e->stream), "memset");
     if (N) {
-      dim3 grid((e->P2 + 127) / 128, (unsigned)N);
+      dim3 grid((e->P2 + 127) / 128, (unsigned)std::min<int64_t>(N, 65535));
       k_build_cov<<<grid, 128, 0, e->stream>>>(e->d, tb, e->ctl);
       ck(cudaGetLastError(), "k_build_cov");
     }
     ck(cudaStreamSynchronize(e->stream), "sync");
+    const Ctl after = read_ctl(e);
+    if (after.err) {
+      cov_failed = true;
+      throw std::runtime_error(std::string("device: ") + err_name(after.err));
+    }
   });
+  if (rc && cov_failed) {  // leave the engine empty rather than half-loaded
+    const std::string msg = g_err;
+    seis_set_hypothesis(e, 0, nullptr, nullptr, nullptr, nullptr);
+    g_err = msg;
+  }
+  return rc;
 }
 
 int seis_get_hypothesis(seis_engine* e, int64_t cap, int64_t* n, uint64_t* ids, double* x,
@@ -1899,8 +1916,8 @@ int seis_get_hypothesis(seis_engine* e, int64_t cap, int64_t* n, uint64_t* ids, 
     ck(cudaMemcpy(x, tb.x, m * 8, cudaMemcpyDeviceToHost), "D2H");
     ck(cudaMemcpy(t, tb.t, m * 8, cudaMemcpyDeviceToHost), "D2H");
     if (arrivals) {  // in chunks of <= 512 MiB
-      const int64_t chunk =
-          std::max<int64_t>(1, std::min<int64_t>(m, ((int64_t)512 << 20) / ((int64_t)e->S * 8)));
+      const int64_t chunk = std::max<int64_t>(
+          1, std::min<int64_t>({m, ((int64_t)512 << 20) / ((int64_t)e->S * 8), 65535}));
       double* buf = dalloc<double>((size_t)chunk * e->S);
       for (int64_t r0 = 0; r0 < m; r0 += chunk) {
         const int64_t nr = std::min(chunk, m - r0);

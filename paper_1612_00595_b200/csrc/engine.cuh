@@ -160,6 +160,9 @@ enum : int {
   ERR_COUNT_OVERFLOW = 5,
 };
 
+// the first device error of a run wins (later ones are consequences)
+__device__ __forceinline__ void set_err(Ctl* ctl, int code) { atomicCAS(&ctl->err, 0, code); }
+
 __device__ __forceinline__ Win make_win(const Dev& d, double a) {
   // arrival_sample_range, density.hpp:29-36: ceil in fp64 (no contraction:
   // --fmad=false), clamp to [0, n]. cvt.rpi.s32.f64 rounds up and saturates

@@ -481,3 +481,40 @@ def test_serial_production_matches_oracle_philox(E, oc, ws):
     assert np.allclose(tr.row_log_joint, ro["row_lj"], rtol=1e-12, atol=1e-8)
     # snapshots at every record point past burn-in (samplers.hpp:309-312)
     assert [sn.step for sn in tr.snapshots] == [int(v) for v in ro["row_step"][1:] if v >= 500]
+
+
+# ------------------------------------------------------------------ limits
+def test_count_overflow_is_detected(E):
+    """more than 65535 events over one (sample, station): the uint16 counts
+    would wrap; the engine refuses the hypothesis and stays usable."""
+    m = O.Model(lambda_rate=0.01, T=100.0, x_max=10.0, v=2.0, stations=O.stations_line(2, 10.0))
+    em = engine_model(m)
+    sig = np.zeros((2, 100))
+    N = 65536
+    eng = E.Engine(em, sig, event_capacity=N + 8)
+    arr = np.tile(np.array([[50.0, 55.0]]), (N, 1))
+    ev = E.Events(np.arange(N, dtype=np.uint64), np.zeros(N), np.full(N, 50.0), arr)
+    with pytest.raises(RuntimeError, match="overflow"):
+        eng.set_hypothesis(ev)
+    assert eng.get_hypothesis().ids.size == 0
+    ok = E.Events(ev.ids[:65535], ev.x[:65535], ev.t[:65535], arr[:65535])
+    eng.set_hypothesis(ok)
+    assert eng.get_hypothesis(arrivals=False).ids.size == 65535
+    with pytest.raises(ValueError):  # above event_capacity
+        E.Engine(em, sig, event_capacity=4).set_hypothesis(ok)
+
+
+def test_capacity_and_region_limits_fail_loudly(E, oc):
+    m = default_model()
+    w = golden_world("w0", m)
+    # births past a tiny event table: status 3, not a silent wrap
+    eng = E.Engine(engine_model(m), w.signals, event_capacity=2)
+    with pytest.raises(RuntimeError):
+        eng.run_chromatic(E.SamplerConfig(steps_per_epoch=400, epochs=6, n_regions=4, seed=1))
+    # the serial chain lives in one CTA: more than 64 events is refused
+    many = oc.sample_world(O.Model(lambda_rate=100 / 240.0), 5)
+    assert many.events.N > 64
+    eng2 = E.Engine(engine_model(many.model), many.signals, event_capacity=1024)
+    eng2.set_hypothesis(E.Events(many.events.ids, many.events.x, many.events.t, many.events.arr))
+    with pytest.raises(RuntimeError, match="per-region event limit"):
+        eng2.run_chromatic(E.SamplerConfig(algorithm="serial", steps_per_epoch=10, epochs=1))
