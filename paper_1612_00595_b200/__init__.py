@@ -7,5 +7,5 @@ sampler/model API over it. See DESIGN.md.
 from .engine import (  # noqa: F401
     F32, F64, BootstrapCI, Engine, Events, MatchReport, ModelConfig, Partition, SamplerConfig,
     Snapshot, Trace, assign_regions, bootstrap_ci, match_events, metric_trace,
-    load_library, make_world_with_events, partition, partition_offset, run_sampler,
-    sample_world, thomas_events)
+    load_library, load_world, make_world_with_events, partition, partition_offset, run_sampler,
+    sample_world, save_world, thomas_events)

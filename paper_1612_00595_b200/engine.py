@@ -14,6 +14,7 @@ Loading fails loudly if the library is missing or no sm_100 device is present.
 from __future__ import annotations
 
 import ctypes as C
+import json
 import os
 from dataclasses import dataclass, field
 
@@ -332,6 +333,75 @@ def make_world_with_events(config: ModelConfig, cx, ct, seed: int, dtype=F64, th
     if rc:
         raise RuntimeError(L.seis_world_last_error().decode())
     return Events(np.arange(N, dtype=np.uint64), cx.copy(), ct.copy(), arr[:N].copy()), sig
+
+
+# ------------------------------------------------------------ world files
+# "seis world v1": a binary world (model, events with arrivals, signals) in
+# place of the reference's CSV files (worldgen.hpp:157-161; 268 M rows at
+# config[4]). Layout: 8-byte magic, u64 header length, JSON header, then the
+# arrays at 64-byte-aligned offsets listed in the header, little-endian.
+# load_world maps them without copying, so Engine uploads straight from the
+# page cache.
+_WORLD_MAGIC = b"SEISWLD1"
+_MODEL_FIELDS = ("lambda_rate", "T", "x_max", "v", "sigma_arrival", "t_s", "var_noise",
+                 "var_event", "sample_rate")
+
+
+def save_world(path: str, config: ModelConfig, events: "Events", signals: np.ndarray) -> None:
+    S, n = config.n_stations(), config.n_samples()
+    sig = np.ascontiguousarray(signals)
+    if sig.dtype not in (np.float32, np.float64) or sig.shape != (S, n):
+        raise ValueError(f"signals must be float32/float64 [S={S}][n={n}]")
+    N = len(events.ids)
+    arrays = [("stations", np.ascontiguousarray(config.stations, "<f8")),
+              ("ids", np.ascontiguousarray(events.ids, "<u8")),
+              ("x", np.ascontiguousarray(events.x, "<f8")),
+              ("t", np.ascontiguousarray(events.t, "<f8")),
+              ("arrivals", np.ascontiguousarray(events.arrivals, "<f8").reshape(N, S)),
+              ("signals", sig.astype(sig.dtype.newbyteorder("<"), copy=False))]
+    head = {"version": 1, "model": {k: float(getattr(config, k)) for k in _MODEL_FIELDS},
+            "S": S, "n": n, "N": N, "signal_dtype": "f32" if sig.dtype == np.float32 else "f64",
+            "arrays": {}}
+    # two passes: offsets depend on the header length
+    for _ in range(2):
+        hb = json.dumps(head, sort_keys=True).encode()
+        off = (16 + len(hb) + 63) // 64 * 64
+        for name, a in arrays:
+            head["arrays"][name] = [off, a.nbytes]
+            off = (off + a.nbytes + 63) // 64 * 64
+    hb = json.dumps(head, sort_keys=True).encode()
+    with open(path, "wb") as f:
+        f.write(_WORLD_MAGIC)
+        f.write(np.uint64(len(hb)).tobytes())
+        f.write(hb)
+        for name, a in arrays:
+            f.seek(head["arrays"][name][0])
+            f.write(a.tobytes(order="C"))
+        f.truncate(max(v[0] + v[1] for v in head["arrays"].values()))
+
+
+def load_world(path: str):
+    """-> (ModelConfig, Events, signals [S][n]); arrays are read-only memory maps."""
+    with open(path, "rb") as f:
+        if f.read(8) != _WORLD_MAGIC:
+            raise ValueError(f"{path}: not a seis world v1 file")
+        hl = int(np.frombuffer(f.read(8), "<u8")[0])
+        head = json.loads(f.read(hl))
+    if head.get("version") != 1:
+        raise ValueError(f"{path}: unsupported world version {head.get('version')}")
+    S, n, N = head["S"], head["n"], head["N"]
+    sd = "<f4" if head["signal_dtype"] == "f32" else "<f8"
+    shapes = {"stations": ("<f8", (S,)), "ids": ("<u8", (N,)), "x": ("<f8", (N,)),
+              "t": ("<f8", (N,)), "arrivals": ("<f8", (N, S)), "signals": (sd, (S, n))}
+    out = {}
+    for name, (dt, shape) in shapes.items():
+        off, nb = head["arrays"][name]
+        if nb == 0:
+            out[name] = np.zeros(shape, dt)
+        else:
+            out[name] = np.memmap(path, dtype=dt, mode="r", offset=off, shape=shape)
+    cfg = ModelConfig(**head["model"], stations=np.array(out["stations"]))
+    return cfg, Events(out["ids"], out["x"], out["t"], out["arrivals"]), out["signals"]
 
 
 def thomas_events(seed, x_max, T, parent_mean, child_mean, sx, st, cap=1 << 22):

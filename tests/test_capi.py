@@ -100,3 +100,28 @@ def test_evaluation_bridge_bit_exact_vs_reference(built):
     empty = E.Events(np.zeros(0, np.uint64), np.zeros(0), np.zeros(0), np.zeros((0, 1)))
     r = E.match_events(empty, empty)
     assert (r.precision, r.recall, r.location_error) == (1.0, 1.0, 0.0)
+
+
+def test_world_file_round_trip(built, tmp_path):
+    """seis world v1 (binary replacement of the reference's CSV world files,
+    SURVEY §8(f)3): save -> load is bit-identical, and loads as memory maps."""
+    import paper_1612_00595_b200 as E
+    m = engine_model(default_model())
+    for dt in (E.F64, E.F32):
+        ev, sig = E.sample_world(m, 11, dtype=dt, threads=2)
+        p = str(tmp_path / f"w{dt}.seisworld")
+        E.save_world(p, m, ev, sig)
+        m2, ev2, sig2 = E.load_world(p)
+        assert isinstance(sig2, np.memmap) and sig2.dtype == sig.dtype
+        assert np.array_equal(sig2, sig) and np.array_equal(ev2.arrivals, ev.arrivals)
+        assert np.array_equal(ev2.ids, ev.ids) and np.array_equal(ev2.x, ev.x)
+        assert np.array_equal(ev2.t, ev.t) and np.array_equal(m2.stations, m.stations)
+        assert (m2.T, m2.v, m2.lambda_rate, m2.t_s) == (m.T, m.v, m.lambda_rate, m.t_s)
+    empty = E.Events(np.zeros(0, np.uint64), np.zeros(0), np.zeros(0), np.zeros((0, 4)))
+    p = str(tmp_path / "empty.seisworld")
+    E.save_world(p, m, empty, sig)
+    assert E.load_world(p)[1].ids.size == 0
+    with open(p, "r+b") as f:
+        f.write(b"NOTWORLD")
+    with pytest.raises(ValueError):
+        E.load_world(p)
