@@ -346,7 +346,7 @@ template <typename YT, int MODE, int NTT, int MINB>
 __global__ void __launch_bounds__(NTT, MINB)
     k_phase(const Dev d, const Samp sp, const PhaseArgs pa, Ctl* ctl, int stamp) {
   constexpr int NWT = NTT / 32;
-  __shared__ double2 Ts[TBL * 4 + 4];  // {dL, dI} per (count, dc) + a zero row
+  __shared__ double2 Ts[kTsSize];  // {dL, dI} per (dc, count) + a zero entry
   __shared__ OwnEv own[MAXOWN];
   __shared__ StartEv st[MAXOWN];
   __shared__ int pold[MAXDIFF], pnew[MAXDIFF];
@@ -392,8 +392,7 @@ __global__ void __launch_bounds__(NTT, MINB)
   const int win_lo = pa.naive ? pa.reg_wlo[region] : 0;
   const int win_hi = pa.naive ? pa.reg_whi[region] : d.n;
 
-  for (int i = tid; i < TBL * 4 + 4; i += NTT)
-    Ts[i] = i < TBL * 4 && i < d.tab_n * 4 ? d.Dg[i] : make_double2(0, 0);
+  fill_ts(Ts, d, tid, NTT);
   const int logi_base = N - LOGIWIN / 2;
   for (int i = tid; i < MAXOWN + 2; i += NTT) s_logi_k[i] = i < d.logi_n ? d.logi[i] : 0.0;
   for (int i = tid; i < LOGIWIN; i += NTT) {
@@ -703,7 +702,7 @@ __global__ void __launch_bounds__(NTT, MINB)
       // parallel lanes (delta_log_joint density.hpp:223-240; log_accept_ratio
       // and mh_step proposals.hpp:255-291). Lanes 8q..8q+7 reduce proposal q's
       // per-warp partials (fixed order, deterministic).
-      static_assert(MSPEC * 8 <= 32 && NWT % 8 == 0, "reduction layout");
+      static_assert(MSPEC * 8 <= 32, "reduction layout");
       const int q = lane >> 3, g = lane & 7;
       double sig = 0.0, A = 0.0;
       int c = 0;
@@ -1195,14 +1194,13 @@ template <typename YT>
 __global__ void __launch_bounds__(NT, 1)
     k_score_batch(const Dev d, Table tab, const Ctl* ctl, const ChangeDev* ch,
                   const double* rows, double* out) {
-  __shared__ double2 Ts[TBL * 4 + 4];
+  __shared__ double2 Ts[kTsSize];
   __shared__ Prop P;
   __shared__ double rsig[NW], rarr[NW];
   __shared__ int s_bad;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const ChangeDev c = ch[blockIdx.x];
-  for (int i = tid; i < TBL * 4 + 4; i += NT)
-    Ts[i] = i < TBL * 4 && i < d.tab_n * 4 ? d.Dg[i] : make_double2(0, 0);
+  fill_ts(Ts, d, tid, NT);
   if (tid == 0) {
     s_bad = 0;
     P.type = -1;

@@ -20,7 +20,10 @@
 
 namespace seis {
 
-constexpr int NT = 512;          // threads per region CTA
+#ifndef SEIS_NT
+#define SEIS_NT 512
+#endif
+constexpr int NT = SEIS_NT;      // threads per region CTA
 #ifndef SEIS_MSPEC
 #define SEIS_MSPEC 4
 #endif

@@ -90,16 +90,31 @@ __device__ __forceinline__ double warp_sum(double v) {
 // differences precomputed on the host from glibc log (one 16-byte lookup).
 __device__ __forceinline__ int dc_code(int dc) { return dc > 0 ? dc + 1 : dc + 2; }
 
+// Shared copy of the table, code-major: entry (c, code) at code * (TBL + 1) + c,
+// so the lanes of a warp (nearby counts, one code) read neighbouring 16-byte
+// entries instead of entries 64 bytes apart on the same banks; kTsZero is an
+// all-zero entry for masked rows. The global table Dg stays [count][code].
+constexpr int kTsStride = TBL + 1;
+constexpr int kTsZero = 4 * kTsStride;
+constexpr int kTsSize = kTsZero + 1;
+__device__ __forceinline__ int ts_idx(int c, int code) { return code * kTsStride + c; }
+
+__device__ __forceinline__ void fill_ts(double2* Ts, const Dev& d, int tid, int nthreads) {
+  for (int i = tid; i < kTsSize; i += nthreads) {
+    const int code = i / kTsStride, c = i - code * kTsStride;
+    Ts[i] = (code < 4 && c < TBL && c < d.tab_n) ? d.Dg[c * 4 + code] : make_double2(0, 0);
+  }
+}
+
 __device__ __forceinline__ double term(const Dev& d, const double2* Ts, double y, int c, int dc) {
-  const int idx = c * 4 + dc_code(dc);
-  const double2 e = c < TBL ? Ts[idx] : d.Dg[idx];
+  const double2 e = c < TBL ? Ts[ts_idx(c, dc_code(dc))] : d.Dg[c * 4 + dc_code(dc)];
   const double y2 = y * y;
   return fma(-y2, e.y, e.x);
 }
 
 // shared-memory-only lookup; the caller guarantees c < TBL
 __device__ __forceinline__ double term_fast(const double2* Ts, double y, int c, int dc) {
-  const double2 e = Ts[c * 4 + dc_code(dc)];
+  const double2 e = Ts[ts_idx(c, dc_code(dc))];
   return fma(-(y * y), e.y, e.x);
 }
 
@@ -233,7 +248,7 @@ __device__ __forceinline__ void band1(const Dev& d, int j, Win W, const Wins<ND>
       for (int q = 0; q < ND; ++q) cc += sg[q] * inw(base + i0 + k, D.w[q]);
       mx = max(mx, cc);
       const bool in = (unsigned)(i0 + k - sh) < (unsigned)len;
-      const int idx = in ? min(cc, TBL - 3) * 4 + code : TBL * 4;
+      const int idx = in ? ts_idx(min(cc, TBL - 3), code) : kTsZero;
       const double2 e = Ts[idx];
       const double yy = (double)yv[k];
       s += fma(-(yy * yy), e.y, e.x);
@@ -359,7 +374,7 @@ __device__ __forceinline__ void edges(const Dev& d, int j, Win A0, Win R0, const
 #pragma unroll
       for (int q = 0; q < ND; ++q) cc += sg[q] * inw(r[k], D.w[q]);
       big |= cc >= TBL - 2;
-      const int idx = dc[k] ? min(cc, TBL - 3) * 4 + dc_code(dc[k]) : TBL * 4;
+      const int idx = dc[k] ? ts_idx(min(cc, TBL - 3), dc_code(dc[k])) : kTsZero;
       const double2 e = Ts[idx];
       const double yy = (double)yv[k];
       s_loc += fma(-(yy * yy), e.y, e.x);
