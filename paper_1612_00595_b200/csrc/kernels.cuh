@@ -218,8 +218,8 @@ __device__ __forceinline__ void band(const Dev& d, int j, int blo, int bhi, cons
 #ifndef SEIS_BAND_RU
 #define SEIS_BAND_RU 21
 #endif
-#ifndef SEIS_BAND_PIPE
-#define SEIS_BAND_PIPE 0
+#ifndef SEIS_BAND_ACC
+#define SEIS_BAND_ACC 1  // partial sums per lane in the dense band (more measured no faster)
 #endif
 static_assert(kRowPad >= SEIS_BAND_RU, "band1 reads up to RU - 1 rows past the longest window");
 template <int SIGN, int ND, typename YT>
@@ -238,59 +238,12 @@ __device__ __forceinline__ void band1(const Dev& d, int j, Win W, const Wins<ND>
   const YT* __restrict__ yp = reinterpret_cast<const YT*>(d.y) + yix(d.rows, base, j);
   const uint16_t* __restrict__ cp =
       reinterpret_cast<const uint16_t*>(d.cov) + yix(d.rows, base, j);
-  double s = 0.0;
+  // independent partial sums: the rows' DADDs do not wait on each other
+  constexpr int NACC = SEIS_BAND_ACC;
+  double sa[NACC];
+#pragma unroll
+  for (int k = 0; k < NACC; ++k) sa[k] = 0.0;
   int mx = 0;
-  auto consume = [&](const int (&c)[RU], const YT (&yv)[RU], int i0) {
-#pragma unroll
-    for (int k = 0; k < RU; ++k) {
-      int cc = c[k];
-#pragma unroll
-      for (int q = 0; q < ND; ++q) cc += sg[q] * inw(base + i0 + k, D.w[q]);
-      mx = max(mx, cc);
-      const bool in = (unsigned)(i0 + k - sh) < (unsigned)len;
-      const int idx = in ? ts_idx(min(cc, TBL - 3), code) : kTsZero;
-      const double2 e = Ts[idx];
-      const double yy = (double)yv[k];
-      s += fma(-(yy * yy), e.y, e.x);
-    }
-  };
-#if SEIS_BAND_PIPE
-  // two row batches in flight: the next batch's loads are issued before the
-  // current batch is consumed
-  int ca[RU], cb[RU];
-  YT ya[RU], yb[RU];
-#pragma unroll
-  for (int k = 0; k < RU; ++k) {
-    ca[k] = (int)__ldg(cp + k * 32);
-    ya[k] = __ldg(yp + k * 32);
-  }
-  for (int i0 = 0;;) {
-    if (i0 + RU < trips) {
-#pragma unroll
-      for (int k = 0; k < RU; ++k) {
-        cb[k] = (int)__ldg(cp + (RU + k) * 32);
-        yb[k] = __ldg(yp + (RU + k) * 32);
-      }
-    }
-    consume(ca, ya, i0);
-    cp += RU * 32;
-    yp += RU * 32;
-    i0 += RU;
-    if (i0 >= trips) break;
-    if (i0 + RU < trips) {
-#pragma unroll
-      for (int k = 0; k < RU; ++k) {
-        ca[k] = (int)__ldg(cp + (RU + k) * 32);
-        ya[k] = __ldg(yp + (RU + k) * 32);
-      }
-    }
-    consume(cb, yb, i0);
-    cp += RU * 32;
-    yp += RU * 32;
-    i0 += RU;
-    if (i0 >= trips) break;
-  }
-#else
   for (int i0 = 0; i0 < trips; i0 += RU) {
     int c[RU];
     YT yv[RU];
@@ -301,9 +254,22 @@ __device__ __forceinline__ void band1(const Dev& d, int j, Win W, const Wins<ND>
     }
     cp += RU * 32;
     yp += RU * 32;
-    consume(c, yv, i0);
+#pragma unroll
+    for (int k = 0; k < RU; ++k) {
+      int cc = c[k];
+#pragma unroll
+      for (int q = 0; q < ND; ++q) cc += sg[q] * inw(base + i0 + k, D.w[q]);
+      mx = max(mx, cc);
+      const bool in = (unsigned)(i0 + k - sh) < (unsigned)len;
+      const int idx = in ? ts_idx(min(cc, TBL - 3), code) : kTsZero;
+      const double2 e = Ts[idx];
+      const double yy = (double)yv[k];
+      sa[k % NACC] += fma(-(yy * yy), e.y, e.x);
+    }
   }
-#endif
+  double s = sa[0];
+#pragma unroll
+  for (int k = 1; k < NACC; ++k) s += sa[k];
   if (__any_sync(0xffffffffu, mx >= TBL - 3)) {
     s = 0.0;  // slow exact pass with the global table
     const YT* y0 = reinterpret_cast<const YT*>(d.y) + yix(d.rows, 0, j);
