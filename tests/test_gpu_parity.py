@@ -518,3 +518,14 @@ def test_capacity_and_region_limits_fail_loudly(E, oc):
     eng2.set_hypothesis(E.Events(many.events.ids, many.events.x, many.events.t, many.events.arr))
     with pytest.raises(RuntimeError, match="per-region event limit"):
         eng2.run_chromatic(E.SamplerConfig(algorithm="serial", steps_per_epoch=10, epochs=1))
+
+
+def test_production_dense_regions_generic_band(E, oc):
+    """many events per region and long chains: a region's own diff grows past
+    four effective windows per station, the generic band path (density.hpp:
+    263-301 with the frozen view) against the oracle."""
+    m = O.Model(lambda_rate=48 / 240.0)
+    w = oc.sample_world(m, 21)
+    s = O.Sampler(steps_per_epoch=400, epochs=3, n_regions=4, seed=8, dynamic=1, rng_mode=1)
+    tr, ro = _prod_vs_oracle(E, oc, m, w, s, init=w.events)
+    assert tr.final.ids.size > 20
