@@ -1529,8 +1529,14 @@ struct seis_engine {
   long long* snap_rec = nullptr;  // [max_snaps][2] {offset, count}
   int64_t snap_rec_cap = 0;
   std::vector<int64_t> snap_steps;
+  // per-call device scratch, kept between calls (one call at a time per
+  // engine; every call ends with a stream sync): no cudaMalloc/cudaFree on
+  // the run path
+  std::vector<std::pair<void*, size_t>> scratch;
+  size_t scratch_next = 0;
 
   ~seis_engine() {
+    for (auto& b : scratch) cudaFree(b.first);
     cudaFree(stations);
     cudaFree(y);
     cudaFree(cov);
@@ -1564,10 +1570,33 @@ struct seis_engine {
 
 namespace {
 
+void scratch_reset(seis_engine* e) { e->scratch_next = 0; }
+
+// the next scratch buffer of this call, grown when too small
+void* scratch_get(seis_engine* e, size_t bytes) {
+  bytes = std::max<size_t>(bytes, 256);
+  const size_t i = e->scratch_next++;
+  if (i == e->scratch.size()) e->scratch.push_back({nullptr, 0});
+  auto& b = e->scratch[i];
+  if (b.second < bytes) {
+    if (b.first) cudaFree(b.first);
+    b.first = nullptr;
+    b.second = 0;
+    ck(cudaMalloc(&b.first, bytes), "cudaMalloc scratch");
+    b.second = bytes;
+  }
+  return b.first;
+}
+
+template <typename T>
+T* scratch_of(seis_engine* e, size_t n) {
+  return static_cast<T*>(scratch_get(e, n * sizeof(T)));
+}
+
 void upload_signals(seis_engine* e, const void* signals) {
   const size_t esz = e->dtype == SEIS_F64 ? 8 : 4;
-  void* tmp = nullptr;
-  ck(cudaMalloc(&tmp, (size_t)e->S * e->n * esz), "cudaMalloc");
+  scratch_reset(e);
+  void* tmp = scratch_get(e, (size_t)e->S * e->n * esz);
   ck(cudaMemcpyAsync(tmp, signals, (size_t)e->S * e->n * esz, cudaMemcpyHostToDevice, e->stream),
      "H2D signals");
   dim3 grid((e->n + 31) / 32, (e->S_pad + 31) / 32), block(32, 8);
@@ -1581,7 +1610,6 @@ void upload_signals(seis_engine* e, const void* signals) {
                                                       e->n, e->n + kRowPad);
   ck(cudaGetLastError(), "k_transpose");
   ck(cudaStreamSynchronize(e->stream), "sync");
-  cudaFree(tmp);
 }
 
 Ctl read_ctl(seis_engine* e) {
@@ -1858,8 +1886,9 @@ int seis_set_hypothesis(seis_engine* e, int64_t N, const uint64_t* ids, const do
       for (int64_t i = 0; i < N; ++i) slot_of_row[row[i]] = (int)i;
       const int64_t chunk = std::max<int64_t>(
           1, std::min<int64_t>({N, ((int64_t)512 << 20) / ((int64_t)e->S * 8), 65535}));
-      double* raw = dalloc<double>((size_t)chunk * e->S);
-      int* dslot = dalloc<int>(N);
+      scratch_reset(e);
+      double* raw = scratch_of<double>(e, (size_t)chunk * e->S);
+      int* dslot = scratch_of<int>(e, N);
       ck(cudaMemcpyAsync(dslot, slot_of_row.data(), (size_t)N * 4, cudaMemcpyHostToDevice,
                          e->stream),
          "H2D");
@@ -1873,8 +1902,6 @@ int seis_set_hypothesis(seis_engine* e, int64_t N, const uint64_t* ids, const do
         ck(cudaGetLastError(), "k_scatter_arrivals");
       }
       ck(cudaStreamSynchronize(e->stream), "sync");
-      cudaFree(raw);
-      cudaFree(dslot);
     }
     if (nf) ck(cudaMemcpy(e->free_stack, fs.data(), (size_t)nf * 4, cudaMemcpyHostToDevice), "H2D");
     Ctl c{};
@@ -1916,7 +1943,8 @@ int seis_get_hypothesis(seis_engine* e, int64_t cap, int64_t* n, uint64_t* ids, 
     if (arrivals) {  // in chunks of <= 512 MiB
       const int64_t chunk = std::max<int64_t>(
           1, std::min<int64_t>({m, ((int64_t)512 << 20) / ((int64_t)e->S * 8), 65535}));
-      double* buf = dalloc<double>((size_t)chunk * e->S);
+      scratch_reset(e);
+      double* buf = scratch_of<double>(e, (size_t)chunk * e->S);
       for (int64_t r0 = 0; r0 < m; r0 += chunk) {
         const int64_t nr = std::min(chunk, m - r0);
         dim3 grid((unsigned)std::min(64, (e->S + 255) / 256), (unsigned)nr);
@@ -1928,7 +1956,6 @@ int seis_get_hypothesis(seis_engine* e, int64_t cap, int64_t* n, uint64_t* ids, 
            "D2H arrivals");
       }
       ck(cudaStreamSynchronize(e->stream), "sync");
-      cudaFree(buf);
     }
   });
 }
@@ -2147,13 +2174,10 @@ static int run_driver(seis_engine* e, const seis_sampler_cfg* sc, int32_t mode,
                       int64_t n_tape_arr, seis_step_out* step_out, int64_t row_cap,
                       int64_t* row_step, double* row_log_joint, int64_t* row_count,
                       seis_run_stats* stats, bool serial) {
-  std::vector<void*> tmp;
+  scratch_reset(e);
   std::vector<cudaEvent_t> evs;
   auto alloc = [&](size_t bytes) {
-    void* p = nullptr;
-    ck(cudaMalloc(&p, bytes ? bytes : 1), "cudaMalloc");
-    tmp.push_back(p);
-    return p;
+    return scratch_get(e, bytes);
   };
   const int rc = guarded([&] {
     // SamplerConfig::validate + MoveDistribution::validate (samplers.hpp:59-70,
@@ -2473,7 +2497,6 @@ static int run_driver(seis_engine* e, const seis_sampler_cfg* sc, int32_t mode,
     }
   });
   for (auto ev : evs) cudaEventDestroy(ev);
-  for (void* p : tmp) cudaFree(p);
   return rc;
 }
 
@@ -2506,12 +2529,9 @@ extern "C" int seis_run_naive(seis_engine* e, const seis_sampler_cfg* sc, int32_
                               int64_t n_tape_arr, seis_step_out* step_out, int64_t row_cap,
                               int64_t* row_step, double* row_log_joint, int64_t* row_count,
                               seis_run_stats* stats) {
-  std::vector<void*> tmp;
+  scratch_reset(e);
   auto alloc = [&](size_t bytes) {
-    void* p = nullptr;
-    ck(cudaMalloc(&p, bytes ? bytes : 1), "cudaMalloc");
-    tmp.push_back(p);
-    return p;
+    return scratch_get(e, bytes);
   };
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, evp0 = nullptr, evp1 = nullptr;
   const int rc = guarded([&] {
@@ -2701,6 +2721,5 @@ extern "C" int seis_run_naive(seis_engine* e, const seis_sampler_cfg* sc, int32_
   });
   for (cudaEvent_t ev : {ev0, ev1, evp0, evp1})
     if (ev) cudaEventDestroy(ev);
-  for (void* p : tmp) cudaFree(p);
   return rc;
 }

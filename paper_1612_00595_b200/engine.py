@@ -548,15 +548,27 @@ class Engine:
         _check(self.L.seis_set_hypothesis(self.h, len(ids), _p(ids), _p(x), _p(t), _p(a)),
                self.L)
 
-    def get_hypothesis(self, arrivals: bool = True) -> Events:
+    def get_hypothesis(self, arrivals: bool = True, out: Events | None = None) -> Events:
+        """The resident hypothesis (id order). `out`: caller-owned buffers (for
+        example pinned host memory) with room for the events; the result views
+        their first N rows."""
         n = i64(0)
         _check(self.L.seis_get_hypothesis(self.h, 0, C.byref(n), None, None, None, None), self.L)
         N = n.value
         S = self.config.n_stations()
-        ids = np.zeros(max(N, 1), np.uint64)
-        x = np.zeros(max(N, 1))
-        t = np.zeros(max(N, 1))
-        a = np.zeros((max(N, 1), S)) if arrivals else None
+        if out is not None:
+            if len(out.ids) < N or (arrivals and out.arrivals.shape[0] < N):
+                raise ValueError(f"get_hypothesis: out holds fewer than {N} events")
+            ids, x, t = out.ids, out.x, out.t
+            a = out.arrivals if arrivals else None
+            for v in (ids, x, t) + ((a,) if arrivals else ()):
+                if not v.flags.c_contiguous:
+                    raise ValueError("get_hypothesis: out arrays must be C-contiguous")
+        else:
+            ids = np.zeros(max(N, 1), np.uint64)
+            x = np.zeros(max(N, 1))
+            t = np.zeros(max(N, 1))
+            a = np.zeros((max(N, 1), S)) if arrivals else None
         _check(self.L.seis_get_hypothesis(self.h, N, C.byref(n), _p(ids), _p(x), _p(t),
                                           _p(a) if arrivals else None), self.L)
         return Events(ids[:N], x[:N], t[:N], a[:N] if arrivals else None)
