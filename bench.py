@@ -370,11 +370,8 @@ def main():
         h2d = sig.nbytes + ev.N * (24 + 8 * S_)
         d2h = 0
         e2e_steps = max(3, min(args.steps, 10))
-        barrier(dist)
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        props = 0
-        for i in range(e2e_steps):
+
+        def e2e_step(i):
             eng.upload_signals(pin_np)
             eng.set_hypothesis(p_in)
             tr = eng.run_chromatic(sampler_for(c, seed0 + 500 + i), final=False, row_cap=4)
@@ -382,8 +379,17 @@ def main():
                 fin = eng.get_hypothesis(out=p_out)
             except ValueError:  # the hypothesis outgrew the pinned buffer
                 fin = eng.get_hypothesis()
-            props += tr.total_steps
-            d2h = len(fin.ids) * (24 + 8 * S_)
+            return tr.total_steps, len(fin.ids)
+
+        e2e_step(-1)  # untimed: the engine's per-call scratch reaches its size
+        barrier(dist)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        props = 0
+        for i in range(e2e_steps):
+            n_steps, n_final = e2e_step(i)
+            props += n_steps
+            d2h = n_final * (24 + 8 * S_)
         torch.cuda.synchronize()
         wall = reduce_max(dist, time.perf_counter() - t0)
         res["e2e"] = {"value": reduce_sum(dist, props) / wall, "unit": "proposals/s",
