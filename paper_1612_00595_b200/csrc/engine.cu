@@ -359,7 +359,6 @@ __global__ void __launch_bounds__(NTT, MINB)
   __shared__ int s_nown, s_np, s_abort, s_tmp, s_adv, s_accq;
   __shared__ unsigned long long s_births;
   __shared__ double s_delta[MSPEC], s_logr[MSPEC], s_prior[2];
-  __shared__ int s_item;
   __shared__ double s_logi_k[MAXOWN + 2];   // log(i), i <= MAXOWN + 1 (proposal terms)
   // dynamic: [LOGIWIN] log(i), i in [N - LOGIWIN/2, N + LOGIWIN/2), then the
   // per-lane partial sums of the tile-major pass
@@ -517,7 +516,6 @@ __global__ void __launch_bounds__(NTT, MINB)
       tc = now;
     }
     if (tid == 0) {
-      s_item = 0;
       const long long n0 = s_nlocal;
       const long long wb = n0 + 1 - logi_base, wd = n0 - logi_base;
       const double lb = (wb >= 0 && wb < LOGIWIN) ? s_logi_n[wb] : d.logi[n0 + 1];

@@ -118,11 +118,6 @@ __device__ __forceinline__ double term_fast(const double2* Ts, double y, int c, 
   return fma(-(y * y), e.y, e.x);
 }
 
-#ifndef SEIS_SCATTER_SINGLE
-#define SEIS_SCATTER_SINGLE 1
-#endif
-constexpr bool kScatterSingle = SEIS_SCATTER_SINGLE;
-
 template <int N>
 struct Wins {
   Win w[N > 0 ? N : 1];
