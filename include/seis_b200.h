@@ -58,7 +58,7 @@ typedef struct {
   double lambda_rate, T, x_max, v, sigma_arrival, t_s, var_noise, var_event, sample_rate;
 } seis_model_cfg;
 
-/* reference SamplerConfig (samplers.hpp:47-58) for the chromatic drivers */
+/* reference SamplerConfig (samplers.hpp:47-58); the algorithm is the entry point called */
 typedef struct {
   int64_t steps_per_epoch; /* k steps per region between barriers */
   int64_t epochs;          /* sweeps */
