@@ -157,7 +157,8 @@ class ModelConfig:
 
 @dataclass
 class SamplerConfig:
-    """reference SamplerConfig (samplers.hpp:47-58) for every driver (algorithm serial, naive, chromatic-static, chromatic-dynamic)."""
+    """reference SamplerConfig (samplers.hpp:47-58) for every driver:
+    algorithm serial, naive, chromatic-static or chromatic-dynamic."""
     algorithm: str = "chromatic-static"
     steps_per_epoch: int = 500
     epochs: int = 100
