@@ -356,7 +356,7 @@ __global__ void __launch_bounds__(NTT, MINB)
 
   __shared__ int red_cnt[NWT][MSPEC];
   __shared__ int s_w[NWT];
-  __shared__ int s_nown, s_np, s_abort, s_tmp, s_adv, s_accq;
+  __shared__ int s_nown, s_np, s_abort, s_tmp, s_adv, s_accq, s_dc_dirty;
   __shared__ unsigned long long s_births;
   __shared__ double s_delta[MSPEC], s_logr[MSPEC], s_prior[2];
   __shared__ double s_logi_k[MAXOWN + 2];   // log(i), i <= MAXOWN + 1 (proposal terms)
@@ -401,6 +401,7 @@ __global__ void __launch_bounds__(NTT, MINB)
   if (tid == 0) {
     s_nown = 0;
     s_abort = 0;
+    s_dc_dirty = 1;
   }
   if (tid < 16) s_tprof[tid >> 3][tid & 7] = 0ull;  // kernels.cuh
   __syncthreads();
@@ -472,7 +473,7 @@ __global__ void __launch_bounds__(NTT, MINB)
   // thread-0 chain state lives in shared memory: registers are allocated for
   // every thread, and the scoring passes need them more
   __shared__ struct {
-    long long n_local, tc, tprof[6];
+    long long n_local, tc, t0, tprof[6];
     unsigned long long births, n_acc, n_scored, n_arr, n_changed, n_spec;
     int nown, np, nlfree;
   } z;
@@ -495,6 +496,7 @@ __global__ void __launch_bounds__(NTT, MINB)
     births = n_acc = n_scored = n_arr = n_changed = n_spec = 0;
     for (int q = 0; q < 6; ++q) tprof[q] = 0;
     tc = clock64();
+    z.t0 = tc;
   }
   const unsigned long long id_base =
       pa.naive ? ((unsigned long long)region + 1ull) << 32  // samplers.hpp:349
@@ -528,6 +530,10 @@ __global__ void __launch_bounds__(NTT, MINB)
       s_prior[0] = pb;
       s_prior[1] = pdth;
     }
+    // the round's diff windows per station (proposal-major pass): rebuilt only
+    // after an accept changed the region's diff, alongside generation
+    const bool use_dcache = (d.S_pad + 31) / 32 < 4 * NWT && d.S_pad <= kDiffCache && d.n < 65535;
+    const bool dc_build = use_dcache && s_np > 0 && s_dc_dirty;
     if (warp < m && lane == 0) {  // one lane per warp: move types do not diverge
       const int step = i0 + warp;
       gen_proposal<MODE>(d, sp, pa, prop[buf][warp], own, s_nown, region, rlo, rhi, rclosed,
@@ -546,18 +552,16 @@ __global__ void __launch_bounds__(NTT, MINB)
       acc_arr[q][tid] = 0.0;
       acc_cnt[q][tid] = 0;
     }
-    __syncthreads();  // S1: proposals ready
+    if (dc_build) {
+      const int np_c = s_np;
+      for (int j = tid; j < d.S_pad; j += NTT) diff_station(d, j, np_c, pold, pnew, dcache[j]);
+    }
+    __syncthreads();  // S1: proposals (and diff windows) ready
     if (tid == 0) {
       const long long now = clock64();
       tprof[0] += now - tc;
       tc = now;
-    }
-    const bool use_dcache = (d.S_pad + 31) / 32 < 4 * NWT && d.S_pad <= kDiffCache && d.n < 65535;
-    if (use_dcache && s_np > 0) {
-      // the round's diff windows per station, once for every proposal's items
-      const int np_c = s_np;
-      for (int j = tid; j < d.S_pad; j += NTT) diff_station(d, j, np_c, pold, pnew, dcache[j]);
-      __syncthreads();
+      s_dc_dirty = 0;
     }
     {
       const int np_now = s_np;
@@ -598,7 +602,7 @@ __global__ void __launch_bounds__(NTT, MINB)
             in.whi = win_hi;
             double sig = 0.0, arr = 0.0;
             int cnt = 0;
-            score_item<MODE, YT>(d, P, in, tile, np_now, pold, pnew, &X, Ts, sig, arr, cnt);
+            score_item<MODE, YT>(d, P, in, tile, np_now, pold, pnew, X, true, Ts, sig, arr, cnt);
             // per-lane partial sums; the warp reduces them once per round
             acc_sig[q][tid] += sig;
             acc_arr[q][tid] += arr;
@@ -666,16 +670,15 @@ __global__ void __launch_bounds__(NTT, MINB)
           in.wlo = win_lo;
           in.whi = win_hi;
           DiffW X;
-          const DiffW* Xp = nullptr;
           if (use_dcache) {
             if (np_now > 0) {
               diff_from_cache(dcache[tile * 32 + lane], X);
             } else {
               X.nwmax = 0;
             }
-            Xp = &X;
           }
-          score_item<MODE, YT>(d, P, in, tile, np_now, pold, pnew, Xp, Ts, sig, arr, cnt);
+          score_item<MODE, YT>(d, P, in, tile, np_now, pold, pnew, X, use_dcache, Ts, sig, arr,
+                               cnt);
         }
         if (cur_q >= 0) {
           sig = warp_sum(sig);
@@ -883,6 +886,7 @@ __global__ void __launch_bounds__(NTT, MINB)
           atomicAdd(&ctl->id_mismatch, 1ull);
         accq = q;
         adv = q + 1;
+        s_dc_dirty = 1;
         break;
       }
       n_spec += (unsigned long long)(m - adv);
@@ -1028,6 +1032,9 @@ __global__ void __launch_bounds__(NTT, MINB)
     atomicAdd(&ctl->accepted, n_acc);
     atomicAdd(&ctl->speculative, n_spec);
     for (int q = 0; q < 6; ++q) atomicAdd(&ctl->prof[q], (unsigned long long)tprof[q]);
+    const unsigned long long dur = (unsigned long long)(clock64() - z.t0);
+    atomicMax(&ctl->prof[6], dur);  // slowest region chain of the run
+    atomicAdd(&ctl->prof[7], dur);
     for (int q = 0; q < 16; ++q) atomicAdd(&ctl->tprof[q >> 3][q & 7], s_tprof[q >> 3][q & 7]);
   }
 }
@@ -1248,8 +1255,10 @@ __global__ void __launch_bounds__(NT, 1)
   double sig = 0.0, arr = 0.0;
   int cnt = 0;
   const int T_per = (d.S_pad + 31) / 32;
+  DiffW X0;  // no own diff: the batch scores against the resident hypothesis
+  X0.nwmax = 0;
   for (int t = warp; t < T_per; t += NW)
-    score_item<1, YT>(d, P, in, t, 0, nullptr, nullptr, nullptr, Ts, sig, arr, cnt);
+    score_item<1, YT>(d, P, in, t, 0, nullptr, nullptr, X0, true, Ts, sig, arr, cnt);
   sig = warp_sum(sig);
   arr = warp_sum(arr);
   if (lane == 0) {
@@ -2464,8 +2473,8 @@ static int run_driver(seis_engine* e, const seis_sampler_cfg* sc, int32_t mode,
                     cudaMemcpyDeviceToHost),
          "D2H out");
     if (getenv("SEIS_PROF"))
-      fprintf(stderr, "[seis prof] cycles: gen %llu items %llu decide %llu (parallel part %llu) writeback %llu rounds %llu\n",
-              c.prof[0], c.prof[1], c.prof[2], c.prof[5], c.prof[3], c.prof[4]);
+      fprintf(stderr, "[seis prof] cycles: gen %llu items %llu decide %llu (parallel part %llu) writeback %llu rounds %llu; region chains: max %llu sum %llu\n",
+              c.prof[0], c.prof[1], c.prof[2], c.prof[5], c.prof[3], c.prof[4], c.prof[6], c.prof[7]);
     if (getenv("SEIS_PROF"))
       for (int q = 0; q < 8; ++q)
         fprintf(stderr, "[seis prof] type %d: items %llu warp-cycles/item %.0f\n", q,

@@ -502,7 +502,7 @@ __device__ __forceinline__ void diff_from_cache(const DiffS& c, DiffW& X) {
 template <int NR, int NA, typename YT>
 __device__ __forceinline__ void station_item(const Dev& d, const Prop& P, const PassIn& in,
                                              int j, int np, const int* pold, const int* pnew,
-                                             const DiffW* Xp, const double2* Ts, double& sig,
+                                             DiffW X, bool haveX, const double2* Ts, double& sig,
                                              double& arr, int& cnt) {
   const long long t_item = kProfItems ? clock64() : 0;
   const bool v = j < d.S;
@@ -572,9 +572,9 @@ __device__ __forceinline__ void station_item(const Dev& d, const Prop& P, const 
   if (blo >= bhi) return;
   // the tile-major pass hands in the tile's diff windows; otherwise they are
   // built here, only for stations the proposal changes
-  DiffW Xl;
-  if (!Xp) diff_windows(d, j, np, pold, pnew, Xl);
-  const DiffW& X = Xp ? *Xp : Xl;
+  // (by value: a pointer or a reference selected between two DiffW objects
+  // would put them in local memory)
+  if (!haveX) diff_windows(d, j, np, pold, pnew, X);
   const Wins<4>& D = X.D;
   const int(&sg)[4] = X.sg;
   const int nwmax = X.nwmax;
@@ -668,7 +668,8 @@ __device__ __forceinline__ void arrival_item(const Dev& d, const Prop& P, const 
 template <int MODE, typename YT>
 __device__ __forceinline__ void score_item(const Dev& d, const Prop& P, const PassIn& in,
                                            int tile, int np, const int* pold,
-                                           const int* pnew, const DiffW* X, const double2* Ts,
+                                           const int* pnew, const DiffW& X, bool haveX,
+                                           const double2* Ts,
                                            double& sig, double& arr, int& cnt) {
   if (P.skip) return;
   const int j = tile * 32 + (threadIdx.x & 31);
@@ -678,13 +679,13 @@ __device__ __forceinline__ void score_item(const Dev& d, const Prop& P, const Pa
   }
   const int shape = P.nr * 3 + P.na;
   if (shape == 1)  // birth
-    station_item<0, 1, YT>(d, P, in, j, np, pold, pnew, X, Ts, sig, arr, cnt);
+    station_item<0, 1, YT>(d, P, in, j, np, pold, pnew, X, haveX, Ts, sig, arr, cnt);
   else if (shape == 3)  // death
-    station_item<1, 0, YT>(d, P, in, j, np, pold, pnew, X, Ts, sig, arr, cnt);
+    station_item<1, 0, YT>(d, P, in, j, np, pold, pnew, X, haveX, Ts, sig, arr, cnt);
   else if (shape == 4)  // location / arrival
-    station_item<1, 1, YT>(d, P, in, j, np, pold, pnew, X, Ts, sig, arr, cnt);
+    station_item<1, 1, YT>(d, P, in, j, np, pold, pnew, X, haveX, Ts, sig, arr, cnt);
   else  // joint pair, and any other change of <= 2 removed / 2 added events
-    station_item<2, 2, YT>(d, P, in, j, np, pold, pnew, X, Ts, sig, arr, cnt);
+    station_item<2, 2, YT>(d, P, in, j, np, pold, pnew, X, haveX, Ts, sig, arr, cnt);
 }
 
 }  // namespace seis
