@@ -1809,7 +1809,7 @@ int seis_engine_create(const seis_model_cfg* cfg, const double* stations, int64_
     d.T = cfg->T;
     const double var_a = cfg->sigma_arrival * cfg->sigma_arrival;
     d.c0_arr = -0.5 * (kLog2Pi + std::log(var_a));
-    d.twovar_arr = 2.0 * var_a;
+    d.inv_twovar_arr = 1.0 / (2.0 * var_a);
     d.log_lambda_T = std::log(cfg->lambda_rate * cfg->T);
     d.lxa = -std::log(cfg->x_max) - std::log(cfg->T);
     d.log_xmax = std::log(cfg->x_max);

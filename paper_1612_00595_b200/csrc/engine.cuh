@@ -62,7 +62,7 @@ struct Dev {
   int S, S_pad, P2, n;
   int rows;                        // n + kRowPad
   double rate, t_s, v, sigma, x_max, T;
-  double c0_arr, twovar_arr;       // log_gaussian constants for sigma_arrival
+  double c0_arr, inv_twovar_arr;   // log_gaussian constants for sigma_arrival
   double log_lambda_T, lxa;        // log(lambda T), -log(x_max) - log(T)
   double log_xmax;
   const double* stations;          // [S_pad]
@@ -194,9 +194,11 @@ __device__ __forceinline__ double arrival_mean(const Dev& d, double x, double t,
 
 __device__ __forceinline__ double arr_logpdf(const Dev& d, double a, double mean) {
   // log_gaussian(a, mean, sigma^2), density.hpp:15-18 with host-computed
-  // -0.5 (log 2pi + log sigma^2) and 2 sigma^2
+  // -0.5 (log 2pi + log sigma^2) and 1 / (2 sigma^2): the division becomes a
+  // multiplication (identical when 2 sigma^2 is a power of two, as for the
+  // reference default sigma_arrival = 2; otherwise within 1 ulp per term)
   const double dd = a - mean;
-  return d.c0_arr - dd * dd / d.twovar_arr;
+  return d.c0_arr - dd * dd * d.inv_twovar_arr;
 }
 
 }  // namespace seis
