@@ -509,7 +509,7 @@ __global__ void __launch_bounds__(NTT, MINB)
   const int T_per = (d.S_pad + 31) / 32;  // tiles of 32 stations
   int round = 0;
   for (int i0 = 0; i0 < (int)sp.k; ++round) {
-    const int m = min(MSPEC, (int)sp.k - i0);
+    const int m = min(sp.mspec, (int)sp.k - i0);
     const int buf = round & 1;
     __syncthreads();  // S0: previous round's write-back and state are visible
     if (tid == 0) {
@@ -1810,6 +1810,7 @@ int seis_engine_create(const seis_model_cfg* cfg, const double* stations, int64_
     const double var_a = cfg->sigma_arrival * cfg->sigma_arrival;
     d.c0_arr = -0.5 * (kLog2Pi + std::log(var_a));
     d.inv_twovar_arr = 1.0 / (2.0 * var_a);
+    d.inv_v = 1.0 / cfg->v;
     d.log_lambda_T = std::log(cfg->lambda_rate * cfg->T);
     d.lxa = -std::log(cfg->x_max) - std::log(cfg->T);
     d.log_xmax = std::log(cfg->x_max);
@@ -2176,6 +2177,14 @@ int seis_log_joint(seis_engine* e, double* out) {
 // The chromatic driver (run_chromatic, samplers.hpp:401-498) and, with
 // serial = true, run_serial (samplers.hpp:282-315): one region [0, T], no
 // constraint, chunks of record_every steps.
+// Speculative proposals per round (1..MSPEC); SEIS_SPEC overrides the
+// default depth for A/B measurements.
+static int spec_depth() {
+  const char* v = getenv("SEIS_SPEC");
+  const int m = v ? atoi(v) : kSpecDefault;
+  return m < 1 ? 1 : (m > MSPEC ? MSPEC : m);
+}
+
 static int run_driver(seis_engine* e, const seis_sampler_cfg* sc, int32_t mode,
                       const seis_tape_step* tape, int64_t n_tape, const double* tape_arr,
                       int64_t n_tape_arr, seis_step_out* step_out, int64_t row_cap,
@@ -2236,6 +2245,7 @@ static int run_driver(seis_engine* e, const seis_sampler_cfg* sc, int32_t mode,
     sp.step_joint = sc->step_joint;
     sp.joint_t_sd = sc->step_joint / e->cfg.v;
     sp.ncol = ncol;
+    sp.mspec = spec_depth();
     const int bcap = (int)sc->n_regions + 4;
     // every epoch's partition up front (one thread per epoch), so the timed
     // region holds no host round trip
@@ -2615,6 +2625,7 @@ extern "C" int seis_run_naive(seis_engine* e, const seis_sampler_cfg* sc, int32_
     sp.step_joint = sc->step_joint;
     sp.joint_t_sd = sc->step_joint / e->cfg.v;
     sp.ncol = 1;
+    sp.mspec = spec_depth();
     int* births_cnt = static_cast<int*>(alloc((size_t)nreg * 4));
     OutEv* births = static_cast<OutEv*>(alloc((size_t)nreg * MAXOWN * sizeof(OutEv)));
     int* diff_cnt = static_cast<int*>(alloc((size_t)nreg * 4));

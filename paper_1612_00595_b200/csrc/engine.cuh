@@ -28,6 +28,10 @@ constexpr int NT = SEIS_NT;      // threads per region CTA
 #define SEIS_MSPEC 4
 #endif
 constexpr int MSPEC = SEIS_MSPEC;  // speculative proposals evaluated per round
+// default depth at run time (<= MSPEC): at acceptance ~12 % a fourth proposal
+// is discarded speculation more often than it saves a round (measured on
+// configs 1 and 2: 3 beats 4 by 3-4 %, 2 and 1 lose); SEIS_SPEC overrides
+constexpr int kSpecDefault = 3;
 #ifndef SEIS_PROF_ITEMS
 #define SEIS_PROF_ITEMS 0
 #endif
@@ -63,6 +67,7 @@ struct Dev {
   int rows;                        // n + kRowPad
   double rate, t_s, v, sigma, x_max, T;
   double c0_arr, inv_twovar_arr;   // log_gaussian constants for sigma_arrival
+  double inv_v;                    // RN(1 / v): division by v as a reciprocal + one correction
   double log_lambda_T, lxa;        // log(lambda T), -log(x_max) - log(T)
   double log_xmax;
   const double* stations;          // [S_pad]
@@ -85,6 +90,7 @@ struct Samp {
   double logw[5];
   double step_lx, step_lt, step_arr, step_joint, joint_t_sd;
   int ncol;
+  int mspec;  // speculative proposals per round, 1..MSPEC
 };
 
 struct Table {
@@ -188,8 +194,19 @@ __device__ __forceinline__ int inw(int r, Win w) {
   return (unsigned)(r - w.lo) < (unsigned)(w.hi - w.lo) ? 1 : 0;
 }
 
+// |x - s| / v correctly rounded without a division: q0 = a * RN(1/v), the
+// exact remainder r = a - q0 v (one FMA), q = RN(q0 + r * RN(1/v)). With the
+// correctly rounded reciprocal this final step yields the correctly rounded
+// quotient (Markstein's theorem), i.e. the reference's IEEE division bit for
+// bit; tests/test_oracle.py checks it against the host division on 10^7
+// random operands per configuration.
+__device__ __forceinline__ double div_v(const Dev& d, double a) {
+  const double q0 = a * d.inv_v;
+  return fma(fma(-q0, d.v, a), d.inv_v, q0);
+}
+
 __device__ __forceinline__ double arrival_mean(const Dev& d, double x, double t, double s) {
-  return t + fabs(x - s) / d.v;  // model.hpp:73-75
+  return t + div_v(d, fabs(x - s));  // model.hpp:73-75
 }
 
 __device__ __forceinline__ double arr_logpdf(const Dev& d, double a, double mean) {

@@ -244,3 +244,49 @@ def test_serial_tape_matches_reference(oc, seed):
     order = np.argsort(c["final"].ids)
     assert np.array_equal(a["final"].ids, c["final"].ids[order])
     assert np.array_equal(a["final"].arr, c["final"].arr[order])
+
+
+_DIV_CHECK = r"""
+#include <math.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
+static uint64_t s = 0x9e3779b97f4a7c15ull;
+static uint64_t nx(void) { s ^= s << 13; s ^= s >> 7; s ^= s << 17; return s; }
+static double u01(void) { return (double)(nx() >> 11) * 0x1.0p-53; }
+int main(int argc, char** argv) {
+  long bad = 0;
+  for (int k = 1; k + 1 < argc; k += 2) {
+    const double v = strtod(argv[k], 0), span = strtod(argv[k + 1], 0), y = 1.0 / v;
+    for (long i = 0; i < 10000000; ++i) {
+      double a = u01() * span;
+      if (i & 1) a = floor(a * 1024.0) / 1024.0;  /* station-grid-like operands */
+      const double q0 = a * y, q = fma(fma(-q0, v, a), y, q0);
+      bad += q != a / v;
+    }
+  }
+  printf("%ld\n", bad);
+  return 0;
+}
+"""
+
+
+def test_division_by_reciprocal_is_exact(tmp_path):
+    """arrival_mean on the device (engine.cuh div_v) replaces |x - s| / v by
+    q0 = a RN(1/v), q = RN(q0 + (a - q0 v) RN(1/v)); bit-identical to the
+    reference's division (model.hpp:73-75) for every v of configs 0-4 and the
+    default world, 10^7 operands each over [0, x_max]."""
+    import subprocess
+    src = tmp_path / "div.c"
+    src.write_text(_DIV_CHECK)
+    exe = tmp_path / "div"
+    subprocess.run(["gcc", "-O2", "-ffp-contract=off", str(src), "-o", str(exe), "-lm"], check=True)
+    # (v, x_max): reference default (v = 2, x_max = 100) and the SURVEY 8(d)
+    # mapping v = 1.2 x_max R^2 / T of configs 0-4
+    cases = [(2.0, 100.0)]
+    for x_max, T, R in [(1000, 3600, 4), (4000, 3600, 16), (16000, 3600, 64), (16000, 1800, 128),
+                        (32000, 1024, 256)]:
+        cases.append((1.2 * x_max * R * R / T, float(x_max)))
+    args = [f"{x:.17g}" for c in cases for x in c]
+    out = subprocess.run([str(exe)] + args, check=True, capture_output=True, text=True).stdout
+    assert int(out.strip()) == 0
