@@ -357,6 +357,7 @@ __global__ void __launch_bounds__(NTT, MINB)
   __shared__ int red_cnt[NWT][MSPEC];
   __shared__ int s_w[NWT];
   __shared__ int s_nown, s_np, s_abort, s_tmp, s_adv, s_accq, s_dc_dirty;
+  __shared__ int s_specok;  // this round's proposals were generated during the last decision
   __shared__ unsigned long long s_births;
   __shared__ double s_delta[MSPEC], s_logr[MSPEC], s_prior[2];
   __shared__ double s_logi_k[MAXOWN + 2];   // log(i), i <= MAXOWN + 1 (proposal terms)
@@ -402,6 +403,7 @@ __global__ void __launch_bounds__(NTT, MINB)
     s_nown = 0;
     s_abort = 0;
     s_dc_dirty = 1;
+    s_specok = 0;
   }
   if (tid < 16) s_tprof[tid >> 3][tid & 7] = 0ull;  // kernels.cuh
   __syncthreads();
@@ -534,7 +536,7 @@ __global__ void __launch_bounds__(NTT, MINB)
     // after an accept changed the region's diff, alongside generation
     const bool use_dcache = (d.S_pad + 31) / 32 < 4 * NWT && d.S_pad <= kDiffCache && d.n < 65535;
     const bool dc_build = use_dcache && s_np > 0 && s_dc_dirty;
-    if (warp < m && lane == 0) {  // one lane per warp: move types do not diverge
+    if (warp < m && lane == 0 && !(MODE == 0 && s_specok)) {  // one lane per warp: move types do not diverge
       const int step = i0 + warp;
       gen_proposal<MODE>(d, sp, pa, prop[buf][warp], own, s_nown, region, rlo, rhi, rclosed,
                          (int)(pa.step_base + step),
@@ -697,6 +699,19 @@ __global__ void __launch_bounds__(NTT, MINB)
       const long long now = clock64();
       tprof[1] += now - tc;
       tc = now;
+    }
+    // Production mode: while warp 0 decides, lanes 0 of warps 1..m generate
+    // the next round's proposals assuming this round accepts nothing (the
+    // common case: the state, and so every draw, is then unchanged). They are
+    // used only if that holds; after an accept they are regenerated.
+    const int i_next = i0 + m;
+    const int m_next = MODE == 0 ? min(sp.mspec, (int)sp.k - i_next) : 0;
+    if (MODE == 0 && warp >= 1 && warp <= m_next && lane == 0) {
+      const int step = i_next + warp - 1;
+      gen_proposal<MODE>(d, sp, pa, prop[buf ^ 1][warp - 1], own, s_nown, region, rlo, rhi,
+                         rclosed, (int)(pa.step_base + step),
+                         pa.tape_base + (long long)slot_idx * sp.k + step, id_base + s_births,
+                         &ctl->err);
     }
     if (warp == 0) {
       // per-proposal delta / log_r / decision against the round's state, in
@@ -904,6 +919,7 @@ __global__ void __launch_bounds__(NTT, MINB)
       }
       s_adv = adv;
       s_accq = accq;
+      s_specok = (MODE == 0 && accq < 0 && m_next > 0) ? 1 : 0;
       s_nown = nown;
       s_np = np;
       s_births = births;

@@ -79,7 +79,8 @@ def load_library(path: str | None = None) -> C.CDLL:
     global _LIB
     if _LIB is not None and path is None:
         return _LIB
-    path = path or _build.LIB
+    # SEIS_LIB: an alternative build of the same library (A/B measurements)
+    path = path or os.environ.get("SEIS_LIB") or _build.LIB
     if not os.path.exists(path):
         raise ImportError(f"{path} missing: run `python -m paper_1612_00595_b200.build` "
                           "(the engine has no CPU fallback)")
