@@ -177,12 +177,10 @@ SEIS_HD float seis_cos2pif(float u) {
   s = seis_fmaf(t2, s, -0x1.555556p-3f);
   s = seis_fmaf(t2, s, 1.0f);
   s = s * th;
-  switch (k & 3) {
-    case 0: return c;
-    case 1: return -s;
-    case 2: return -c;
-    default: return s;
-  }
+  /* quadrant k & 3 -> c, -s, -c, s: selects, not a switch (lanes of a warp
+   * sit in different quadrants) */
+  const float v = (k & 1) ? s : c;
+  return ((k + 1) & 2) ? -v : v;
 }
 
 /* Standard normal from two 32-bit words: Box-Muller, cosine branch (as the
@@ -201,7 +199,10 @@ SEIS_HD float seis_bm(uint32_t w0, uint32_t w1) {
 SEIS_HD float seis_normal(uint64_t seed, uint32_t sweep, uint32_t region, uint32_t step,
                           uint32_t i) {
   const seis_u32x4 d = seis_draw(seed, sweep, region, step, SEIS_DRAW_NORMAL0 + (i >> 1));
-  return (i & 1u) ? seis_bm(d.w[2], d.w[3]) : seis_bm(d.w[0], d.w[1]);
+  /* pick the words first: neighbouring lanes (stations) have opposite parity */
+  const uint32_t a = (i & 1u) ? d.w[2] : d.w[0];
+  const uint32_t b = (i & 1u) ? d.w[3] : d.w[1];
+  return seis_bm(a, b);
 }
 
 /* normals 2i and 2i+1 of a step from one Philox call */
