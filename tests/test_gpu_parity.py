@@ -529,3 +529,20 @@ def test_production_dense_regions_generic_band(E, oc):
     s = O.Sampler(steps_per_epoch=400, epochs=3, n_regions=4, seed=8, dynamic=1, rng_mode=1)
     tr, ro = _prod_vs_oracle(E, oc, m, w, s, init=w.events)
     assert tr.final.ids.size > 20
+
+
+@pytest.mark.parametrize("depth", [1, 2, 4])
+@pytest.mark.parametrize("S", [96, 2080])
+def test_production_independent_of_speculation_depth(E, oc, monkeypatch, depth, S):
+    """The speculative rounds (up to M proposals scored against one state, the
+    next round's proposals generated during the decision) must reproduce the
+    sequential chain for every depth M (SEIS_SPEC; default 3): decisions,
+    deltas and the final hypothesis equal the oracle's. S = 96 runs the
+    proposal-major item order with the per-round diff-window cache, S = 2080
+    (65 station tiles) the tile-major order."""
+    monkeypatch.setenv("SEIS_SPEC", str(depth))
+    m = _mapped_model(S=S, T=400.0, n_regions=24, x_max=4000.0, lam_events=30)
+    w = oc.sample_world(m, 11)
+    w32 = O.World(m, w.events, w.signals.astype(np.float32).astype(np.float64))
+    s = O.Sampler(steps_per_epoch=24, epochs=3, n_regions=24, seed=21, dynamic=1, rng_mode=1)
+    _prod_vs_oracle(E, oc, m, w32, s, init=w.events, dtype=np.float32)
