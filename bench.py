@@ -260,6 +260,10 @@ def main():
                     help="override steps per region per sweep (configs 3/4: the mapped k "
                          "drives the hypothesis past HBM, see DESIGN.md)")
     ap.add_argument("--capacity", type=int, default=0, help="event capacity (default 2N + 256)")
+    ap.add_argument("--start", default="truth", choices=["truth", "empty"],
+                    help="truth: steady state from the world's events (default); empty: the "
+                         "reference's own start (samplers.hpp:409), the chain evolving over "
+                         "the warm-up and timed sweeps (no e2e leg)")
     args = ap.parse_args()
     c = dict(CONFIGS[args.config])
     if args.k:
@@ -285,7 +289,8 @@ def main():
     def sweep(i):
         return eng.run_chromatic(sampler_for(c, seed0 + i), final=False, row_cap=4)
 
-    eng.set_hypothesis(truth)
+    if args.start == "truth":
+        eng.set_hypothesis(truth)
     for i in range(args.warmup):
         sweep(i)
     torch.cuda.synchronize()
@@ -325,7 +330,10 @@ def main():
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference generative model sample_world, world seed 0; "
                 f"{'fp32' if c['dtype'] == 'f32' else 'fp64'} signals)",
-        "config": {"workload": c["desc"], "start": "truth hypothesis (seis_set_hypothesis)",
+        "config": {"workload": c["desc"],
+                   "start": ("truth hypothesis (seis_set_hypothesis)" if args.start == "truth"
+                             else f"empty hypothesis, timed sweeps {args.warmup + 1}.."
+                                  f"{args.warmup + args.steps} of one chain"),
                    "parallelism": "replicas" if ws > 1 else "single",
                    "sweeps_per_s": ws * args.steps / (t_max / 1e3),
                    "scored_proposals_per_s": reduce_sum(dist, acc["scored"]) / (t_max / 1e3),
@@ -347,7 +355,7 @@ def main():
     # e2e through the C-ABI with host buffers: per step upload the observed
     # signals from pinned memory, load the start hypothesis, one sweep, read
     # the final hypothesis back
-    if not args.no_e2e:
+    if not args.no_e2e and args.start == "truth":
         pin = torch.empty(sig.size * sig.itemsize, dtype=torch.uint8, pin_memory=True)
         pin_np = pin.numpy().view(sig.dtype).reshape(sig.shape)
         pin_np[...] = sig

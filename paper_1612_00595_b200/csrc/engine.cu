@@ -660,6 +660,9 @@ __global__ void __launch_bounds__(NTT, MINB)
             cur_q = q;
           }
           const Prop& P = prop[buf][q];
+          // nothing to score: a skipped proposal, or a production arrival
+          // move outside the tile of its one station (before the cache read)
+          if (P.skip || (MODE == 0 && P.type == 3 && tile != 0)) continue;
           PassIn in;
           in.src = P.na == 0 ? SRC_NONE
                              : (MODE == 1 ? SRC_ROWS : (P.type == 0 ? SRC_BIRTH : SRC_SHIFT));
