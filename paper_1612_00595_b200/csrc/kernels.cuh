@@ -211,7 +211,7 @@ __device__ __forceinline__ void band(const Dev& d, int j, int blo, int bhi, cons
 // rows past a lane's window index the zero row of the table. cnt is the
 // window length (computed by the caller).
 #ifndef SEIS_BAND_RU
-#define SEIS_BAND_RU 21
+#define SEIS_BAND_RU 20  // = t_s * rate of the reference default: a 20-row window is one unmasked batch
 #endif
 #ifndef SEIS_BAND_ACC
 #define SEIS_BAND_ACC 1  // partial sums per lane in the dense band (more measured no faster)
