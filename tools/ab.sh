@@ -1,4 +1,6 @@
 #!/bin/bash
+# A/B of alternative builds (tools/build_variant.sh NAME -DFLAG=...), on the GPU box:
+#   bash tools/ab.sh "1 2" 2 base variant
 # A/B of variant libraries: ab.sh "configs" reps lib1 lib2 ...
 cfgs=$1; reps=$2; shift 2
 for c in $cfgs; do for r in $(seq $reps); do for v in "$@"; do
