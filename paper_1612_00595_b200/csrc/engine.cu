@@ -346,6 +346,7 @@ template <typename YT, int MODE, int NTT, int MINB>
 __global__ void __launch_bounds__(NTT, MINB)
     k_phase(const Dev d, const Samp sp, const PhaseArgs pa, Ctl* ctl, int stamp) {
   constexpr int NWT = NTT / 32;
+  static_assert(NTT == NT, "diff_cache_overflow() places the cache for NT threads");
   __shared__ double2 Ts[kTsSize];  // {dL, dI} per (dc, count) + a zero entry
   __shared__ OwnEv own[MAXOWN];
   __shared__ StartEv st[MAXOWN];
@@ -556,7 +557,9 @@ __global__ void __launch_bounds__(NTT, MINB)
     }
     if (dc_build) {
       const int np_c = s_np;
-      for (int j = tid; j < d.S_pad; j += NTT) diff_station(d, j, np_c, pold, pnew, dcache[j]);
+      DiffS4x* ovf = const_cast<DiffS4x*>(diff_cache_overflow());
+      for (int j = tid; j < d.S_pad; j += NTT)
+        diff_station(d, j, np_c, pold, pnew, dcache[j], ovf[j]);
     }
     __syncthreads();  // S1: proposals (and diff windows) ready
     if (tid == 0) {
@@ -1445,7 +1448,7 @@ thread_local std::string g_err;
 // dynamic: the log(i) window + per-lane partial sums (2 double + 1 int per
 // speculative slot and thread)
 constexpr int kPhaseSmem = LOGIWIN * (int)sizeof(double) + MSPEC * NT * (2 * 8 + 4) +
-                           kDiffCache * (int)sizeof(DiffS);
+                           kDiffCache * (int)(sizeof(DiffS) + sizeof(DiffS4x));
 
 int fail(int code, const std::string& m) {
   g_err = m;

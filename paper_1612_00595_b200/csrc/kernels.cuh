@@ -410,11 +410,12 @@ struct DiffW {
 
 // Walk the region's (start, current) pairs at station j with each batch of
 // four pairs' pool loads issued together; first four effective windows kept.
+template <int K>
 __device__ __forceinline__ int diff_collect(const Dev& d, int j, int np, const int* pold,
-                                            const int* pnew, Win (&w)[4], int (&sg)[4]) {
+                                            const int* pnew, Win (&w)[K], int (&sg)[K]) {
   int nw = 0;
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
+  for (int k = 0; k < K; ++k) {
     w[k] = empty_win();
     sg[k] = 0;
   }
@@ -437,7 +438,7 @@ __device__ __forceinline__ int diff_collect(const Dev& d, int j, int np, const i
       if (weq(wo, wn)) continue;
       if (wo.hi > wo.lo) {
 #pragma unroll
-        for (int m = 0; m < 4; ++m)
+        for (int m = 0; m < K; ++m)
           if (m == nw) {
             w[m] = wo;
             sg[m] = -1;
@@ -446,7 +447,7 @@ __device__ __forceinline__ int diff_collect(const Dev& d, int j, int np, const i
       }
       if (wn.hi > wn.lo) {
 #pragma unroll
-        for (int m = 0; m < 4; ++m)
+        for (int m = 0; m < K; ++m)
           if (m == nw) {
             w[m] = wn;
             sg[m] = 1;
@@ -460,7 +461,7 @@ __device__ __forceinline__ int diff_collect(const Dev& d, int j, int np, const i
 
 __device__ __forceinline__ void diff_windows(const Dev& d, int j, int np, const int* pold,
                                              const int* pnew, DiffW& X) {
-  const int nw = diff_collect(d, j, np, pold, pnew, X.D.w, X.sg);
+  const int nw = diff_collect<4>(d, j, np, pold, pnew, X.D.w, X.sg);
   X.nwmax = (int)__reduce_max_sync(0xffffffffu, (unsigned)nw);
 }
 
@@ -471,18 +472,41 @@ struct DiffS {
   int8_t sg[4];
   int n;
 };
+// windows 5..8 of a station (a region that has accepted several births this
+// phase, as during burn-in from an empty start), kept in a second array so
+// the common four-window path reads what it did before
+struct DiffS4x {
+  uint16_t lo[4], hi[4];
+  int8_t sg[4];
+};
 
 __device__ __forceinline__ void diff_station(const Dev& d, int j, int np, const int* pold,
-                                             const int* pnew, DiffS& o) {
-  Win w[4];
-  int sg[4];
-  o.n = diff_collect(d, j, np, pold, pnew, w, sg);
+                                             const int* pnew, DiffS& o, DiffS4x& ov) {
+  Win w[8];
+  int sg[8];
+  o.n = diff_collect<8>(d, j, np, pold, pnew, w, sg);
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     o.lo[k] = (uint16_t)w[k].lo;
     o.hi[k] = (uint16_t)w[k].hi;
     o.sg[k] = (int8_t)sg[k];
+    ov.lo[k] = (uint16_t)w[4 + k].lo;
+    ov.hi[k] = (uint16_t)w[4 + k].hi;
+    ov.sg[k] = (int8_t)sg[4 + k];
   }
+}
+
+// k_phase's per-round diff-window cache (proposal-major pass): active under
+// the same condition k_phase builds it; the overflow windows follow the
+// cache in dynamic shared memory
+__device__ __forceinline__ bool diff_cache_active(const Dev& d, int np) {
+  return np > 0 && (d.S_pad + 31) / 32 < 4 * (NT / 32) && d.S_pad <= kDiffCache && d.n < 65535;
+}
+__device__ __forceinline__ const DiffS4x* diff_cache_overflow() {
+  extern __shared__ double s_dyn_diff[];
+  return reinterpret_cast<const DiffS4x*>(
+      reinterpret_cast<const char*>(s_dyn_diff + LOGIWIN + 2 * MSPEC * NT + MSPEC * NT / 2) +
+      (size_t)kDiffCache * sizeof(DiffS));
 }
 
 __device__ __forceinline__ void diff_from_cache(const DiffS& c, DiffW& X) {
@@ -618,6 +642,23 @@ __device__ __forceinline__ void station_item(const Dev& d, const Prop& P, const 
       band<NR, NA, 2, YT>(d, j, blo, bhi, R, A, D2, sg2, Ts, sig, cnt);
   } else if (nwmax <= 4) {
     band<NR, NA, 4, YT>(d, j, blo, bhi, R, A, D, sg, Ts, sig, cnt);
+  } else if (nwmax <= 8 && haveX && diff_cache_active(d, np)) {
+    // five to eight windows at some station of the tile (a region that has
+    // accepted several births this phase, as during burn-in from an empty
+    // start): the first four from the registers, the rest from the round
+    // cache's overflow array (12x cheaper per item than band_generic)
+    const DiffS4x& ov = diff_cache_overflow()[j];
+    Wins<8> D8;
+    int sg8[8];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      D8.w[q] = D.w[q];
+      sg8[q] = sg[q];
+      D8.w[4 + q].lo = ov.lo[q];
+      D8.w[4 + q].hi = ov.hi[q];
+      sg8[4 + q] = ov.sg[q];
+    }
+    band<NR, NA, 8, YT>(d, j, blo, bhi, R, A, D8, sg8, Ts, sig, cnt);
   } else {
     band_generic<NR, NA, YT>(d, j, v, blo, bhi, R, A, np, pold, pnew, Ts, &sig, &cnt);
   }

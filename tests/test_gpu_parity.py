@@ -546,3 +546,17 @@ def test_production_independent_of_speculation_depth(E, oc, monkeypatch, depth, 
     w32 = O.World(m, w.events, w.signals.astype(np.float32).astype(np.float64))
     s = O.Sampler(steps_per_epoch=24, epochs=3, n_regions=24, seed=21, dynamic=1, rng_mode=1)
     _prod_vs_oracle(E, oc, m, w32, s, init=w.events, dtype=np.float32)
+
+
+@pytest.mark.parametrize("steps", [200, 800])
+def test_production_burn_in_from_empty_many_windows(E, oc, steps):
+    """Burn-in from the reference's empty start: regions accept many births
+    within a phase, so stations see five to eight own diff windows (the
+    eight-window band fed by the round cache's overflow array) and, with the
+    longer chains, more than eight (the generic band); every decision, delta
+    and the final hypothesis against the oracle."""
+    m = _mapped_model(S=64, T=300.0, n_regions=6, x_max=1000.0, lam_events=40)
+    w = oc.sample_world(m, 5)
+    s = O.Sampler(steps_per_epoch=steps, epochs=3, n_regions=6, seed=13, dynamic=0, rng_mode=1)
+    tr, ro = _prod_vs_oracle(E, oc, m, w, s)
+    assert tr.final.ids.size > 10
