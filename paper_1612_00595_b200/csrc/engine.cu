@@ -1906,10 +1906,12 @@ int seis_set_hypothesis(seis_engine* e, int64_t N, const uint64_t* ids, const do
     e->cur = 0;
     Table& tb = e->tab[0];
     if (N) {
-      ck(cudaMemcpy(tb.id, hid.data(), N * 8, cudaMemcpyHostToDevice), "H2D");
-      ck(cudaMemcpy(tb.x, hx.data(), N * 8, cudaMemcpyHostToDevice), "H2D");
-      ck(cudaMemcpy(tb.t, ht.data(), N * 8, cudaMemcpyHostToDevice), "H2D");
-      ck(cudaMemcpy(tb.slot, hs.data(), N * 4, cudaMemcpyHostToDevice), "H2D");
+      // stream-ordered copies from pageable vectors (each returns once staged;
+      // the vectors outlive the final synchronisation in read_ctl)
+      ck(cudaMemcpyAsync(tb.id, hid.data(), N * 8, cudaMemcpyHostToDevice, e->stream), "H2D");
+      ck(cudaMemcpyAsync(tb.x, hx.data(), N * 8, cudaMemcpyHostToDevice, e->stream), "H2D");
+      ck(cudaMemcpyAsync(tb.t, ht.data(), N * 8, cudaMemcpyHostToDevice, e->stream), "H2D");
+      ck(cudaMemcpyAsync(tb.slot, hs.data(), N * 4, cudaMemcpyHostToDevice, e->stream), "H2D");
       // arrivals in chunks of input rows (<= 512 MiB staging), each row
       // scattered to its slot
       std::vector<int> slot_of_row(N);
@@ -1931,21 +1933,22 @@ int seis_set_hypothesis(seis_engine* e, int64_t N, const uint64_t* ids, const do
         k_scatter_arrivals<<<grid, 256, 0, e->stream>>>(raw, dslot + r0, e->S, e->S_pad, e->pool);
         ck(cudaGetLastError(), "k_scatter_arrivals");
       }
-      ck(cudaStreamSynchronize(e->stream), "sync");
     }
-    if (nf) ck(cudaMemcpy(e->free_stack, fs.data(), (size_t)nf * 4, cudaMemcpyHostToDevice), "H2D");
+    if (nf)
+      ck(cudaMemcpyAsync(e->free_stack, fs.data(), (size_t)nf * 4, cudaMemcpyHostToDevice,
+                         e->stream),
+         "H2D");
     Ctl c{};
     c.n_events = (int)N;
     c.free_top = nf;
-    ck(cudaMemcpy(e->ctl, &c, sizeof c, cudaMemcpyHostToDevice), "H2D");
+    ck(cudaMemcpyAsync(e->ctl, &c, sizeof c, cudaMemcpyHostToDevice, e->stream), "H2D");
     ck(cudaMemsetAsync(e->cov, 0, (size_t)(e->n + kRowPad) * e->P2 * 4, e->stream), "memset");
     if (N) {
       dim3 grid((e->P2 + 127) / 128, (unsigned)std::min<int64_t>(N, 65535));
       k_build_cov<<<grid, 128, 0, e->stream>>>(e->d, tb, e->ctl);
       ck(cudaGetLastError(), "k_build_cov");
     }
-    ck(cudaStreamSynchronize(e->stream), "sync");
-    const Ctl after = read_ctl(e);
+    const Ctl after = read_ctl(e);  // the one synchronisation of the call
     if (after.err) {
       cov_failed = true;
       throw std::runtime_error(std::string("device: ") + err_name(after.err));
@@ -1967,9 +1970,9 @@ int seis_get_hypothesis(seis_engine* e, int64_t cap, int64_t* n, uint64_t* ids, 
     const int64_t m = std::min<int64_t>(cap, c.n_events);
     if (m <= 0) return;
     const Table& tb = e->tab[e->cur];
-    ck(cudaMemcpy(ids, tb.id, m * 8, cudaMemcpyDeviceToHost), "D2H");
-    ck(cudaMemcpy(x, tb.x, m * 8, cudaMemcpyDeviceToHost), "D2H");
-    ck(cudaMemcpy(t, tb.t, m * 8, cudaMemcpyDeviceToHost), "D2H");
+    ck(cudaMemcpyAsync(ids, tb.id, m * 8, cudaMemcpyDeviceToHost, e->stream), "D2H");
+    ck(cudaMemcpyAsync(x, tb.x, m * 8, cudaMemcpyDeviceToHost, e->stream), "D2H");
+    ck(cudaMemcpyAsync(t, tb.t, m * 8, cudaMemcpyDeviceToHost, e->stream), "D2H");
     if (arrivals) {  // in chunks of <= 512 MiB
       const int64_t chunk = std::max<int64_t>(
           1, std::min<int64_t>({m, ((int64_t)512 << 20) / ((int64_t)e->S * 8), 65535}));
@@ -1985,8 +1988,8 @@ int seis_get_hypothesis(seis_engine* e, int64_t cap, int64_t* n, uint64_t* ids, 
                            cudaMemcpyDeviceToHost, e->stream),
            "D2H arrivals");
       }
-      ck(cudaStreamSynchronize(e->stream), "sync");
     }
+    ck(cudaStreamSynchronize(e->stream), "sync");
   });
 }
 
@@ -2276,6 +2279,7 @@ static int run_driver(seis_engine* e, const seis_sampler_cfg* sc, int32_t mode,
     int* nreg_d = static_cast<int*>(alloc((size_t)n_ep * 4));
     int* perr = static_cast<int*>(alloc(4));
     std::vector<int> h_nreg(n_ep);
+    int herr = 0;
     if (serial) {  // config.full_region() (model.hpp:109)
       const double hb[2] = {0.0, e->cfg.T};
       ck(cudaMemcpy(bnd, hb, sizeof hb, cudaMemcpyHostToDevice), "H2D");
@@ -2286,14 +2290,11 @@ static int run_driver(seis_engine* e, const seis_sampler_cfg* sc, int32_t mode,
           e->cfg.T, l, tau, ncol, sc->dynamic ? 1 : 0, sc->seed, 0, (int)n_ep, 0.0, bcap, bnd,
           nreg_d, perr, nullptr);
       ck(cudaGetLastError(), "k_partition");
-      int herr = 0;
       ck(cudaMemcpyAsync(h_nreg.data(), nreg_d, (size_t)n_ep * 4, cudaMemcpyDeviceToHost,
                          e->stream),
          "D2H nreg");
       ck(cudaMemcpyAsync(&herr, perr, 4, cudaMemcpyDeviceToHost, e->stream), "D2H");
-      ck(cudaStreamSynchronize(e->stream), "sync");
-      if (herr == 1) throw std::logic_error("color_partition: separation invariant violated");
-      if (herr == 2) throw std::runtime_error("partition capacity");
+      // checked after the synchronisation that also brings next_base back
     }
     const int n_slots = serial ? 1 : (int)((sc->n_regions + 1 + ncol - 1) / ncol) + 1;
     int* births_cnt = static_cast<int*>(alloc((size_t)n_slots * 4));
@@ -2337,6 +2338,8 @@ static int run_driver(seis_engine* e, const seis_sampler_cfg* sc, int32_t mode,
     unsigned long long next_base = 0;
     ck(cudaMemcpyAsync(&next_base, maxid, 8, cudaMemcpyDeviceToHost, e->stream), "D2H");
     ck(cudaStreamSynchronize(e->stream), "sync");
+    if (herr == 1) throw std::logic_error("color_partition: separation invariant violated");
+    if (herr == 2) throw std::runtime_error("partition capacity");
     int64_t launches = 0;  // kernels launched inside the timed region
     cudaEvent_t ev_start, ev_stop;
     ck(cudaEventCreate(&ev_start), "event");
