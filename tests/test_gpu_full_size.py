@@ -1,0 +1,67 @@
+"""GPU: size-independent properties at BASELINE.json's full sizes (configs 1 and 2).
+
+The O(S N) oracle cannot score these worlds in test time, so the sweep is
+checked through properties that hold at any size:
+- the coverage counts the engine maintains incrementally across a sweep equal
+  the counts rebuilt from the final hypothesis (`seis_log_joint` reads the
+  resident counts; after a get/set round trip it reads rebuilt ones, with the
+  same fixed reduction order, so the two values are bit-identical);
+- the merged hypothesis is sorted by id with unique ids (merge = sort by id,
+  samplers.hpp:471-482) and every event lies in the prior's support
+  ([0, x_max] x [0, T], density.hpp:218-221);
+- the production chain is deterministic (philox stream spec v1 keyed by
+  (seed, sweep, region, step)): the same seed from the same start gives a
+  bit-identical hypothesis, a different seed a different one.
+"""
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def E(built):
+    import paper_1612_00595_b200 as E
+    return E
+
+
+def _same(a, b):
+    return (len(a.ids) == len(b.ids) and np.array_equal(a.ids, b.ids)
+            and np.array_equal(a.x.view(np.uint64), b.x.view(np.uint64))
+            and np.array_equal(a.t.view(np.uint64), b.t.view(np.uint64))
+            and np.array_equal(a.arrivals.view(np.uint64), b.arrivals.view(np.uint64)))
+
+
+@pytest.mark.parametrize("cfg", [1, 2])
+def test_full_size_sweep_properties(E, cfg):
+    import bench
+    c = dict(bench.CONFIGS[cfg])
+    m, ev, sig = bench.make_world(c, os.cpu_count() or 1)
+    cap = int(ev.N * 2 + 256)
+    truth = E.Events(ev.ids, ev.x, ev.t, ev.arrivals)
+    eng = E.Engine(m, sig, event_capacity=cap)
+    eng.set_hypothesis(truth)
+    tr = eng.run_chromatic(bench.sampler_for(c, 7), final=False, row_cap=4)
+    assert tr.total_steps == c["n_regions"] * c["k"]
+    assert tr.total_accepted > 0
+    lj_incremental = eng.log_joint()
+    h = eng.get_hypothesis()
+
+    assert np.all(np.diff(h.ids.astype(np.uint64)) > 0), "merged hypothesis not sorted by unique id"
+    assert np.all((h.x >= 0.0) & (h.x <= m.x_max)) and np.all((h.t >= 0.0) & (h.t <= m.T))
+    assert h.arrivals.shape == (len(h.ids), c["S"]) and np.all(np.isfinite(h.arrivals))
+
+    # incremental coverage == coverage rebuilt from the final hypothesis
+    eng.set_hypothesis(h)
+    assert eng.log_joint() == lj_incremental
+
+    # determinism at full size: same seed, same start -> bit-identical chain
+    eng.set_hypothesis(truth)
+    eng.run_chromatic(bench.sampler_for(c, 7), final=False, row_cap=4)
+    assert _same(eng.get_hypothesis(), h)
+    eng.set_hypothesis(truth)
+    eng.run_chromatic(bench.sampler_for(c, 8), final=False, row_cap=4)
+    assert not _same(eng.get_hypothesis(), h)
+    eng.close()
