@@ -1064,6 +1064,10 @@ __global__ void __launch_bounds__(NTT, MINB)
 // ----------------------------------------------------------------- barrier
 // Coverage commit: C += sum over regions of (own_now - own_start) windows;
 // same-color footprints overlap, so packed 32-bit atomics.
+#ifndef SEIS_COMMIT_THREADS
+#define SEIS_COMMIT_THREADS 512
+#endif
+constexpr int kCommitThreads = SEIS_COMMIT_THREADS;
 __global__ void k_commit(Dev d, int color, int ncol, int nreg, const int* diff_cnt,
                          const DiffPair* diff, int* free_stack, Ctl* ctl) {
   const int slot_idx = blockIdx.x;
@@ -1072,10 +1076,14 @@ __global__ void k_commit(Dev d, int color, int ncol, int nreg, const int* diff_c
   const int nd = diff_cnt[slot_idx];
   const DiffPair* de = diff + (size_t)slot_idx * MAXDOUT;
   const double2* pool2 = reinterpret_cast<const double2*>(d.pool);
-  for (int q = 0; q < nd; ++q) {
+  // (diff entry, station pair) items over the whole CTA: a region's few
+  // entries x P2 pairs, so every thread has work even when P2 is small
+  const long long n_items = (long long)nd * d.P2;
+  for (long long it = threadIdx.x; it < n_items; it += blockDim.x) {
+    const int q = (int)(it / d.P2), p = (int)(it - (long long)q * d.P2);
     if (de[q].kind != 0) continue;
     const int so = de[q].old_slot, sn = de[q].new_slot;
-    for (int p = threadIdx.x; p < d.P2; p += blockDim.x) {
+    {
       Win o0 = empty_win(), o1 = empty_win(), n0 = empty_win(), n1 = empty_win();
       if (so >= 0) {
         const double2 a = pool2[(size_t)so * d.P2 + p];
@@ -2433,7 +2441,8 @@ static int run_driver(seis_engine* e, const seis_sampler_cfg* sc, int32_t mode,
         phase_ev.emplace_back(a, b);
       }
       ck(cudaGetLastError(), "k_phase");
-      k_commit<<<ncr, 256, 0, e->stream>>>(e->d, color, std::max(ncol, 1), nreg, diff_cnt, diff,
+      k_commit<<<ncr, kCommitThreads, 0, e->stream>>>(e->d, color, std::max(ncol, 1), nreg,
+                                                      diff_cnt, diff,
                                              e->free_stack, e->ctl);
       ck(cudaGetLastError(), "k_commit");
       const int nxt = e->cur ^ 1;
@@ -2712,7 +2721,7 @@ extern "C" int seis_run_naive(seis_engine* e, const seis_sampler_cfg* sc, int32_
     ck(cudaEventRecord(evp1, e->stream), "event");
     ck(cudaGetLastError(), "k_phase (naive)");
     // the union: coverage of every region's events, table of all births
-    k_commit<<<nreg, 256, 0, e->stream>>>(e->d, 0, 1, nreg, diff_cnt, diff, e->free_stack,
+    k_commit<<<nreg, kCommitThreads, 0, e->stream>>>(e->d, 0, 1, nreg, diff_cnt, diff, e->free_stack,
                                           e->ctl);
     const int nxt = e->cur ^ 1;
     k_rebuild<<<1, 1024, 0, e->stream>>>(e->tab[e->cur], e->tab[nxt], e->cap, stamp,
