@@ -57,36 +57,53 @@ __device__ __host__ inline double d_offset_uniform(uint64_t seed, uint64_t purpo
 // epoch: boundaries by the reference's repeated fp64 addition, colors i % k,
 // separation invariant checked against the nearest same-colored region
 // (equivalent to the reference's all-pairs check since boundaries increase).
-__global__ void k_partition(double T, double l, double tau, int ncol, int mode, uint64_t seed,
-                            int epoch0, int n_ep, double u_explicit, int bcap, double* bnd,
-                            int* nreg, int* err, int* colors) {
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+// One CTA per epoch: thread 0 places the boundaries (the reference's repeated
+// fp64 addition is sequential), then the CTA fills colors and checks the
+// separation invariant in parallel.
+constexpr int kPartThreads = 128;
+__global__ void __launch_bounds__(kPartThreads)
+    k_partition(double T, double l, double tau, int ncol, int mode, uint64_t seed, int epoch0,
+                int n_ep, double u_explicit, int bcap, double* bnd, int* nreg, int* err,
+                int* colors) {
+  const int e = blockIdx.x;
   if (e >= n_ep) return;
   const int epoch = epoch0 + e;
-  // mode 0 static (u = 0), 1 dynamic (u redrawn after every epoch,
-  // samplers.hpp:488-493), 2 explicit offset
-  double u = 0.0;
-  if (mode == 1 && epoch > 0) u = d_offset_uniform(seed, 6, (uint64_t)epoch, 0.0, l);
-  if (mode == 2) u = u_explicit;
   double* b = bnd + (size_t)e * bcap;
-  int nb = 0;
-  b[nb++] = 0.0;
-  double x = u > 0 ? u : l;
-  while (x < T - 1e-9) {
-    if (nb >= bcap - 1) {
-      atomicExch(err, 2);
-      return;
+  __shared__ int s_n;
+  if (threadIdx.x == 0) {
+    // mode 0 static (u = 0), 1 dynamic (u redrawn after every epoch,
+    // samplers.hpp:488-493), 2 explicit offset
+    double u = 0.0;
+    if (mode == 1 && epoch > 0) u = d_offset_uniform(seed, 6, (uint64_t)epoch, 0.0, l);
+    if (mode == 2) u = u_explicit;
+    int nb = 0;
+    b[nb++] = 0.0;
+    double x = u > 0 ? u : l;
+    while (x < T - 1e-9) {
+      if (nb >= bcap - 1) {
+        atomicExch(err, 2);
+        nb = -1;
+        break;
+      }
+      b[nb++] = x;
+      x += l;
     }
-    b[nb++] = x;
-    x += l;
+    if (nb > 0) {
+      b[nb++] = T;
+      nreg[e] = nb - 1;
+    }
+    s_n = nb - 1;
   }
-  b[nb++] = T;
-  const int n = nb - 1;
-  nreg[e] = n;
+  __syncthreads();
+  const int n = s_n;
+  if (n < 0) return;
   if (colors)
-    for (int i = 0; i < n; ++i) colors[(size_t)e * bcap + i] = i % ncol;  // partition.hpp:81-82
-  for (int i = 0; i + ncol < n; ++i)
-    if (b[i + ncol] - b[i + 1] < tau - 1e-9) atomicExch(err, 1);
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+      colors[(size_t)e * bcap + i] = i % ncol;  // partition.hpp:81-82
+  bool bad = false;
+  for (int i = threadIdx.x; i + ncol < n; i += blockDim.x)
+    bad |= b[i + ncol] - b[i + 1] < tau - 1e-9;
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicExch(err, 1);
 }
 
 __global__ void k_offsets(uint64_t seed, int64_t epoch, double l, double* out) {
@@ -2075,7 +2092,7 @@ int seis_partition(double T, double l, double offset, double tau, int64_t cap,
     ck(cudaMemset(err, 0, 4), "memset");
     // offset passed explicitly: epoch-0 static path with the given u
     int* col = dalloc<int>(bcap);
-    k_partition<<<1, 1>>>(T, l, tau, k, 2, 0, 0, 1, offset, bcap, b, nr, err, col);
+    k_partition<<<1, kPartThreads>>>(T, l, tau, k, 2, 0, 0, 1, offset, bcap, b, nr, err, col);
     ck(cudaGetLastError(), "k_partition");
     int h_nr = 0, h_err = 0;
     ck(cudaMemcpy(&h_nr, nr, 4, cudaMemcpyDeviceToHost), "D2H");
@@ -2294,7 +2311,7 @@ static int run_driver(seis_engine* e, const seis_sampler_cfg* sc, int32_t mode,
       h_nreg[0] = 1;
     } else {
       ck(cudaMemsetAsync(perr, 0, 4, e->stream), "memset");
-      k_partition<<<(unsigned)((n_ep + 63) / 64), 64, 0, e->stream>>>(
+      k_partition<<<(unsigned)n_ep, kPartThreads, 0, e->stream>>>(
           e->cfg.T, l, tau, ncol, sc->dynamic ? 1 : 0, sc->seed, 0, (int)n_ep, 0.0, bcap, bnd,
           nreg_d, perr, nullptr);
       ck(cudaGetLastError(), "k_partition");
@@ -2609,7 +2626,7 @@ extern "C" int seis_run_naive(seis_engine* e, const seis_sampler_cfg* sc, int32_
     int* perr = static_cast<int*>(alloc(4));
     ck(cudaMemsetAsync(perr, 0, 4, e->stream), "memset");
     // build_partition only: no coloring, no separation check (tau = -inf)
-    k_partition<<<1, 1, 0, e->stream>>>(e->cfg.T, l, -INFINITY, 1, 0, 0, 0, 1, 0.0, bcap, bnd,
+    k_partition<<<1, kPartThreads, 0, e->stream>>>(e->cfg.T, l, -INFINITY, 1, 0, 0, 0, 1, 0.0, bcap, bnd,
                                          nreg_d, perr, nullptr);
     int nreg = 0, herr = 0;
     ck(cudaMemcpyAsync(&nreg, nreg_d, 4, cudaMemcpyDeviceToHost, e->stream), "D2H");
