@@ -1085,6 +1085,12 @@ __global__ void __launch_bounds__(NTT, MINB)
 #define SEIS_COMMIT_THREADS 512
 #endif
 constexpr int kCommitThreads = SEIS_COMMIT_THREADS;
+// regions with few CTAs (config[1]: 128 per phase) split their items over
+// blockIdx.y so the commit fills every SM several CTAs deep
+inline dim3 commit_grid(int ncr, int n_sm) {
+  const int split = std::max(1, std::min(8, (4 * n_sm + ncr - 1) / std::max(ncr, 1)));
+  return dim3((unsigned)ncr, (unsigned)split);
+}
 __global__ void k_commit(Dev d, int color, int ncol, int nreg, const int* diff_cnt,
                          const DiffPair* diff, int* free_stack, Ctl* ctl) {
   const int slot_idx = blockIdx.x;
@@ -1096,7 +1102,8 @@ __global__ void k_commit(Dev d, int color, int ncol, int nreg, const int* diff_c
   // (diff entry, station pair) items over the whole CTA: a region's few
   // entries x P2 pairs, so every thread has work even when P2 is small
   const long long n_items = (long long)nd * d.P2;
-  for (long long it = threadIdx.x; it < n_items; it += blockDim.x) {
+  for (long long it = (long long)blockIdx.y * blockDim.x + threadIdx.x; it < n_items;
+       it += (long long)gridDim.y * blockDim.x) {
     const int q = (int)(it / d.P2), p = (int)(it - (long long)q * d.P2);
     if (de[q].kind != 0) continue;
     const int so = de[q].old_slot, sn = de[q].new_slot;
@@ -1137,8 +1144,8 @@ __global__ void k_commit(Dev d, int color, int ncol, int nreg, const int* diff_c
       }
     }
   }
-  __syncthreads();
-  if (threadIdx.x == 0)
+  // the freed slots are popped again only by the next phase's k_phase
+  if (blockIdx.y == 0 && threadIdx.x == 0)
     for (int q = 0; q < nd; ++q) {
       const int slot = de[q].old_slot;
       if (slot >= 0) {  // replaced / dead start versions and recycled versions
@@ -2458,7 +2465,7 @@ static int run_driver(seis_engine* e, const seis_sampler_cfg* sc, int32_t mode,
         phase_ev.emplace_back(a, b);
       }
       ck(cudaGetLastError(), "k_phase");
-      k_commit<<<ncr, kCommitThreads, 0, e->stream>>>(e->d, color, std::max(ncol, 1), nreg,
+      k_commit<<<commit_grid(ncr, e->n_sm), kCommitThreads, 0, e->stream>>>(e->d, color, std::max(ncol, 1), nreg,
                                                       diff_cnt, diff,
                                              e->free_stack, e->ctl);
       ck(cudaGetLastError(), "k_commit");
@@ -2738,7 +2745,7 @@ extern "C" int seis_run_naive(seis_engine* e, const seis_sampler_cfg* sc, int32_
     ck(cudaEventRecord(evp1, e->stream), "event");
     ck(cudaGetLastError(), "k_phase (naive)");
     // the union: coverage of every region's events, table of all births
-    k_commit<<<nreg, kCommitThreads, 0, e->stream>>>(e->d, 0, 1, nreg, diff_cnt, diff, e->free_stack,
+    k_commit<<<commit_grid(nreg, e->n_sm), kCommitThreads, 0, e->stream>>>(e->d, 0, 1, nreg, diff_cnt, diff, e->free_stack,
                                           e->ctl);
     const int nxt = e->cur ^ 1;
     k_rebuild<<<1, 1024, 0, e->stream>>>(e->tab[e->cur], e->tab[nxt], e->cap, stamp,
