@@ -65,3 +65,33 @@ def test_full_size_sweep_properties(E, cfg):
     eng.run_chromatic(bench.sampler_for(c, 8), final=False, row_cap=4)
     assert not _same(eng.get_hypothesis(), h)
     eng.close()
+
+
+def test_static_partition_reuse_across_runs(E):
+    """The engine keeps the last static partition (no launch, no round trip);
+    a run with another region count must rebuild it, and returning to the
+    first count must give the first chain again, as a fresh engine does."""
+    import bench
+    from paper_1612_00595_b200 import SamplerConfig
+    c = dict(bench.CONFIGS[1])
+    m, ev, sig = bench.make_world(c, os.cpu_count() or 1)
+    truth = E.Events(ev.ids, ev.x, ev.t, ev.arrivals)
+
+    def sc(n_regions, seed=3):
+        return SamplerConfig(algorithm="chromatic-static", steps_per_epoch=16, epochs=2,
+                             n_regions=n_regions, seed=seed, record_every=1 << 30)
+
+    def run(eng, n_regions):
+        eng.set_hypothesis(truth)
+        eng.run_chromatic(sc(n_regions), final=False, row_cap=4)
+        return eng.get_hypothesis()
+
+    eng = E.Engine(m, sig, event_capacity=ev.N * 2 + 256)
+    h256 = run(eng, 256)
+    h128 = run(eng, 128)
+    assert _same(run(eng, 256), h256)
+    fresh = E.Engine(m, sig, event_capacity=ev.N * 2 + 256)
+    assert _same(run(fresh, 128), h128)
+    assert not _same(h128, h256)
+    fresh.close()
+    eng.close()
