@@ -67,10 +67,10 @@ def test_full_size_sweep_properties(E, cfg):
     eng.close()
 
 
-def test_static_partition_reuse_across_runs(E):
-    """The engine keeps the last static partition (no launch, no round trip);
-    a run with another region count must rebuild it, and returning to the
-    first count must give the first chain again, as a fresh engine does."""
+def test_region_count_changes_between_runs(E):
+    """Runs on one engine with different static partitions (256, 128, 256
+    regions) leave no state behind: returning to the first region count gives
+    the first chain again, and the second matches a fresh engine's."""
     import bench
     from paper_1612_00595_b200 import SamplerConfig
     c = dict(bench.CONFIGS[1])
