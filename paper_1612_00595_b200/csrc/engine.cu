@@ -1091,8 +1091,9 @@ inline dim3 commit_grid(int ncr, int n_sm) {
   const int split = std::max(1, std::min(8, (4 * n_sm + ncr - 1) / std::max(ncr, 1)));
   return dim3((unsigned)ncr, (unsigned)split);
 }
-__global__ void k_commit(Dev d, int color, int ncol, int nreg, const int* diff_cnt,
-                         const DiffPair* diff, int* free_stack, Ctl* ctl) {
+__device__ __forceinline__ void commit_body(const Dev& d, int color, int ncol, int nreg,
+                                            const int* diff_cnt, const DiffPair* diff,
+                                            int* free_stack, Ctl* ctl) {
   const int slot_idx = blockIdx.x;
   const int region = color + slot_idx * ncol;
   if (region >= nreg) return;
@@ -1155,6 +1156,11 @@ __global__ void k_commit(Dev d, int color, int ncol, int nreg, const int* diff_c
     }
 }
 
+__global__ void k_commit(Dev d, int color, int ncol, int nreg, const int* diff_cnt,
+                         const DiffPair* diff, int* free_stack, Ctl* ctl) {
+  commit_body(d, color, ncol, nreg, diff_cnt, diff, free_stack, ctl);
+}
+
 // block-wide exclusive scan of one int per thread (1024 threads)
 __device__ int block_scan_excl(int v, int* total) {
   __shared__ int ws[32];
@@ -1187,12 +1193,12 @@ __device__ int block_scan_excl(int v, int* total) {
 // Event-table rebuild (merge + sort_by_id, samplers.hpp:471-482) without a
 // sort: survivors keep their id order, births (ids above every old id,
 // increasing with region slot) are appended region by region.
-__global__ void __launch_bounds__(1024) k_rebuild(Table in, Table out, int cap, int stamp,
-                                                  const int* fate_stamp, const int* fate_alive,
-                                                  const double* fate_x, const double* fate_t,
-                                                  const int* fate_slot, int n_slots,
-                                                  const int* births_cnt, const OutEv* births,
-                                                  Ctl* ctl) {
+__device__ __forceinline__ void rebuild_body(Table in, Table out, int cap, int stamp,
+                                             const int* fate_stamp, const int* fate_alive,
+                                             const double* fate_x, const double* fate_t,
+                                             const int* fate_slot, int n_slots,
+                                             const int* births_cnt, const OutEv* births,
+                                             Ctl* ctl) {
   const int N = ctl->n_events;
   int base = 0;
   for (int c0 = 0; c0 < N; c0 += blockDim.x) {
@@ -1235,6 +1241,33 @@ __global__ void __launch_bounds__(1024) k_rebuild(Table in, Table out, int cap, 
     if (base > cap) set_err(ctl, ERR_TABLE_OVERFLOW);
     ctl->n_events = min(base, cap);
   }
+}
+
+__global__ void __launch_bounds__(1024) k_rebuild(Table in, Table out, int cap, int stamp,
+                                                  const int* fate_stamp, const int* fate_alive,
+                                                  const double* fate_x, const double* fate_t,
+                                                  const int* fate_slot, int n_slots,
+                                                  const int* births_cnt, const OutEv* births,
+                                                  Ctl* ctl) {
+  rebuild_body(in, out, cap, stamp, fate_stamp, fate_alive, fate_x, fate_t, fate_slot, n_slots,
+               births_cnt, births, ctl);
+}
+
+// The color barrier in one launch: the commit CTAs (grid.x < ncr) and, in the
+// last column, one table rebuild CTA. The two touch disjoint state (coverage,
+// free stack / next table, n_events), so the rebuild runs beside the commit.
+__global__ void k_barrier(Dev d, int color, int ncol, int nreg, const int* diff_cnt,
+                          const DiffPair* diff, int* free_stack, Ctl* ctl, Table in, Table out,
+                          int cap, int stamp, const int* fate_stamp, const int* fate_alive,
+                          const double* fate_x, const double* fate_t, const int* fate_slot,
+                          int n_slots, const int* births_cnt, const OutEv* births) {
+  if (blockIdx.x == gridDim.x - 1) {
+    if (blockIdx.y == 0)
+      rebuild_body(in, out, cap, stamp, fate_stamp, fate_alive, fate_x, fate_t, fate_slot,
+                   n_slots, births_cnt, births, ctl);
+    return;
+  }
+  commit_body(d, color, ncol, nreg, diff_cnt, diff, free_stack, ctl);
 }
 
 // ----------------------------------------------------------------- score batch
@@ -2465,16 +2498,15 @@ static int run_driver(seis_engine* e, const seis_sampler_cfg* sc, int32_t mode,
         phase_ev.emplace_back(a, b);
       }
       ck(cudaGetLastError(), "k_phase");
-      k_commit<<<commit_grid(ncr, e->n_sm), kCommitThreads, 0, e->stream>>>(e->d, color, std::max(ncol, 1), nreg,
-                                                      diff_cnt, diff,
-                                             e->free_stack, e->ctl);
-      ck(cudaGetLastError(), "k_commit");
       const int nxt = e->cur ^ 1;
-      k_rebuild<<<1, 1024, 0, e->stream>>>(e->tab[e->cur], e->tab[nxt], e->cap, stamp,
-                                            e->fate_stamp, e->fate_alive, e->fate_x, e->fate_t,
-                                            e->fate_slot, ncr, births_cnt, births, e->ctl);
-      ck(cudaGetLastError(), "k_rebuild");
-      launches += 3;
+      dim3 bg = commit_grid(ncr, e->n_sm);
+      bg.x += 1;  // + the table rebuild CTA
+      k_barrier<<<bg, kCommitThreads, 0, e->stream>>>(
+          e->d, color, std::max(ncol, 1), nreg, diff_cnt, diff, e->free_stack, e->ctl,
+          e->tab[e->cur], e->tab[nxt], e->cap, stamp, e->fate_stamp, e->fate_alive, e->fate_x,
+          e->fate_t, e->fate_slot, ncr, births_cnt, births);
+      ck(cudaGetLastError(), "k_barrier");
+      launches += 2;
       e->cur = nxt;
       tape_base += (long long)ncr * kk;
       executed += (int64_t)ncr * kk;
