@@ -119,7 +119,18 @@ typedef struct {
   int64_t n_rows;                       /* trace rows produced */
   int64_t final_events;
   int64_t speculative_discarded;        /* proposals evaluated ahead of an accept, then dropped */
+  int64_t phases;                       /* region-sweep kernel launches (color phases) */
 } seis_run_stats;
+
+/* reference PhaseRecord (samplers.hpp:87-95): one per committed region
+ * segment, in commit order (run_chromatic samplers.hpp:479; run_naive_parallel
+ * samplers.hpp:370; run_serial records none) */
+typedef struct {
+  int64_t epoch;
+  int32_t color, pad_;
+  int64_t region;
+  int64_t steps;
+} seis_phase_record;
 
 const char* seis_last_error(void);
 
@@ -152,6 +163,13 @@ int seis_get_hypothesis(seis_engine* eng, int64_t cap, int64_t* n, uint64_t* ids
 int seis_set_snapshot_capacity(seis_engine* eng, int64_t max_events, int64_t max_snapshots);
 int seis_get_snapshots(seis_engine* eng, int64_t cap_snap, int64_t* n_snap, int64_t* snap_step,
                        int64_t* snap_count, int64_t cap_ev, uint64_t* ids, double* x, double* t);
+
+/* Trace::phases of the engine's last run (*n = count, at most cap written). */
+int seis_get_phases(seis_engine* eng, int64_t cap, int64_t* n, seis_phase_record* out);
+/* TraceRow::wall_seconds (= Snapshot::wall_seconds at the same step,
+ * samplers.hpp:73-85) of the last run's trace rows: device time from the
+ * start of the run to the row, from CUDA events on the engine's stream. */
+int seis_get_row_wall(seis_engine* eng, int64_t cap, int64_t* n, double* wall_seconds);
 
 int seis_partition(double T, double l, double offset, double tau, int64_t cap,
                    int64_t* n_regions, double* boundaries /* cap */, int32_t* colors /* cap */,

@@ -419,6 +419,24 @@ def ref_bench_region_steps(world: World, truth: Events, sampler: Sampler, thread
     return props.value, wall.value
 
 
+def ref_thomas_events(seed, x_max, T, parent_mean=2000.0, child_mean=10.0, sx=50.0, st=None,
+                      cap=1 << 20):
+    """Thomas cluster process of config[4] drawn with the reference's own Rng
+    (oracle/_ref sr_thomas_events); returns (cx, ct)."""
+    L = C.CDLL(REF_SO)
+    f = L.sr_thomas_events
+    f.argtypes = [u64, f64, f64, f64, f64, f64, f64, i64, P, P, P]
+    st = 0.0015625 * T if st is None else st
+    cx = np.zeros(cap)
+    ct = np.zeros(cap)
+    n = i64(0)
+    rc = f(seed, x_max, T, parent_mean, child_mean, sx, st, cap, C.byref(n), _p(cx), _p(ct))
+    if rc:
+        L.sr_last_error.restype = C.c_char_p
+        raise RuntimeError(L.sr_last_error().decode())
+    return cx[:n.value].copy(), ct[:n.value].copy()
+
+
 def philox(c, k):
     L = C.CDLL(ORACLE_SO)
     o = (C.c_uint32 * 4)()

@@ -217,6 +217,37 @@ int sr_sample_world(const so_model* m, uint64_t seed, int64_t cap, int64_t* n_ev
   });
 }
 
+// Thomas cluster process of BASELINE config[4]: the engine's
+// host generator (worldgen.cpp seis_thomas_events) drawn here with the
+// reference's own Rng/derive_stream under purpose ids 100-102 (outside the
+// reference's 1..7), so the reference arm builds its world without the engine.
+int sr_thomas_events(uint64_t seed, double x_max, double T, double parent_mean,
+                     double child_mean, double sx, double st, int64_t cap, int64_t* n, double* cx,
+                     double* ct) {
+  return guarded([&] {
+    Rng pc = derive_stream(seed, 100);
+    const uint64_t np = pc.poisson(parent_mean);
+    int64_t k = 0;
+    for (uint64_t p = 0; p < np; ++p) {
+      Rng pr = derive_stream(seed, 101, p);
+      const double px = pr.uniform(0.0, x_max), pt = pr.uniform(0.0, T);
+      Rng ch = derive_stream(seed, 102, p);
+      const uint64_t nc = ch.poisson(child_mean);
+      for (uint64_t c = 0; c < nc; ++c) {
+        const double x = px + ch.normal(0.0, sx), t = pt + ch.normal(0.0, st);
+        if (x < 0.0 || x > x_max || t < 0.0 || t >= T) continue;
+        if (k < cap) {
+          cx[k] = x;
+          ct[k] = t;
+        }
+        ++k;
+      }
+    }
+    *n = k;
+    if (k > cap) throw std::runtime_error("capacity");
+  });
+}
+
 int sr_make_world_with_events(const so_model* m, int64_t n, const double* cx, const double* ct,
                               uint64_t seed, uint64_t* ids, double* x, double* t, double* arr,
                               double* signals) {

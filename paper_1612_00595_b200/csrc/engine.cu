@@ -854,6 +854,7 @@ __global__ void __launch_bounds__(NTT, MINB)
             } else {
               const int top = atomicSub(&ctl->free_top, 1) - 1;
               if (top < 0) {
+                atomicAdd(&ctl->free_top, 1);  // undo the failed pop: the stack stays valid
                 set_err(ctl, ERR_POOL_EXHAUSTED);
                 ok = false;
                 break;
@@ -1085,6 +1086,8 @@ __global__ void __launch_bounds__(NTT, MINB)
 #define SEIS_COMMIT_THREADS 512
 #endif
 constexpr int kCommitThreads = SEIS_COMMIT_THREADS;
+static_assert(kCommitThreads % 32 == 0 && kCommitThreads >= 64 && kCommitThreads <= 1024,
+              "block_scan_excl needs whole warps, at most 32 of them");
 // regions with few CTAs (config[1]: 128 per phase) split their items over
 // blockIdx.y so the commit fills every SM several CTAs deep
 inline dim3 commit_grid(int ncr, int n_sm) {
@@ -1151,7 +1154,10 @@ __device__ __forceinline__ void commit_body(const Dev& d, int color, int ncol, i
       const int slot = de[q].old_slot;
       if (slot >= 0) {  // replaced / dead start versions and recycled versions
         const int top = atomicAdd(&ctl->free_top, 1);
-        free_stack[top] = slot;
+        if (top >= 0 && top < d.pool_cap)
+          free_stack[top] = slot;
+        else
+          set_err(ctl, ERR_POOL_EXHAUSTED);  // never write outside the stack
       }
     }
 }
@@ -1161,7 +1167,8 @@ __global__ void k_commit(Dev d, int color, int ncol, int nreg, const int* diff_c
   commit_body(d, color, ncol, nreg, diff_cnt, diff, free_stack, ctl);
 }
 
-// block-wide exclusive scan of one int per thread (1024 threads)
+// block-wide exclusive scan of one int per thread (any block size that is a
+// multiple of 32, up to 1024 threads)
 __device__ int block_scan_excl(int v, int* total) {
   __shared__ int ws[32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1256,7 +1263,7 @@ __global__ void __launch_bounds__(1024) k_rebuild(Table in, Table out, int cap, 
 // The color barrier in one launch: the commit CTAs (grid.x < ncr) and, in the
 // last column, one table rebuild CTA. The two touch disjoint state (coverage,
 // free stack / next table, n_events), so the rebuild runs beside the commit.
-__global__ void k_barrier(Dev d, int color, int ncol, int nreg, const int* diff_cnt,
+__global__ void __launch_bounds__(kCommitThreads) k_barrier(Dev d, int color, int ncol, int nreg, const int* diff_cnt,
                           const DiffPair* diff, int* free_stack, Ctl* ctl, Table in, Table out,
                           int cap, int stamp, const int* fate_stamp, const int* fate_alive,
                           const double* fate_x, const double* fate_t, const int* fate_slot,
@@ -1591,6 +1598,10 @@ struct seis_engine {
   seis_model_cfg cfg{};
   int S = 0, S_pad = 0, P2 = 0, n = 0, dtype = 0, cap = 0;
   int pool_slots = 0;  // arrival versions: live events + this phase's retired ones
+  // the last run's Trace::phases (samplers.hpp:87-95,370,479) and the device
+  // time of its trace rows since the run started (TraceRow/Snapshot wall_seconds)
+  std::vector<seis_phase_record> phases;
+  std::vector<double> row_wall;
   cudaStream_t stream = nullptr;
   Dev d{};
   double* stations = nullptr;
@@ -1821,6 +1832,9 @@ int seis_engine_create(const seis_model_cfg* cfg, const double* stations, int64_
       const size_t fit = free_b > reserve ? (free_b - reserve) / per : 0;
       const size_t want = 2 * (size_t)e->cap + 2048;
       size_t slots = std::min<size_t>(want, std::max<size_t>(fit, (size_t)e->cap));
+      // SEIS_POOL_SLOTS (tests): a smaller pool, to exercise exhaustion
+      if (const char* ov = getenv("SEIS_POOL_SLOTS"))
+        slots = std::max<size_t>((size_t)e->cap, std::min<size_t>(slots, (size_t)atoll(ov)));
       void* p = nullptr;
       while (cudaMalloc(&p, slots * per) != cudaSuccess) {
         (void)cudaGetLastError();
@@ -1897,6 +1911,11 @@ int seis_engine_create(const seis_model_cfg* cfg, const double* stations, int64_
     const double var_a = cfg->sigma_arrival * cfg->sigma_arrival;
     d.c0_arr = -0.5 * (kLog2Pi + std::log(var_a));
     d.inv_twovar_arr = 1.0 / (2.0 * var_a);
+    d.twovar_arr = 2.0 * var_a;
+    {
+      int ex = 0;
+      d.arr_div = std::frexp(d.twovar_arr, &ex) == 0.5 ? 0 : 1;  // mantissa 0.5: a power of two
+    }
     d.inv_v = 1.0 / cfg->v;
     d.log_lambda_T = std::log(cfg->lambda_rate * cfg->T);
     d.lxa = -std::log(cfg->x_max) - std::log(cfg->T);
@@ -2105,6 +2124,22 @@ int seis_get_snapshots(seis_engine* e, int64_t cap_snap, int64_t* n_snap, int64_
       ck(cudaMemcpy(x, e->snap_x, total * 8, cudaMemcpyDeviceToHost), "D2H");
       ck(cudaMemcpy(t, e->snap_t, total * 8, cudaMemcpyDeviceToHost), "D2H");
     }
+  });
+}
+
+int seis_get_phases(seis_engine* e, int64_t cap, int64_t* n, seis_phase_record* out) {
+  return guarded([&] {
+    const int64_t np = (int64_t)e->phases.size();
+    *n = np;
+    for (int64_t i = 0; i < np && i < cap; ++i) out[i] = e->phases[i];
+  });
+}
+
+int seis_get_row_wall(seis_engine* e, int64_t cap, int64_t* n, double* wall_seconds) {
+  return guarded([&] {
+    const int64_t nr = (int64_t)e->row_wall.size();
+    *n = nr;
+    for (int64_t i = 0; i < nr && i < cap; ++i) wall_seconds[i] = e->row_wall[i];
   });
 }
 
@@ -2337,8 +2372,20 @@ static int run_driver(seis_engine* e, const seis_sampler_cfg* sc, int32_t mode,
     sp.ncol = ncol;
     sp.mspec = spec_depth();
     const int bcap = (int)sc->n_regions + 4;
-    // every epoch's partition up front (one thread per epoch), so the timed
-    // region holds no host round trip
+    // the timed region starts before the partition kernel: everything the run
+    // launches (partition, id base, counters, phases, barriers, rows) is inside
+    cudaEvent_t ev_start, ev_stop;
+    ck(cudaEventCreate(&ev_start), "event");
+    ck(cudaEventCreate(&ev_stop), "event");
+    evs.push_back(ev_start);
+    evs.push_back(ev_stop);
+    ck(cudaEventRecord(ev_start, e->stream), "event");
+    int64_t launches = 0;  // kernels launched inside the timed region
+    e->phases.clear();
+    e->row_wall.clear();
+    std::vector<cudaEvent_t> row_ev;
+    // every epoch's partition up front (one CTA per epoch), so the phases
+    // hold no host round trip
     const int64_t n_ep = (sc->dynamic && !serial) ? sc->epochs : 1;
     double* bnd = static_cast<double*>(alloc((size_t)n_ep * bcap * 8));
     int* nreg_d = static_cast<int*>(alloc((size_t)n_ep * 4));
@@ -2355,6 +2402,7 @@ static int run_driver(seis_engine* e, const seis_sampler_cfg* sc, int32_t mode,
           e->cfg.T, l, tau, ncol, sc->dynamic ? 1 : 0, sc->seed, 0, (int)n_ep, 0.0, bcap, bnd,
           nreg_d, perr, nullptr);
       ck(cudaGetLastError(), "k_partition");
+      ++launches;
       ck(cudaMemcpyAsync(h_nreg.data(), nreg_d, (size_t)n_ep * 4, cudaMemcpyDeviceToHost,
                          e->stream),
          "D2H nreg");
@@ -2400,17 +2448,12 @@ static int run_driver(seis_engine* e, const seis_sampler_cfg* sc, int32_t mode,
     // next_base: above every id already present (reference starts empty at 0)
     k_max_id<<<1, 1024, 0, e->stream>>>(e->tab[e->cur], e->ctl, maxid);
     k_reset_counters<<<1, 1, 0, e->stream>>>(e->ctl);
+    launches += 2;
     unsigned long long next_base = 0;
     ck(cudaMemcpyAsync(&next_base, maxid, 8, cudaMemcpyDeviceToHost, e->stream), "D2H");
     ck(cudaStreamSynchronize(e->stream), "sync");
     if (herr == 1) throw std::logic_error("color_partition: separation invariant violated");
     if (herr == 2) throw std::runtime_error("partition capacity");
-    int64_t launches = 0;  // kernels launched inside the timed region
-    cudaEvent_t ev_start, ev_stop;
-    ck(cudaEventCreate(&ev_start), "event");
-    ck(cudaEventCreate(&ev_stop), "event");
-    evs.push_back(ev_start);
-    evs.push_back(ev_stop);
     const bool timing = stats != nullptr;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> phase_ev;
     int64_t n_rows = 0;
@@ -2441,11 +2484,15 @@ static int run_driver(seis_engine* e, const seis_sampler_cfg* sc, int32_t mode,
         k_record<<<1, 1, 0, e->stream>>>(e->ctl, cnt_dev + n_rows);
         ++launches;
         h_row_step.push_back(executed);
+        cudaEvent_t rv = nullptr;
+        ck(cudaEventCreate(&rv), "event");
+        evs.push_back(rv);
+        ck(cudaEventRecord(rv, e->stream), "event");
+        row_ev.push_back(rv);
       }
       ++n_rows;
       if (executed > 0 || n_rows > 1) take_snapshot(executed);
     };
-    ck(cudaEventRecord(ev_start, e->stream), "event");
     record_row(0);
     int64_t executed = 0, last_recorded = 0;
     long long tape_base = 0;
@@ -2507,6 +2554,10 @@ static int run_driver(seis_engine* e, const seis_sampler_cfg* sc, int32_t mode,
           e->fate_t, e->fate_slot, ncr, births_cnt, births);
       ck(cudaGetLastError(), "k_barrier");
       launches += 2;
+      if (!serial)  // Trace::phases, one record per committed region (samplers.hpp:479)
+        for (int slot = 0; slot < ncr; ++slot)
+          e->phases.push_back({(int64_t)epoch, (int32_t)color, 0,
+                               (int64_t)color + (int64_t)slot * ncol, (int64_t)kk});
       e->cur = nxt;
       tape_base += (long long)ncr * kk;
       executed += (int64_t)ncr * kk;
@@ -2551,6 +2602,11 @@ static int run_driver(seis_engine* e, const seis_sampler_cfg* sc, int32_t mode,
     if (last_recorded != executed) record_row(executed);
     ck(cudaEventRecord(ev_stop, e->stream), "event");
     ck(cudaStreamSynchronize(e->stream), "run");
+    for (auto rv : row_ev) {
+      float ms = 0.f;
+      ck(cudaEventElapsedTime(&ms, ev_start, rv), "elapsed");
+      e->row_wall.push_back(1e-3 * (double)ms);
+    }
     const Ctl c = read_ctl(e);
     if (c.err) throw std::runtime_error(std::string("device: ") + err_name(c.err));
     if (mode == 1 && tape_base != n_tape)
@@ -2601,6 +2657,7 @@ static int run_driver(seis_engine* e, const seis_sampler_cfg* sc, int32_t mode,
       stats->n_rows = n_rows;
       stats->final_events = c.n_events;
       stats->speculative_discarded = (int64_t)c.speculative;
+      stats->phases = (int64_t)phase_ev.size();
     }
   });
   for (auto ev : evs) cudaEventDestroy(ev);
@@ -2790,6 +2847,15 @@ extern "C" int seis_run_naive(seis_engine* e, const seis_sampler_cfg* sc, int32_
     if (sc->record_log_joint) launch_lj_any(e, lj_dev, lj_scratch);
     ck(cudaEventRecord(ev1, e->stream), "event");
     ck(cudaStreamSynchronize(e->stream), "run");
+    // Trace::phases of run_naive_parallel: one record per region (samplers.hpp:370)
+    e->phases.clear();
+    for (int r = 0; r < nreg; ++r) e->phases.push_back({0, 0, 0, (int64_t)r, spr});
+    e->row_wall.clear();
+    {
+      float ms = 0.f;  // checkpoints complete together, at the end of the launch
+      ck(cudaEventElapsedTime(&ms, ev0, evp1), "elapsed");
+      for (int64_t ci = 0; ci < n_cp; ++ci) e->row_wall.push_back(ci ? 1e-3 * (double)ms : 0.0);
+    }
     const Ctl c = read_ctl(e);
     if (c.err) throw std::runtime_error(std::string("device: ") + err_name(c.err));
     std::vector<int> hcp((size_t)n_cp * nreg);
@@ -2823,6 +2889,7 @@ extern "C" int seis_run_naive(seis_engine* e, const seis_sampler_cfg* sc, int32_
       stats->total_ms = ms;
       stats->kernel_launches = 3 + (sc->record_log_joint ? 3 : 0);
       stats->n_rows = n_cp;
+      stats->phases = 1;
       stats->final_events = c.n_events;
       stats->speculative_discarded = (int64_t)c.speculative;
     }

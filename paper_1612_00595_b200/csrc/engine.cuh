@@ -67,6 +67,8 @@ struct Dev {
   int rows;                        // n + kRowPad
   double rate, t_s, v, sigma, x_max, T;
   double c0_arr, inv_twovar_arr;   // log_gaussian constants for sigma_arrival
+  double twovar_arr;               // 2 sigma^2 (divided by when it is not a power of two)
+  int arr_div;                     // 1: 2 sigma^2 is not a power of two -> true division
   double inv_v;                    // RN(1 / v): division by v as a reciprocal + one correction
   double log_lambda_T, lxa;        // log(lambda T), -log(x_max) - log(T)
   double log_xmax;
@@ -211,11 +213,13 @@ __device__ __forceinline__ double arrival_mean(const Dev& d, double x, double t,
 
 __device__ __forceinline__ double arr_logpdf(const Dev& d, double a, double mean) {
   // log_gaussian(a, mean, sigma^2), density.hpp:15-18 with host-computed
-  // -0.5 (log 2pi + log sigma^2) and 1 / (2 sigma^2): the division becomes a
-  // multiplication (identical when 2 sigma^2 is a power of two, as for the
-  // reference default sigma_arrival = 2; otherwise within 1 ulp per term)
+  // -0.5 (log 2pi + log sigma^2). When 2 sigma^2 is a power of two (the
+  // reference default sigma_arrival = 2) the division by it is exactly a
+  // multiplication by its reciprocal; otherwise (d.arr_div, warp-uniform) the
+  // reference's division is kept so every ModelConfig stays bit-exact.
   const double dd = a - mean;
-  return d.c0_arr - dd * dd * d.inv_twovar_arr;
+  const double q = d.arr_div ? __ddiv_rn(dd * dd, d.twovar_arr) : dd * dd * d.inv_twovar_arr;
+  return d.c0_arr - q;
 }
 
 }  // namespace seis

@@ -50,7 +50,16 @@ class _StatsC(C.Structure):
     _fields_ = [("total_steps", i64), ("total_accepted", i64), ("scored_proposals", i64),
                 ("changed_samples", i64), ("arrival_values", i64), ("algorithmic_bytes", f64),
                 ("sweep_kernel_ms", f64), ("total_ms", f64), ("kernel_launches", i64),
-                ("n_rows", i64), ("final_events", i64), ("speculative_discarded", i64)]
+                ("n_rows", i64), ("final_events", i64), ("speculative_discarded", i64),
+                ("phases", i64)]
+
+
+class _PhaseC(C.Structure):
+    _fields_ = [("epoch", i64), ("color", i32), ("pad_", i32), ("region", i64), ("steps", i64)]
+
+
+PHASE_DTYPE = np.dtype([("epoch", "<i8"), ("color", "<i4"), ("pad_", "<i4"), ("region", "<i8"),
+                        ("steps", "<i8")])
 
 
 TAPE_DTYPE = np.dtype([
@@ -69,7 +78,7 @@ EXPORTS = ("seis_last_error", "seis_engine_create", "seis_engine_destroy", "seis
            "seis_world_last_error", "seis_world_generate", "seis_world_with_events",
            "seis_thomas_events", "seis_set_snapshot_capacity", "seis_get_snapshots",
            "seis_run_naive", "seis_run_serial", "seis_engine_pool_slots", "seis_eval_last_error",
-           "seis_match_events", "seis_bootstrap_ci")
+           "seis_match_events", "seis_bootstrap_ci", "seis_get_phases", "seis_get_row_wall")
 
 _LIB = None
 
@@ -110,6 +119,8 @@ def load_library(path: str | None = None) -> C.CDLL:
     L.seis_bootstrap_ci.argtypes = [P, i64, f64, i32, u64, P]
     L.seis_set_snapshot_capacity.argtypes = [P, i64, i64]
     L.seis_get_snapshots.argtypes = [P, i64, P, P, P, i64, P, P, P]
+    L.seis_get_phases.argtypes = [P, i64, P, P]
+    L.seis_get_row_wall.argtypes = [P, i64, P, P]
     if path == _build.LIB:
         _LIB = L
     return L
@@ -206,6 +217,7 @@ class Snapshot:
     ids: np.ndarray
     x: np.ndarray
     t: np.ndarray
+    wall_seconds: float = 0.0
 
 
 @dataclass
@@ -220,14 +232,18 @@ class Trace:
     final: Events | None = None
     step_out: np.ndarray | None = None
     snapshots: list = field(default_factory=list)
+    # TraceRow::wall_seconds (device time since the run started, CUDA events)
+    row_wall: np.ndarray | None = None
+    # Trace::phases (PhaseRecord, samplers.hpp:87-95): PHASE_DTYPE records
+    phases: np.ndarray | None = None
 
     def write_trace_csv(self, path: str) -> None:
-        """write_trace_csv (samplers.hpp:511-516). wall_seconds is not
-        measured per row on the device: written as 0."""
+        """write_trace_csv (samplers.hpp:511-516)."""
+        wall = self.row_wall if self.row_wall is not None else np.zeros(len(self.row_step))
         with open(path, "w") as f:
             f.write("wall_seconds,step,log_joint,event_count\n")
-            for st, lj, c in zip(self.row_step, self.row_log_joint, self.row_count):
-                f.write(f"0,{int(st)},{_fmt(lj)},{int(c)}\n")
+            for w, st, lj, c in zip(wall, self.row_step, self.row_log_joint, self.row_count):
+                f.write(f"{_fmt(w)},{int(st)},{_fmt(lj)},{int(c)}\n")
 
     def write_samples_csv(self, path: str) -> None:
         """write_samples_csv (samplers.hpp:518-524)."""
@@ -682,8 +698,31 @@ class Engine:
                    step_out=out)
         if final:
             tr.final = self.get_hypothesis()
+        tr.row_wall = self.row_wall()[:nr]
+        tr.phases = self.phases()
         tr.snapshots = self._get_snapshots()
+        wall_at = {int(s_): float(w_) for s_, w_ in zip(tr.row_step, tr.row_wall)}
+        for sn in tr.snapshots:
+            sn.wall_seconds = wall_at.get(sn.step, 0.0)
         return tr
+
+    def phases(self) -> np.ndarray:
+        """Trace::phases of the last run (seis_get_phases)."""
+        n = i64(0)
+        _check(self.L.seis_get_phases(self.h, 0, C.byref(n), None), self.L)
+        out = np.zeros(n.value, PHASE_DTYPE)
+        if n.value:
+            _check(self.L.seis_get_phases(self.h, n.value, C.byref(n), _p(out)), self.L)
+        return out
+
+    def row_wall(self) -> np.ndarray:
+        """TraceRow::wall_seconds of the last run (seis_get_row_wall)."""
+        n = i64(0)
+        _check(self.L.seis_get_row_wall(self.h, 0, C.byref(n), None), self.L)
+        out = np.zeros(n.value)
+        if n.value:
+            _check(self.L.seis_get_row_wall(self.h, n.value, C.byref(n), _p(out)), self.L)
+        return out
 
 
 def run_sampler(config: ModelConfig, signals: np.ndarray, sc: SamplerConfig,

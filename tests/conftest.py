@@ -10,6 +10,11 @@ if ROOT not in sys.path:
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (sm_100) GPU")
+    # build the oracle (and oracle/_ref when the reference tree is present)
+    # before collection, so skipif(not have_ref()) reflects this container and
+    # never skips a reference-pinning test only because the build came later
+    from oracle import oracle as O
+    O.build()
 
 
 @pytest.fixture(scope="session")

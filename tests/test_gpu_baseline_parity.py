@@ -1,0 +1,342 @@
+"""GPU parity at the BASELINE.json shapes and at non-default ModelConfigs.
+
+The engine (through its C-ABI) against the reference itself (oracle/_ref: the
+reference headers compiled in place, falling back to the pinned C oracle when
+the reference build is absent) on identical inputs:
+
+* config[1] at full size (S = 1600, T = 3600, 405 events, 256 regions): the
+  engine's world generator equals the reference's bit for bit; a reference
+  tape (k = 2, one epoch, both colors, from the truth hypothesis: every
+  proposal, uniform, delta and decision of the reference's own run_chromatic
+  composition) replayed through replay mode: decisions identical except ties,
+  deltas within 1e-9 relative, final hypothesis identical; the tape's
+  proposals scored against the truth hypothesis through seis_score_batch
+  (about 170 reference deltas; the replay above compares all 375).
+* config[2] at full size (S = 16384, 5013 events): 16 changes of every move
+  shape through seis_score_batch against the reference's delta_log_joint.
+* non-default ModelConfig values (sigma_arrival whose 2 sigma^2 is not a power
+  of two, t_s, sample_rate != 1, var_noise, var_event): reference tape replay,
+  production mode against the C oracle (philox spec) and batched deltas.
+
+Bars (BASELINE.json north_star): decisions bit-exact except |log a - log u| <
+1e-9; deltas within 1e-5 relative (asserted at 1e-9 here).
+"""
+import os
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from tests.helpers import engine_model, engine_sampler
+
+pytestmark = pytest.mark.gpu
+
+TIE = 1e-9
+DTOL = 1e-9
+
+
+@pytest.fixture(scope="module")
+def E(built):
+    import paper_1612_00595_b200 as E
+    return E
+
+
+@pytest.fixture(scope="module")
+def ref(built):
+    """the reference compiled in place when present, else the pinned C oracle"""
+    return O.Oracle("ref") if O.have_ref() else O.Oracle("c")
+
+
+def close(a, b, tol=DTOL):
+    if np.isinf(a) or np.isinf(b):
+        return a == b
+    return abs(a - b) <= tol * max(1.0, abs(b))
+
+
+def _bench():
+    import bench
+    return bench
+
+
+def _ev(E, ev):
+    return E.Events(ev.ids, ev.x, ev.t, ev.arr)
+
+
+def _replay(E, m, w, tape, tape_arr, s, final, init=None, dtype=np.float32, cap=2048):
+    eng = E.Engine(engine_model(m), w.signals.astype(dtype), event_capacity=cap)
+    if init is not None:
+        eng.set_hypothesis(_ev(E, init))
+    tr = eng.run_chromatic(engine_sampler(s), tape=tape, tape_arrivals=tape_arr)
+    out = tr.step_out
+    assert np.array_equal(out["scored"], tape["scored"])
+    drawn = tape["u_drawn"] == 1
+    tie = np.zeros(len(tape), bool)
+    tie[drawn] = np.abs(tape["log_r"][drawn] - np.log(tape["u"][drawn])) < TIE
+    sc = tape["scored"] == 1
+    tie |= sc & (np.abs(tape["log_r"]) < TIE)
+    mism = (out["accepted"] != tape["accepted"]) & ~tie
+    assert not mism.any(), np.where(mism)[0][:10]
+    bad = [i for i in np.where(sc)[0] if not close(out["delta"][i], tape["delta"][i])]
+    assert not bad, [(i, out["delta"][i], tape["delta"][i]) for i in bad[:5]]
+    fin = tr.final
+    assert np.array_equal(fin.ids, final.ids)
+    assert np.array_equal(fin.x, final.x) and np.array_equal(fin.t, final.t)
+    assert np.array_equal(fin.arrivals, final.arr)
+    return eng, tr
+
+
+# ------------------------------------------------------------------ config[1]
+@pytest.fixture(scope="module")
+def c1(E, ref):
+    b = _bench()
+    c = dict(b.CONFIGS[1])
+    om = O.Model(**b.model_params(c))
+    w = ref.sample_world(om, 0, cap=2048)
+    w.signals = w.signals.astype(np.float32).astype(np.float64)  # the fp32 inputs, widened
+    s = O.Sampler(steps_per_epoch=2, epochs=1, n_regions=c["n_regions"], seed=5, dynamic=0,
+                  record_every=1 << 30)
+    r = ref.run_chromatic(w, s, init=w.events, tape=True)
+    return c, om, w, s, r
+
+
+def test_config1_world_generator_matches_reference(E, c1):
+    c, om, w, _, _ = c1
+    m, ev, sig = _bench().make_world(c, os.cpu_count() or 1)
+    assert np.array_equal(ev.ids, w.events.ids)
+    assert np.array_equal(ev.x, w.events.x) and np.array_equal(ev.t, w.events.t)
+    assert np.array_equal(ev.arrivals, w.events.arr)
+    assert np.array_equal(sig.astype(np.float64), w.signals)
+
+
+def test_config1_reference_tape_replay(E, c1):
+    c, om, w, s, r = c1
+    t = r["tape"]
+    assert len(t) == 2 * c["n_regions"] and (t["scored"] == 1).sum() >= 200
+    assert (t["accepted"] == 1).sum() > 10  # both colors commit changes
+    _replay(E, om, w, t, r["tape_arr"], s, r["final"], init=w.events)
+
+
+def test_config1_score_batch_vs_reference_deltas(E, c1):
+    """every scored tape proposal of a color-0 region made before that region
+    accepted anything is scored against the truth hypothesis (frozen snapshot
+    = truth, no own diff): its reference delta is delta_log_joint(truth, change)"""
+    c, om, w, s, r = c1
+    t, ta = r["tape"], r["tape_arr"]
+    S = om.S
+    changes, want = [], []
+    seen_acc = set()
+    for i in range(len(t)):
+        if t["color"][i] != 0:
+            continue
+        reg = int(t["region"][i])
+        if reg in seen_acc:
+            continue
+        if t["scored"][i] == 1 and np.isfinite(t["delta"][i]):
+            rem = [int(t["removed_id"][i][q]) for q in range(int(t["n_removed"][i]))]
+            off = int(t["added_arr_off"][i])
+            add = [(t["added_x"][i][a], t["added_t"][i][a], ta[off + a * S: off + (a + 1) * S])
+                   for a in range(int(t["n_added"][i]))]
+            changes.append((rem, add))
+            want.append(t["delta"][i])
+        if t["accepted"][i] == 1:
+            seen_acc.add(reg)
+    assert len(changes) >= 120
+    eng = E.Engine(engine_model(om), w.signals.astype(np.float32), event_capacity=2048)
+    eng.set_hypothesis(_ev(E, w.events))
+    got = eng.delta_log_joint(changes)
+    bad = [(i, got[i], want[i]) for i in range(len(want)) if not close(got[i], want[i])]
+    assert not bad, bad[:5]
+
+
+def _random_changes(rng, m, ev, n_each):
+    """changes of every move shape against hypothesis ev (birth, death,
+    location, arrival, joint pair), arrivals drawn as the proposals do"""
+    S = m.S
+    st = np.asarray(m.stations)
+
+    def arrivals(x, t):
+        return t + np.abs(x - st) / m.v
+
+    out = []
+    for _ in range(n_each):
+        x, t = rng.uniform(0, m.x_max), rng.uniform(0, m.T)
+        out.append(([], [(x, t, arrivals(x, t) + m.sigma_arrival * rng.standard_normal(S))]))
+    for _ in range(n_each):
+        out.append(([int(ev.ids[rng.integers(ev.N)])], []))
+    for _ in range(n_each):
+        i = rng.integers(ev.N)
+        x, t = ev.x[i] + 4 * rng.standard_normal(), ev.t[i] + 4 * rng.standard_normal()
+        out.append(([int(ev.ids[i])], [(x, t, ev.arr[i] + (arrivals(x, t) -
+                                                            arrivals(ev.x[i], ev.t[i])))]))
+    for _ in range(n_each):
+        i = rng.integers(ev.N)
+        a = ev.arr[i].copy()
+        a[rng.integers(S)] += rng.standard_normal()
+        out.append(([int(ev.ids[i])], [(ev.x[i], ev.t[i], a)]))
+    for _ in range(max(1, n_each // 2)):
+        i, j = rng.choice(ev.N, 2, replace=False)
+        adds = []
+        for q in (i, j):
+            x, t = ev.x[q] + rng.standard_normal(), ev.t[q] + rng.standard_normal() / m.v
+            adds.append((x, t, ev.arr[q] + (arrivals(x, t) - arrivals(ev.x[q], ev.t[q]))))
+        out.append(([int(ev.ids[i]), int(ev.ids[j])], adds))
+    return out
+
+
+def _ref_deltas(ref, m, w, changes, threads=None):
+    idx = {int(v): i for i, v in enumerate(w.events.ids)}
+
+    def one(ch):
+        rem, add = ch
+        a = None
+        if add:
+            a = O.Events(np.arange(len(add), dtype=np.uint64) + (1 << 40),
+                         np.array([q[0] for q in add]), np.array([q[1] for q in add]),
+                         np.stack([np.asarray(q[2], np.float64) for q in add]))
+        return ref.delta(m, w.signals, w.events, [idx[r] for r in rem], a)
+
+    threads = threads or min(16, os.cpu_count() or 1)
+    with ThreadPoolExecutor(threads) as ex:  # the ctypes calls release the GIL
+        return list(ex.map(one, changes))
+
+
+def test_config2_score_batch_vs_reference_deltas(E, ref):
+    b = _bench()
+    c = dict(b.CONFIGS[2])
+    m, ev, sig = b.make_world(c, os.cpu_count() or 1)
+    om = O.Model(**b.model_params(c))
+    w = O.World(om, O.Events(ev.ids, ev.x, ev.t, ev.arrivals), sig.astype(np.float64))
+    changes = _random_changes(np.random.default_rng(2), om, w.events, 3)
+    assert len(changes) >= 13
+    want = _ref_deltas(ref, om, w, changes)
+    eng = E.Engine(m, sig, event_capacity=2 * ev.N + 256)
+    eng.set_hypothesis(E.Events(ev.ids, ev.x, ev.t, ev.arrivals))
+    got = eng.delta_log_joint(changes)
+    bad = [(i, got[i], want[i]) for i in range(len(want)) if not close(got[i], want[i])]
+    assert not bad, bad[:5]
+
+
+# ------------------------------------------------------------------ non-default ModelConfig
+NONDEFAULT = [
+    # 2 sigma^2 = 4.5 (not a power of two), shorter signals, two samples per
+    # time unit, other variances
+    dict(sigma_arrival=1.5, t_s=12.0, sample_rate=2.0, var_noise=0.5, var_event=3.0),
+    # 2 sigma^2 = 2.42, t_s longer than the 20-row dense band batch, rate 0.5
+    dict(sigma_arrival=1.1, t_s=33.0, sample_rate=0.5, var_noise=2.0, var_event=2.5),
+]
+
+
+def _nd_model(p, S=8, T=240.0, x_max=100.0, lam=0.05):
+    return O.Model(lambda_rate=lam, T=T, x_max=x_max, v=2.0, stations=O.stations_line(S, x_max),
+                   **p)
+
+
+@pytest.mark.parametrize("pi", range(len(NONDEFAULT)))
+def test_nondefault_model_reference_tape_replay(E, ref, pi):
+    m = _nd_model(NONDEFAULT[pi])
+    w = ref.sample_world(m, 3 + pi)
+    s = O.Sampler(steps_per_epoch=150, epochs=4, n_regions=4, seed=7 + pi, dynamic=1,
+                  record_every=1 << 30)
+    r = ref.run_chromatic(w, s, init=w.events, tape=True)
+    assert (r["tape"]["accepted"] == 1).sum() > 20
+    _replay(E, m, w, r["tape"], r["tape_arr"], s, r["final"], init=w.events,
+            dtype=np.float64, cap=512)
+
+
+@pytest.mark.parametrize("pi", range(len(NONDEFAULT)))
+def test_nondefault_model_production_matches_oracle(E, pi):
+    oc = O.Oracle("c")
+    m = _nd_model(NONDEFAULT[pi], S=24)
+    w = oc.sample_world(m, 11 + pi)
+    s = O.Sampler(steps_per_epoch=120, epochs=5, n_regions=4, seed=3 + pi, dynamic=1,
+                  rng_mode=1, record_every=200)
+    ro = oc.run_chromatic(w, s, tape=True, rowlj=True)
+    eng = E.Engine(engine_model(m), w.signals, event_capacity=1024)
+    tr = eng.run_chromatic(engine_sampler(s, record_log_joint=True), decisions=len(ro["tape"]))
+    so, t = tr.step_out, ro["tape"]
+    assert np.array_equal(so["accepted"], t["accepted"])
+    sc = (t["scored"] == 1) & np.isfinite(t["delta"])
+    assert np.allclose(so["delta"][sc], t["delta"][sc], rtol=1e-11, atol=1e-9)
+    assert tr.total_accepted == ro["total_accepted"] and tr.total_accepted > 10
+    assert np.array_equal(tr.final.ids, ro["final"].ids)
+    assert np.array_equal(tr.final.arrivals, ro["final"].arr)
+    assert np.allclose(tr.row_log_joint, ro["row_lj"], rtol=1e-12, atol=1e-8)
+
+
+@pytest.mark.parametrize("pi", range(len(NONDEFAULT)))
+def test_nondefault_model_score_batch(E, ref, pi):
+    m = _nd_model(NONDEFAULT[pi], S=40, lam=0.1)
+    w = ref.sample_world(m, 21 + pi)
+    changes = _random_changes(np.random.default_rng(pi), m, w.events, 20)
+    want = _ref_deltas(ref, m, w, changes)
+    eng = E.Engine(engine_model(m), w.signals, event_capacity=512)
+    eng.set_hypothesis(_ev(E, w.events))
+    got = eng.delta_log_joint(changes)
+    bad = [(i, got[i], want[i]) for i in range(len(want)) if not close(got[i], want[i])]
+    assert not bad, bad[:5]
+    assert close(eng.log_joint(), ref.log_joint(m, w.signals, w.events), 1e-12)
+
+
+# ------------------------------------------------------------------ failure recovery
+def test_pool_exhaustion_fails_loudly_and_engine_recovers(E, monkeypatch):
+    """A run whose arrival versions outgrow the pool stops with status 3 (the
+    failed pop is undone, no push lands outside the free stack) and the
+    engine is usable afterwards: reloading a hypothesis and running again
+    matches the oracle."""
+    monkeypatch.setenv("SEIS_POOL_SLOTS", "40")
+    oc = O.Oracle("c")
+    m = O.Model(lambda_rate=60 / 240.0)
+    w = oc.sample_world(m, 4)
+    eng = E.Engine(engine_model(m), w.signals, event_capacity=32)
+    assert eng.pool_slots == 40
+    with pytest.raises(RuntimeError, match="pool|table"):
+        eng.run_chromatic(E.SamplerConfig(steps_per_epoch=300, epochs=4, n_regions=4, seed=1))
+    few = O.Events(w.events.ids[:6], w.events.x[:6], w.events.t[:6], w.events.arr[:6])
+    s = O.Sampler(steps_per_epoch=20, epochs=2, n_regions=4, seed=9, dynamic=0, rng_mode=1,
+                  weights=(0.0, 0.25, 0.5, 0.25, 0.0))
+    ro = oc.run_chromatic(w, s, init=few, tape=False)
+    eng.set_hypothesis(_ev(E, few))
+    tr = eng.run_chromatic(engine_sampler(s))
+    assert np.array_equal(tr.final.ids, ro["final"].ids)
+    assert np.array_equal(tr.final.arrivals, ro["final"].arr)
+
+
+# ------------------------------------------------------------------ posterior, mapped shape
+def test_posterior_mapped_shape_within_seed_spread(E):
+    """north_star: posterior precision, recall and mean location error agree
+    with the reference's within seed-to-seed spread, on a BASELINE-mapped
+    shape (S = 96 stations, 32 time regions, l / tau = 1.2; the reference's
+    own run_sampler from the empty hypothesis: tests/golden/posterior_mapped.npz,
+    4 worlds x 3 seeds, make_golden_mapped.py). Engine: production mode
+    (philox stream) on the same worlds, 6 seeds each. Bar: |mean difference|
+    <= 3 standard errors of the difference, no extra slack."""
+    from tests.helpers import golden
+    g = golden("posterior_mapped.npz")
+    S, T, nr, x_max, n_ev = [float(v) for v in g["shape"]]
+    k, ep, nreg = [int(v) for v in g["sampler"]]
+    thr = float(g["threshold"][0])
+    oc = O.Oracle("c")
+    m = O.Model(lambda_rate=n_ev / T, T=T, x_max=x_max, v=1.2 * x_max * nr / T,
+                stations=O.stations_line(int(S), x_max))
+    rows = g["rows"]
+    stats = []
+    for ws in sorted(set(int(v) for v in rows[:, 0])):
+        w = oc.sample_world(m, ws)
+        assert w.events.N == int(rows[rows[:, 0] == ws][0, 6])  # the reference's world
+        eng = E.Engine(engine_model(m), w.signals, event_capacity=1024)
+        for rs in range(11, 17):
+            eng.set_hypothesis(E.Events(np.zeros(0, np.uint64), np.zeros(0), np.zeros(0),
+                                        np.zeros((0, m.S))))
+            sc = E.SamplerConfig(algorithm="chromatic-dynamic", steps_per_epoch=k, epochs=ep,
+                                 n_regions=nreg, seed=rs, burn_in_fraction=0.0,
+                                 record_every=1 << 30)
+            f = eng.run_chromatic(sc).final
+            stats.append(oc.match_events(w.events, O.Events(f.ids, f.x, f.t, f.arrivals),
+                                         thr)[:3])
+    gpu = np.array(stats)
+    ref = rows[:, 2:5]
+    for c, name in enumerate(["precision", "recall", "location_error"]):
+        a, b = gpu[:, c], ref[:, c]
+        se = np.sqrt(a.var(ddof=1) / len(a) + b.var(ddof=1) / len(b))
+        assert abs(a.mean() - b.mean()) <= 3.0 * se, (name, a.mean(), b.mean(), se)

@@ -51,7 +51,7 @@ def test_reference_arm_nonzero_rank_exits_clean():
     # the process group, so run rank 0 alongside it
     env0 = dict(env, RANK="0", LOCAL_RANK="0")
     cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2",
-           "--steps", "1", "--warmup", "0", "--ref-seconds", "0.5", "--config", "0"]
+           "--steps", "1", "--warmup", "3", "--ref-seconds", "0.3", "--config", "0"]
     p0 = subprocess.Popen(cmd, env=env0, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)
     p1 = subprocess.Popen(cmd, env=env, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)
     o1, e1 = p1.communicate(timeout=600)
@@ -64,3 +64,6 @@ def test_reference_arm_nonzero_rank_exits_clean():
     assert line["impl"] == "reference"
     if "unavailable" not in line:
         assert line["value"] > 0 and line["cpu_baseline"]["kind"] == "reference"
+        # the reference arm builds its world with the reference's generator and
+        # never loads the engine
+        assert line["detail"]["engine_imported"] is False
