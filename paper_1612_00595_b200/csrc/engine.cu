@@ -129,6 +129,61 @@ __global__ void k_region_of(const double* b, int n, int64_t m, const double* t, 
   if (i < m) out[i] = region_of(b, n, t[i]);
 }
 
+// Dispatch order of a color phase's region chains (longest processing time
+// first). A chain with no phase-start events proposes mostly null moves
+// (death, location, arrival and joint need an event) and costs a fraction of
+// one with events; CTAs are dispatched in blockIdx order, so slots with more
+// events go first and the cheap chains fill the last wave instead of leaving
+// SMs idle behind a late expensive chain. The order never changes results:
+// each chain's draws, births' ids and outputs are keyed by its slot.
+__device__ int block_scan_excl(int v, int* total);
+constexpr int kOrderBuckets = 3;  // phase-start events >= 2, 1, 0
+__global__ void __launch_bounds__(1024)
+    k_order(const double* tab_t, const int* n_events, const double* bnd, int nreg, int color,
+            int ncol, int ncr, int* cnt, int* order) {
+  __shared__ int s_tot[kOrderBuckets], s_base[kOrderBuckets];
+  const int tid = threadIdx.x;
+  for (int i = tid; i < ncr; i += blockDim.x) cnt[i] = 0;
+  __syncthreads();
+  const int N = *n_events;
+  for (int i = tid; i < N; i += blockDim.x) {
+    const int r = region_of(bnd, nreg, tab_t[i]);
+    if (r >= color && (r - color) % ncol == 0) atomicAdd(&cnt[(r - color) / ncol], 1);
+  }
+  __syncthreads();
+  // stable counting sort: buckets in decreasing cost, slots (time order)
+  // ascending inside a bucket, so concurrently running chains stay
+  // neighbours in time and share signal rows in L2
+  for (int b = tid; b < kOrderBuckets; b += blockDim.x) s_tot[b] = 0;
+  __syncthreads();
+  for (int s = tid; s < ncr; s += blockDim.x)
+    atomicAdd(&s_tot[max(0, kOrderBuckets - 1 - min(cnt[s], kOrderBuckets - 1))], 1);
+  __syncthreads();
+  if (tid == 0) {
+    int acc = 0;
+    for (int b = 0; b < kOrderBuckets; ++b) {
+      s_base[b] = acc;
+      acc += s_tot[b];
+    }
+  }
+  __syncthreads();
+  for (int c0 = 0; c0 < ncr; c0 += blockDim.x) {
+    const int s = c0 + tid;
+    const int b = s < ncr ? kOrderBuckets - 1 - min(cnt[s], kOrderBuckets - 1) : -1;
+    int pos = 0;
+#pragma unroll
+    for (int q = 0; q < kOrderBuckets; ++q) {
+      int tot;
+      const int ex = block_scan_excl(b == q ? 1 : 0, &tot);
+      if (b == q) pos = s_base[q] + ex;
+      __syncthreads();
+      if (tid == 0) s_base[q] += tot;
+      __syncthreads();
+    }
+    if (s < ncr) order[pos] = s;
+  }
+}
+
 // ----------------------------------------------------------------- signals
 template <typename YT>
 __global__ void k_transpose(const YT* __restrict__ src, YT* __restrict__ dst, int S, int S_pad,
@@ -391,7 +446,7 @@ __global__ void __launch_bounds__(NTT, MINB)
   __shared__ long long s_nlocal;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int slot_idx = blockIdx.x;
+  const int slot_idx = pa.slot_order ? pa.slot_order[blockIdx.x] : (int)blockIdx.x;
   if (tid == 0) {  // a CTA that stops on an error leaves nothing for the barrier
     pa.births_cnt[slot_idx] = 0;
     pa.diff_cnt[slot_idx] = 0;
@@ -1519,8 +1574,18 @@ namespace {
 thread_local std::string g_err;
 // dynamic: the log(i) window + per-lane partial sums (2 double + 1 int per
 // speculative slot and thread)
-constexpr int kPhaseSmem = LOGIWIN * (int)sizeof(double) + MSPEC * NT * (2 * 8 + 4) +
-                           kDiffCache * (int)(sizeof(DiffS) + sizeof(DiffS4x));
+constexpr int kPhaseSmemTile = LOGIWIN * (int)sizeof(double) + MSPEC * NT * (2 * 8 + 4);
+// + the per-round diff-window cache of the proposal-major pass (few stations)
+constexpr int kPhaseSmem = kPhaseSmemTile + kDiffCache * (int)(sizeof(DiffS) + sizeof(DiffS4x));
+// The tile-major pass (S_pad >= 2048: 64 station tiles and more) never builds
+// the diff-window cache, so its launches leave that shared memory to L1: the
+// band rows a warp's proposals share on a tile stay resident between them.
+// SEIS_SMEM_FULL=1 keeps the full allocation (A/B).
+inline int phase_smem(const Dev& d) {
+  static const bool full = getenv("SEIS_SMEM_FULL") && atoi(getenv("SEIS_SMEM_FULL")) == 1;
+  const bool dcache = (d.S_pad + 31) / 32 < 4 * NW && d.S_pad <= kDiffCache && d.n < 65535;
+  return (dcache || full) ? kPhaseSmem : kPhaseSmemTile;
+}
 
 int fail(int code, const std::string& m) {
   g_err = m;
@@ -1759,7 +1824,8 @@ namespace {
 // config[2]): a chain's rounds slow down more than sharing an SM gains.
 template <typename YT, int MODE>
 void launch_phase_t(seis_engine* e, int ncr, const Samp& sp, const PhaseArgs& pa, int stamp) {
-  k_phase<YT, MODE, NT, SEIS_MINB><<<ncr, NT, kPhaseSmem, e->stream>>>(e->d, sp, pa, e->ctl, stamp);
+  k_phase<YT, MODE, NT, SEIS_MINB><<<ncr, NT, phase_smem(e->d), e->stream>>>(e->d, sp, pa, e->ctl,
+                                                                            stamp);
 }
 
 void launch_phase(seis_engine* e, int mode, int ncr, const Samp& sp, const PhaseArgs& pa,
@@ -1912,10 +1978,6 @@ int seis_engine_create(const seis_model_cfg* cfg, const double* stations, int64_
     d.c0_arr = -0.5 * (kLog2Pi + std::log(var_a));
     d.inv_twovar_arr = 1.0 / (2.0 * var_a);
     d.twovar_arr = 2.0 * var_a;
-    {
-      int ex = 0;
-      d.arr_div = std::frexp(d.twovar_arr, &ex) == 0.5 ? 0 : 1;  // mantissa 0.5: a power of two
-    }
     d.inv_v = 1.0 / cfg->v;
     d.log_lambda_T = std::log(cfg->lambda_rate * cfg->T);
     d.lxa = -std::log(cfg->x_max) - std::log(cfg->T);
@@ -2422,6 +2484,10 @@ static int run_driver(seis_engine* e, const seis_sampler_cfg* sc, int32_t mode,
     OutEv* births = static_cast<OutEv*>(alloc((size_t)n_slots * MAXOWN * sizeof(OutEv)));
     int* diff_cnt = static_cast<int*>(alloc((size_t)n_slots * 4));
     DiffPair* diff = static_cast<DiffPair*>(alloc((size_t)n_slots * MAXDOUT * sizeof(DiffPair)));
+    // cost-ordered dispatch (k_order); SEIS_ORDER=0 disables it (A/B)
+    const bool use_order = !serial && !(getenv("SEIS_ORDER") && atoi(getenv("SEIS_ORDER")) == 0);
+    int* order_cnt = static_cast<int*>(alloc((size_t)n_slots * 4));
+    int* order = static_cast<int*>(alloc((size_t)n_slots * 4));
     seis_tape_step* d_tape = nullptr;
     double* d_tarr = nullptr;
     seis_step_out* d_out = nullptr;
@@ -2538,6 +2604,13 @@ static int run_driver(seis_engine* e, const seis_sampler_cfg* sc, int32_t mode,
         evs.push_back(a);
         evs.push_back(b);
         ck(cudaEventRecord(a, e->stream), "event");
+      }
+      if (use_order && ncr > e->n_sm) {
+        k_order<<<1, 1024, 0, e->stream>>>(e->tab[e->cur].t, &e->ctl->n_events, bndp, nreg,
+                                           color, std::max(ncol, 1), ncr, order_cnt, order);
+        ck(cudaGetLastError(), "k_order");
+        pa.slot_order = order;
+        ++launches;
       }
       launch_phase(e, mode, ncr, spk, pa, stamp);
       if (timing) {

@@ -67,8 +67,7 @@ struct Dev {
   int rows;                        // n + kRowPad
   double rate, t_s, v, sigma, x_max, T;
   double c0_arr, inv_twovar_arr;   // log_gaussian constants for sigma_arrival
-  double twovar_arr;               // 2 sigma^2 (divided by when it is not a power of two)
-  int arr_div;                     // 1: 2 sigma^2 is not a power of two -> true division
+  double twovar_arr;               // 2 sigma^2
   double inv_v;                    // RN(1 / v): division by v as a reciprocal + one correction
   double log_lambda_T, lxa;        // log(lambda T), -log(x_max) - log(T)
   double log_xmax;
@@ -160,6 +159,10 @@ struct PhaseArgs {
   long long step_base;             // chain step of this launch's first step
   int* births_total;               // [n_slots] accepted births of the phase (may be null)
   unsigned long long* order_io;    // serial: [0] count, [1..] ids in list order (may be null)
+  // dispatch order: CTA b runs region slot slot_order[b] (k_order: slots with
+  // more phase-start events first, so the cheap event-free chains fill the
+  // last wave); null = identity
+  const int* slot_order;
 };
 
 enum : int {
@@ -213,13 +216,14 @@ __device__ __forceinline__ double arrival_mean(const Dev& d, double x, double t,
 
 __device__ __forceinline__ double arr_logpdf(const Dev& d, double a, double mean) {
   // log_gaussian(a, mean, sigma^2), density.hpp:15-18 with host-computed
-  // -0.5 (log 2pi + log sigma^2). When 2 sigma^2 is a power of two (the
-  // reference default sigma_arrival = 2) the division by it is exactly a
-  // multiplication by its reciprocal; otherwise (d.arr_div, warp-uniform) the
-  // reference's division is kept so every ModelConfig stays bit-exact.
+  // -0.5 (log 2pi + log sigma^2); the division d^2 / (2 sigma^2) is the
+  // correctly rounded quotient by the reciprocal + one FMA correction, as in
+  // div_v (bit-identical to the reference's division for every sigma_arrival;
+  // exact in the first step already when 2 sigma^2 is a power of two)
   const double dd = a - mean;
-  const double q = d.arr_div ? __ddiv_rn(dd * dd, d.twovar_arr) : dd * dd * d.inv_twovar_arr;
-  return d.c0_arr - q;
+  const double n2 = dd * dd;
+  const double q0 = n2 * d.inv_twovar_arr;
+  return d.c0_arr - fma(fma(-q0, d.twovar_arr, n2), d.inv_twovar_arr, q0);
 }
 
 }  // namespace seis

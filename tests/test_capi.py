@@ -125,3 +125,15 @@ def test_world_file_round_trip(built, tmp_path):
         f.write(b"NOTWORLD")
     with pytest.raises(ValueError):
         E.load_world(p)
+
+
+@pytest.mark.skipif(not O.have_ref(), reason="needs oracle/_ref (reference tree)")
+def test_thomas_events_match_reference_rng(built):
+    """config[4]'s Thomas cluster process: the engine's host generator and the
+    same draws made with the reference's own Rng (oracle/_ref, used by the
+    reference arm of bench.py) give identical events"""
+    from paper_1612_00595_b200 import thomas_events
+    for T, x_max, pm in ((1024.0, 32000.0, 2000.0), (240.0, 100.0, 5.0)):
+        cx, ct = thomas_events(3, x_max, T, pm, 10.0, 50.0, 0.0015625 * T)
+        rx, rt = O.ref_thomas_events(3, x_max, T, pm, 10.0, 50.0, 0.0015625 * T)
+        assert len(cx) > 0 and np.array_equal(cx, rx) and np.array_equal(ct, rt)

@@ -340,3 +340,41 @@ def test_posterior_mapped_shape_within_seed_spread(E):
         a, b = gpu[:, c], ref[:, c]
         se = np.sqrt(a.var(ddof=1) / len(a) + b.var(ddof=1) / len(b))
         assert abs(a.mean() - b.mean()) <= 3.0 * se, (name, a.mean(), b.mean(), se)
+
+
+# ------------------------------------------------------------------ Trace::phases / wall clock
+def test_phase_records_commit_colors_in_order(E):
+    """test_samplers.cpp:130-155: within an epoch every color-0 commit precedes
+    every color-1 commit, one PhaseRecord per committed region
+    (samplers.hpp:479) with the epoch's steps; dynamic partitions change the
+    region count between epochs; row wall clocks increase."""
+    oc = O.Oracle("c")
+    m = O.Model()
+    w = oc.sample_world(m, 5)
+    eng = E.Engine(engine_model(m), w.signals)
+    for alg in ("chromatic-static", "chromatic-dynamic"):
+        eng.set_hypothesis(E.Events(np.zeros(0, np.uint64), np.zeros(0), np.zeros(0),
+                                    np.zeros((0, m.S))))
+        tr = eng.run_chromatic(E.SamplerConfig(algorithm=alg, epochs=4, steps_per_epoch=100,
+                                               n_regions=4, seed=3, record_every=400))
+        ph = tr.phases
+        assert len(ph) >= 4 * 4
+        last_epoch, last_color = -1, -1
+        for p in ph:
+            if p["epoch"] != last_epoch:
+                assert p["epoch"] == last_epoch + 1 and p["color"] == 0
+                last_epoch = p["epoch"]
+            else:
+                assert p["color"] >= last_color
+            last_color = p["color"]
+            assert p["steps"] == 100 and p["region"] % 2 == p["color"]
+        assert last_epoch == 3
+        assert int(ph["steps"].sum()) == tr.total_steps
+        assert len(tr.row_wall) == len(tr.row_step)
+        assert tr.row_wall[0] >= 0 and np.all(np.diff(tr.row_wall) > 0)
+    # naive: one record per region (samplers.hpp:370); serial: none
+    eng.set_hypothesis(E.Events(np.zeros(0, np.uint64), np.zeros(0), np.zeros(0),
+                                np.zeros((0, m.S))))
+    tr = eng.run_chromatic(E.SamplerConfig(algorithm="naive", epochs=2, steps_per_epoch=50,
+                                           n_regions=4, seed=3))
+    assert list(tr.phases["region"]) == [0, 1, 2, 3] and set(tr.phases["steps"]) == {100}

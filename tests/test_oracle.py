@@ -261,6 +261,7 @@ int main(int argc, char** argv) {
     for (long i = 0; i < 10000000; ++i) {
       double a = u01() * span;
       if (i & 1) a = floor(a * 1024.0) / 1024.0;  /* station-grid-like operands */
+      if (span < 0) { const double dd = u01() * 40.0 - 20.0; a = dd * dd; } /* (a - mean)^2 */
       const double q0 = a * y, q = fma(fma(-q0, v, a), y, q0);
       bad += q != a / v;
     }
@@ -287,6 +288,10 @@ def test_division_by_reciprocal_is_exact(tmp_path):
     for x_max, T, R in [(1000, 3600, 4), (4000, 3600, 16), (16000, 3600, 64), (16000, 1800, 128),
                         (32000, 1024, 256)]:
         cases.append((1.2 * x_max * R * R / T, float(x_max)))
+    # arr_logpdf: (a - mean)^2 / (2 sigma^2) for sigma_arrival values whose
+    # 2 sigma^2 is and is not a power of two (span < 0 selects squared operands)
+    for sig in (2.0, 1.5, 1.1, 0.7, 3.3, 2.5):
+        cases.append((2.0 * (sig * sig), -1.0))
     args = [f"{x:.17g}" for c in cases for x in c]
     out = subprocess.run([str(exe)] + args, check=True, capture_output=True, text=True).stdout
     assert int(out.strip()) == 0
