@@ -161,6 +161,7 @@ int seis_get_hypothesis(seis_engine* eng, int64_t cap, int64_t* n, uint64_t* ids
  * at every trace row once executed >= burn_in_fraction * planned steps.
  * Snapshots are packed back to back: snapshot i holds snap_count[i] events. */
 int seis_set_snapshot_capacity(seis_engine* eng, int64_t max_events, int64_t max_snapshots);
+/* ids == NULL: only snap_step / snap_count are written (sizes the event buffers) */
 int seis_get_snapshots(seis_engine* eng, int64_t cap_snap, int64_t* n_snap, int64_t* snap_step,
                        int64_t* snap_count, int64_t cap_ev, uint64_t* ids, double* x, double* t);
 

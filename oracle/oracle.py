@@ -135,6 +135,34 @@ def build(quiet: bool = True) -> None:
                    stdout=subprocess.DEVNULL if quiet else None)
 
 
+REF_INC = "/root/reference/proj/include"
+BINDING_CHECK = os.path.join(HERE, "_ref", "binding_check")
+
+
+def build_binding() -> str | None:
+    """Compile tests/binding/binding_check.cpp — include/seis_b200.hpp (the
+    C++ binding of INTEGRATION.md) against the unmodified reference headers,
+    linked to the engine library — into oracle/_ref/binding_check. Needs the
+    reference tree (this container) and the built engine; the binary travels
+    to the GPU box. Returns the path, or None when it cannot be built here."""
+    root = os.path.dirname(HERE)
+    src = os.path.join(root, "tests", "binding", "binding_check.cpp")
+    lib = os.path.join(root, "paper_1612_00595_b200", "_lib")
+    deps = [src, os.path.join(root, "include", "seis_b200.hpp"),
+            os.path.join(root, "include", "seis_b200.h"), os.path.join(lib, "libseis_b200.so")]
+    if not os.path.isdir(os.path.join(REF_INC, "seismic")) or not os.path.exists(deps[-1]):
+        return BINDING_CHECK if os.path.exists(BINDING_CHECK) else None
+    if os.path.exists(BINDING_CHECK) and all(
+            os.path.getmtime(d) <= os.path.getmtime(BINDING_CHECK) for d in deps):
+        return BINDING_CHECK
+    os.makedirs(os.path.dirname(BINDING_CHECK), exist_ok=True)
+    subprocess.run(["g++", "-std=gnu++20", "-O2", "-pthread", "-I", REF_INC,
+                    "-I", os.path.join(root, "include"), src, "-L", lib, "-lseis_b200",
+                    "-Wl,-rpath,$ORIGIN/../../paper_1612_00595_b200/_lib", "-o", BINDING_CHECK],
+                   check=True)
+    return BINDING_CHECK
+
+
 class Oracle:
     def __init__(self, which: str = "c"):
         path, pre = (ORACLE_SO, "so_") if which == "c" else (REF_SO, "sr_")

@@ -2180,6 +2180,7 @@ int seis_get_snapshots(seis_engine* e, int64_t cap_snap, int64_t* n_snap, int64_
       snap_count[i] = rec[2 * i + 1];
       total = std::max<int64_t>(total, rec[2 * i] + rec[2 * i + 1]);
     }
+    if (!ids) return;  // steps and counts only
     if (total > cap_ev) throw std::invalid_argument("event buffer too small for the snapshots");
     if (total > 0) {
       ck(cudaMemcpy(ids, e->snap_id, total * 8, cudaMemcpyDeviceToHost), "D2H");
@@ -2915,6 +2916,19 @@ extern "C" int seis_run_naive(seis_engine* e, const seis_sampler_cfg* sc, int32_
                                           e->fate_slot, nreg, births_cnt, births, e->ctl);
     ck(cudaGetLastError(), "naive commit");
     e->cur = nxt;
+    // the union's final snapshot (samplers.hpp:388-391 at the last checkpoint;
+    // the intermediate checkpoints' event lists are not kept on the device)
+    e->snap_steps.clear();
+    if (e->snap_cap > 0) {
+      const long long zero = 0;
+      ck(cudaMemcpyAsync(e->snap_top, &zero, 8, cudaMemcpyHostToDevice, e->stream), "H2D");
+      const int64_t total = spr * nreg;
+      if (total >= (int64_t)(sc->burn_in_fraction * (double)total) && e->snap_rec_cap > 0) {
+        k_snapshot<<<1, 256, 0, e->stream>>>(e->tab[e->cur], e->ctl, e->snap_id, e->snap_x,
+                                              e->snap_t, e->snap_top, e->snap_cap, e->snap_rec);
+        e->snap_steps.push_back(total);
+      }
+    }
     double* lj_dev = static_cast<double*>(alloc(8));
     double* lj_scratch = static_cast<double*>(alloc((2 * 296 + 1) * 8));
     if (sc->record_log_joint) launch_lj_any(e, lj_dev, lj_scratch);

@@ -137,3 +137,19 @@ def test_thomas_events_match_reference_rng(built):
         cx, ct = thomas_events(3, x_max, T, pm, 10.0, 50.0, 0.0015625 * T)
         rx, rt = O.ref_thomas_events(3, x_max, T, pm, 10.0, 50.0, 0.0015625 * T)
         assert len(cx) > 0 and np.array_equal(cx, rx) and np.array_equal(ct, rt)
+
+
+@pytest.mark.skipif(not os.path.isdir(O.REF_INC), reason="needs the reference headers")
+def test_cpp_binding_compiles_against_reference_headers(built):
+    """include/seis_b200.hpp (INTEGRATION.md's binding) compiles against the
+    unmodified reference headers and links the engine; without a GPU its
+    errors follow the reference's: std::invalid_argument for validation,
+    std::runtime_error for the missing device"""
+    import subprocess
+    import torch
+    exe = O.build_binding()
+    assert exe and os.path.exists(exe)
+    if torch.cuda.is_available():
+        pytest.skip("GPU present: covered by test_gpu_baseline_parity")
+    r = subprocess.run([exe, "cpu"], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0 and "OK cpu" in r.stdout, r.stdout + r.stderr

@@ -378,3 +378,18 @@ def test_phase_records_commit_colors_in_order(E):
     tr = eng.run_chromatic(E.SamplerConfig(algorithm="naive", epochs=2, steps_per_epoch=50,
                                            n_regions=4, seed=3))
     assert list(tr.phases["region"]) == [0, 1, 2, 3] and set(tr.phases["steps"]) == {100}
+
+
+# ------------------------------------------------------------------ the C++ binding
+def test_cpp_binding_run_sampler_on_gpu(E):
+    """seismic::b200::run_sampler (include/seis_b200.hpp, compiled against the
+    reference headers in the build container: oracle/_ref/binding_check) for
+    every algorithm next to the reference's own run_sampler: same total steps,
+    trace-row steps, Trace::phases and snapshot steps; increasing wall clocks"""
+    import subprocess
+    exe = O.build_binding()
+    if not exe:
+        pytest.skip("binding_check not built (needs the reference headers at build time)")
+    r = subprocess.run([exe, "gpu"], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    assert r.returncode == 0 and "OK gpu" in r.stdout, r.stdout + r.stderr
