@@ -152,6 +152,16 @@ int seis_upload_signals(seis_engine* eng, const void* signals);
 
 int seis_set_hypothesis(seis_engine* eng, int64_t n, const uint64_t* ids, const double* x,
                         const double* t, const double* arrivals /* [n][S] */);
+/* The same in pieces, for hypotheses whose arrivals do not fit in host memory
+ * at once: _begin takes the events, _rows uploads the arrival rows of input
+ * events i0 .. i0 + n - 1 (any order, every row exactly once), _end builds the
+ * coverage counts. Other calls on the engine between _begin and _end are an
+ * error (status 2). */
+int seis_set_hypothesis_begin(seis_engine* eng, int64_t n, const uint64_t* ids, const double* x,
+                              const double* t);
+int seis_set_hypothesis_rows(seis_engine* eng, int64_t i0, int64_t n,
+                             const double* arrivals /* [n][S] */);
+int seis_set_hypothesis_end(seis_engine* eng);
 /* arrivals may be NULL; *n receives the event count, at most cap are written */
 int seis_get_hypothesis(seis_engine* eng, int64_t cap, int64_t* n, uint64_t* ids, double* x,
                         double* t, double* arrivals);
@@ -232,6 +242,21 @@ int seis_world_with_events(const seis_model_cfg* cfg, const double* stations, in
                            int64_t n, const double* cx, const double* ct, uint64_t seed,
                            double* arrivals /* [n][S] */, void* signals /* [S][n] */,
                            int32_t dtype, int32_t threads);
+/* Streaming generation (no N x S arrival matrix in host memory): the same
+ * events and signals as seis_world_generate / seis_world_with_events, the
+ * coverage counts accumulated per station from chunks of events; arrivals of
+ * any event range regenerated with seis_world_arrivals (for
+ * seis_set_hypothesis_begin/_rows/_end). */
+int seis_world_generate_events(const seis_model_cfg* cfg, const double* stations, int64_t S,
+                               uint64_t seed, int64_t cap, int64_t* n_events, uint64_t* ids,
+                               double* x, double* t, void* signals /* [S][n] */, int32_t dtype,
+                               int32_t threads);
+int seis_world_with_events_signals(const seis_model_cfg* cfg, const double* stations, int64_t S,
+                                   int64_t n, const double* cx, const double* ct, uint64_t seed,
+                                   void* signals /* [S][n] */, int32_t dtype, int32_t threads);
+int seis_world_arrivals(const seis_model_cfg* cfg, const double* stations, int64_t S,
+                        uint64_t seed, int64_t i0, int64_t n, const double* x, const double* t,
+                        double* arrivals /* [n][S] */, int32_t threads);
 int seis_thomas_events(uint64_t seed, double x_max, double T, double parent_mean,
                        double child_mean, double sx, double st, int64_t cap, int64_t* n,
                        double* cx, double* ct);

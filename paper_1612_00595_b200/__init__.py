@@ -8,4 +8,5 @@ from .engine import (  # noqa: F401
     F32, F64, BootstrapCI, Engine, Events, MatchReport, ModelConfig, Partition, SamplerConfig,
     Snapshot, Trace, assign_regions, bootstrap_ci, match_events, metric_trace,
     load_library, load_world, make_world_with_events, partition, partition_offset, run_sampler,
-    sample_world, save_world, thomas_events)
+    sample_world, sample_world_events, make_world_with_events_signals, save_world,
+    thomas_events, world_arrivals)

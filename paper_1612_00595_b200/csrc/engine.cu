@@ -1667,6 +1667,11 @@ struct seis_engine {
   // time of its trace rows since the run started (TraceRow/Snapshot wall_seconds)
   std::vector<seis_phase_record> phases;
   std::vector<double> row_wall;
+  // hypothesis load in pieces (seis_set_hypothesis_begin/_rows/_end)
+  int64_t load_n = -1, load_chunk = 0;
+  std::vector<int> load_slot_of_row;
+  double* load_raw = nullptr;
+  int* load_dslot = nullptr;
   cudaStream_t stream = nullptr;
   Dev d{};
   double* stations = nullptr;
@@ -2024,10 +2029,14 @@ int seis_upload_signals(seis_engine* e, const void* signals) {
   return guarded([&] { upload_signals(e, signals); });
 }
 
-int seis_set_hypothesis(seis_engine* e, int64_t N, const uint64_t* ids, const double* x,
-                        const double* t, const double* arrivals) {
-  bool cov_failed = false;
-  const int rc = guarded([&] {
+// Hypothesis load in pieces (seis_set_hypothesis = begin + rows + end): the
+// table in id order (the reference's World::events after sort_by_id), slot i
+// for the i-th smallest id, arrival rows scattered to their slots through a
+// <= 512 MiB device staging buffer, then the coverage counts.
+namespace {
+int hyp_begin(seis_engine* e, int64_t N, const uint64_t* ids, const double* x, const double* t) {
+  return guarded([&] {
+    e->load_n = -1;
     if (N < 0 || N > e->cap) throw std::invalid_argument("hypothesis larger than event_capacity");
     std::vector<int64_t> order(N);
     for (int64_t i = 0; i < N; ++i) order[i] = i;
@@ -2036,49 +2045,36 @@ int seis_set_hypothesis(seis_engine* e, int64_t N, const uint64_t* ids, const do
       if (ids[order[i]] == ids[order[i - 1]]) throw std::invalid_argument("duplicate event id");
     std::vector<unsigned long long> hid(N);
     std::vector<double> hx(N), ht(N);
-    std::vector<long long> row(N);
     std::vector<int> hs(N), fs(e->pool_slots);
+    e->load_slot_of_row.assign(N, 0);
     for (int64_t i = 0; i < N; ++i) {
       const int64_t k = order[i];
       hid[i] = ids[k];
       hx[i] = x[k];
       ht[i] = t[k];
       hs[i] = (int)i;
-      row[i] = k;  // slot i holds input row k
+      e->load_slot_of_row[k] = (int)i;  // input row k goes to slot i
     }
     // free stack: slots N..pool_slots-1 (top of stack = lowest)
     int nf = 0;
     for (int s2 = e->pool_slots - 1; s2 >= (int)N; --s2) fs[nf++] = s2;
     e->cur = 0;
     Table& tb = e->tab[0];
+    scratch_reset(e);
+    e->load_chunk = std::max<int64_t>(
+        1, std::min<int64_t>({std::max<int64_t>(N, 1), ((int64_t)512 << 20) / ((int64_t)e->S * 8),
+                              65535}));
+    e->load_raw = scratch_of<double>(e, (size_t)e->load_chunk * e->S);
+    e->load_dslot = scratch_of<int>(e, std::max<int64_t>(N, 1));
     if (N) {
-      // stream-ordered copies from pageable vectors (each returns once staged;
-      // the vectors outlive the final synchronisation in read_ctl)
+      // stream-ordered copies from pageable vectors (each returns once staged)
       ck(cudaMemcpyAsync(tb.id, hid.data(), N * 8, cudaMemcpyHostToDevice, e->stream), "H2D");
       ck(cudaMemcpyAsync(tb.x, hx.data(), N * 8, cudaMemcpyHostToDevice, e->stream), "H2D");
       ck(cudaMemcpyAsync(tb.t, ht.data(), N * 8, cudaMemcpyHostToDevice, e->stream), "H2D");
       ck(cudaMemcpyAsync(tb.slot, hs.data(), N * 4, cudaMemcpyHostToDevice, e->stream), "H2D");
-      // arrivals in chunks of input rows (<= 512 MiB staging), each row
-      // scattered to its slot
-      std::vector<int> slot_of_row(N);
-      for (int64_t i = 0; i < N; ++i) slot_of_row[row[i]] = (int)i;
-      const int64_t chunk = std::max<int64_t>(
-          1, std::min<int64_t>({N, ((int64_t)512 << 20) / ((int64_t)e->S * 8), 65535}));
-      scratch_reset(e);
-      double* raw = scratch_of<double>(e, (size_t)chunk * e->S);
-      int* dslot = scratch_of<int>(e, N);
-      ck(cudaMemcpyAsync(dslot, slot_of_row.data(), (size_t)N * 4, cudaMemcpyHostToDevice,
-                         e->stream),
+      ck(cudaMemcpyAsync(e->load_dslot, e->load_slot_of_row.data(), (size_t)N * 4,
+                         cudaMemcpyHostToDevice, e->stream),
          "H2D");
-      for (int64_t r0 = 0; r0 < N; r0 += chunk) {
-        const int64_t nr = std::min(chunk, N - r0);
-        ck(cudaMemcpyAsync(raw, arrivals + (size_t)r0 * e->S, (size_t)nr * e->S * 8,
-                           cudaMemcpyHostToDevice, e->stream),
-           "H2D arrivals");
-        dim3 grid((unsigned)std::min(64, (e->S_pad + 255) / 256), (unsigned)nr);
-        k_scatter_arrivals<<<grid, 256, 0, e->stream>>>(raw, dslot + r0, e->S, e->S_pad, e->pool);
-        ck(cudaGetLastError(), "k_scatter_arrivals");
-      }
     }
     if (nf)
       ck(cudaMemcpyAsync(e->free_stack, fs.data(), (size_t)nf * 4, cudaMemcpyHostToDevice,
@@ -2089,9 +2085,50 @@ int seis_set_hypothesis(seis_engine* e, int64_t N, const uint64_t* ids, const do
     c.free_top = nf;
     ck(cudaMemcpyAsync(e->ctl, &c, sizeof c, cudaMemcpyHostToDevice, e->stream), "H2D");
     ck(cudaMemsetAsync(e->cov, 0, (size_t)(e->n + kRowPad) * e->P2 * 4, e->stream), "memset");
+    // (pageable sources: each copy returned once its data was staged)
+    e->load_n = N;
+  });
+}
+
+int hyp_rows(seis_engine* e, int64_t i0, int64_t n, const double* arrivals, bool sync) {
+  return guarded([&] {
+    if (e->load_n < 0) throw std::invalid_argument("seis_set_hypothesis_rows without _begin");
+    if (i0 < 0 || n < 0 || i0 + n > e->load_n)
+      throw std::invalid_argument("arrival rows outside the hypothesis");
+    for (int64_t r0 = 0; r0 < n; r0 += e->load_chunk) {
+      const int64_t nr = std::min(e->load_chunk, n - r0);
+      ck(cudaMemcpyAsync(e->load_raw, arrivals + (size_t)r0 * e->S, (size_t)nr * e->S * 8,
+                         cudaMemcpyHostToDevice, e->stream),
+         "H2D arrivals");
+      dim3 grid((unsigned)std::min(64, (e->S_pad + 255) / 256), (unsigned)nr);
+      k_scatter_arrivals<<<grid, 256, 0, e->stream>>>(e->load_raw, e->load_dslot + i0 + r0, e->S,
+                                                      e->S_pad, e->pool);
+      ck(cudaGetLastError(), "k_scatter_arrivals");
+    }
+    // the caller may reuse its (possibly pinned) buffer after the call
+    if (sync) ck(cudaStreamSynchronize(e->stream), "sync");
+  });
+}
+}  // namespace
+
+int seis_set_hypothesis_begin(seis_engine* e, int64_t N, const uint64_t* ids, const double* x,
+                              const double* t) {
+  return hyp_begin(e, N, ids, x, t);
+}
+
+int seis_set_hypothesis_rows(seis_engine* e, int64_t i0, int64_t n, const double* arrivals) {
+  return hyp_rows(e, i0, n, arrivals, true);
+}
+
+int seis_set_hypothesis_end(seis_engine* e) {
+  bool cov_failed = false;
+  const int rc = guarded([&] {
+    if (e->load_n < 0) throw std::invalid_argument("seis_set_hypothesis_end without _begin");
+    const int64_t N = e->load_n;
+    e->load_n = -1;
     if (N) {
       dim3 grid((e->P2 + 127) / 128, (unsigned)std::min<int64_t>(N, 65535));
-      k_build_cov<<<grid, 128, 0, e->stream>>>(e->d, tb, e->ctl);
+      k_build_cov<<<grid, 128, 0, e->stream>>>(e->d, e->tab[0], e->ctl);
       ck(cudaGetLastError(), "k_build_cov");
     }
     const Ctl after = read_ctl(e);  // the one synchronisation of the call
@@ -2105,6 +2142,16 @@ int seis_set_hypothesis(seis_engine* e, int64_t N, const uint64_t* ids, const do
     seis_set_hypothesis(e, 0, nullptr, nullptr, nullptr, nullptr);
     g_err = msg;
   }
+  return rc;
+}
+
+int seis_set_hypothesis(seis_engine* e, int64_t N, const uint64_t* ids, const double* x,
+                        const double* t, const double* arrivals) {
+  // one synchronisation for the whole call (in _end)
+  int rc = hyp_begin(e, N, ids, x, t);
+  if (rc == SEIS_OK && N > 0) rc = hyp_rows(e, 0, N, arrivals, false);
+  if (rc == SEIS_OK) return seis_set_hypothesis_end(e);
+  e->load_n = -1;
   return rc;
 }
 

@@ -128,6 +128,74 @@ struct Gen {
   }
 };
 
+// Streaming variant: the coverage counts of
+// worldgen.hpp:42-46 without materialising the N x S arrival matrix. Events
+// are drawn in chunks of B (their per-event streams are independent,
+// worldgen.hpp:34-38); each chunk's windows go into per-station difference
+// arrays (+1 at lo, -1 at hi; stations split over threads, no atomics), the
+// prefix sums are the reference's counts exactly (integer increments
+// commute). Host memory: S (n + 1) int32 + B S fp64, independent of N.
+struct StreamCounts {
+  const Gen& g;
+  int threads;
+  std::vector<int32_t> diff;  // [S][n + 1]
+  std::vector<double> buf;    // [B][S]
+  int64_t B;
+  StreamCounts(const Gen& g_, int threads_) : g(g_), threads(std::max(1, threads_)) {
+    diff.assign(static_cast<size_t>(g.S) * (g.n + 1), 0);
+    B = std::max<int64_t>(1, std::min<int64_t>(4096, ((int64_t)256 << 20) / (8 * g.S)));
+    buf.resize(static_cast<size_t>(B) * g.S);
+  }
+  template <class F>
+  void par(int64_t n, F&& f) {
+    const int64_t T = std::max<int64_t>(1, std::min<int64_t>(threads, n));
+    std::vector<std::thread> pool;
+    for (int64_t k = 0; k < T; ++k) pool.emplace_back([&, k] { f(n * k / T, n * (k + 1) / T); });
+    for (auto& th : pool) th.join();
+  }
+  void add(uint64_t seed, int64_t N, const double* x, const double* t) {
+    for (int64_t e0 = 0; e0 < N; e0 += B) {
+      const int64_t nb = std::min(B, N - e0);
+      par(nb, [&](int64_t a, int64_t b) {
+        for (int64_t i = a; i < b; ++i)
+          g.arrivals(seed, (uint64_t)(e0 + i), x[e0 + i], t[e0 + i], buf.data() + i * g.S);
+      });
+      par(g.S, [&](int64_t j0, int64_t j1) {
+        for (int64_t j = j0; j < j1; ++j) {
+          int32_t* d = diff.data() + static_cast<size_t>(j) * (g.n + 1);
+          for (int64_t i = 0; i < nb; ++i) {
+            int64_t lo, hi;
+            g.range(buf[i * g.S + j], lo, hi);
+            if (lo < hi) {
+              ++d[lo];
+              --d[hi];
+            }
+          }
+        }
+      });
+    }
+  }
+  // noise with the count-dependent variance (worldgen.hpp:46-51)
+  void signals(uint64_t seed, void* out, int dtype) {
+    par(g.S, [&](int64_t j0, int64_t j1) {
+      for (int64_t j = j0; j < j1; ++j) {
+        const int32_t* d = diff.data() + static_cast<size_t>(j) * (g.n + 1);
+        Rng r = Rng::derive(seed, 4, static_cast<uint64_t>(j));
+        int32_t cnt = 0;
+        for (int64_t s2 = 0; s2 < g.n; ++s2) {
+          cnt += d[s2];
+          const double var = g.c->var_noise + cnt * g.c->var_event;
+          const double y = r.normal(0.0, std::sqrt(var));
+          if (dtype == SEIS_F64)
+            static_cast<double*>(out)[j * g.n + s2] = y;
+          else
+            static_cast<float*>(out)[j * g.n + s2] = static_cast<float>(y);
+        }
+      }
+    });
+  }
+};
+
 int guard(int code, const std::string& m) {
   g_werr = m;
   return code;
@@ -190,6 +258,70 @@ int seis_world_with_events(const seis_model_cfg* cfg, const double* stations, in
       });
     for (auto& th : pool) th.join();
     g.signals(seed, N, arrivals, signals, dtype, threads);
+    return SEIS_OK;
+  } catch (const std::exception& e) {
+    return guard(SEIS_ERUNTIME, e.what());
+  }
+}
+
+// sample_world (worldgen.hpp:20-53) without the N x S arrival matrix: the
+// events (ids, x, t) and the signals, bit-exact with seis_world_generate;
+// arrivals are regenerated on demand with seis_world_arrivals.
+int seis_world_generate_events(const seis_model_cfg* cfg, const double* stations, int64_t S,
+                               uint64_t seed, int64_t cap, int64_t* n_events, uint64_t* ids,
+                               double* x, double* t, void* signals, int32_t dtype,
+                               int32_t threads) {
+  try {
+    Gen g{cfg, stations, S, static_cast<int64_t>(std::llround(cfg->sample_rate * cfg->T))};
+    Rng count = Rng::derive(seed, 1);
+    const uint64_t N = count.poisson(cfg->lambda_rate * cfg->T);
+    *n_events = static_cast<int64_t>(N);
+    if (static_cast<int64_t>(N) > cap) return guard(SEIS_ERUNTIME, "event capacity too small");
+    for (uint64_t i = 0; i < N; ++i) {
+      Rng cr = Rng::derive(seed, 2, i);
+      ids[i] = i;
+      x[i] = cr.uniform(0.0, cfg->x_max);
+      t[i] = cr.uniform(0.0, cfg->T);
+    }
+    StreamCounts sc(g, threads);
+    sc.add(seed, (int64_t)N, x, t);
+    sc.signals(seed, signals, dtype);
+    return SEIS_OK;
+  } catch (const std::exception& e) {
+    return guard(SEIS_ERUNTIME, e.what());
+  }
+}
+
+// make_world_with_events (worldgen.hpp:57-86) without the arrival matrix.
+int seis_world_with_events_signals(const seis_model_cfg* cfg, const double* stations, int64_t S,
+                                   int64_t N, const double* cx, const double* ct, uint64_t seed,
+                                   void* signals, int32_t dtype, int32_t threads) {
+  try {
+    Gen g{cfg, stations, S, static_cast<int64_t>(std::llround(cfg->sample_rate * cfg->T))};
+    StreamCounts sc(g, threads);
+    sc.add(seed, N, cx, ct);
+    sc.signals(seed, signals, dtype);
+    return SEIS_OK;
+  } catch (const std::exception& e) {
+    return guard(SEIS_ERUNTIME, e.what());
+  }
+}
+
+// Arrivals of events i0 .. i0 + n - 1 of a world (their per-event streams,
+// worldgen.hpp:34-38): rows [n][S]; x, t hold those n events' coordinates.
+int seis_world_arrivals(const seis_model_cfg* cfg, const double* stations, int64_t S,
+                        uint64_t seed, int64_t i0, int64_t n, const double* x, const double* t,
+                        double* arrivals, int32_t threads) {
+  try {
+    Gen g{cfg, stations, S, static_cast<int64_t>(std::llround(cfg->sample_rate * cfg->T))};
+    const int64_t T = std::max<int64_t>(1, std::min<int64_t>(threads, std::max<int64_t>(n, 1)));
+    std::vector<std::thread> pool;
+    for (int64_t k = 0; k < T; ++k)
+      pool.emplace_back([&, k] {
+        for (int64_t i = n * k / T; i < n * (k + 1) / T; ++i)
+          g.arrivals(seed, (uint64_t)(i0 + i), x[i], t[i], arrivals + i * S);
+      });
+    for (auto& th : pool) th.join();
     return SEIS_OK;
   } catch (const std::exception& e) {
     return guard(SEIS_ERUNTIME, e.what());

@@ -78,7 +78,9 @@ EXPORTS = ("seis_last_error", "seis_engine_create", "seis_engine_destroy", "seis
            "seis_world_last_error", "seis_world_generate", "seis_world_with_events",
            "seis_thomas_events", "seis_set_snapshot_capacity", "seis_get_snapshots",
            "seis_run_naive", "seis_run_serial", "seis_engine_pool_slots", "seis_eval_last_error",
-           "seis_match_events", "seis_bootstrap_ci", "seis_get_phases", "seis_get_row_wall")
+           "seis_match_events", "seis_bootstrap_ci", "seis_get_phases", "seis_get_row_wall",
+           "seis_set_hypothesis_begin", "seis_set_hypothesis_rows", "seis_set_hypothesis_end",
+           "seis_world_generate_events", "seis_world_with_events_signals", "seis_world_arrivals")
 
 _LIB = None
 
@@ -120,6 +122,12 @@ def load_library(path: str | None = None) -> C.CDLL:
     L.seis_set_snapshot_capacity.argtypes = [P, i64, i64]
     L.seis_get_snapshots.argtypes = [P, i64, P, P, P, i64, P, P, P]
     L.seis_get_phases.argtypes = [P, i64, P, P]
+    L.seis_set_hypothesis_begin.argtypes = [P, i64, P, P, P]
+    L.seis_set_hypothesis_rows.argtypes = [P, i64, i64, P]
+    L.seis_set_hypothesis_end.argtypes = [P]
+    L.seis_world_generate_events.argtypes = [P, P, i64, u64, i64, P, P, P, P, P, i32, i32]
+    L.seis_world_with_events_signals.argtypes = [P, P, i64, i64, P, P, u64, P, i32, i32]
+    L.seis_world_arrivals.argtypes = [P, P, i64, u64, i64, i64, P, P, P, i32]
     L.seis_get_row_wall.argtypes = [P, i64, P, P]
     if path == _build.LIB:
         _LIB = L
@@ -353,6 +361,70 @@ def make_world_with_events(config: ModelConfig, cx, ct, seed: int, dtype=F64, th
     return Events(np.arange(N, dtype=np.uint64), cx.copy(), ct.copy(), arr[:N].copy()), sig
 
 
+def sample_world_events(config: ModelConfig, seed: int, dtype=F64, threads: int = 0,
+                        cap: int = 1 << 22):
+    """sample_world (worldgen.hpp:20-53) streamed: the events without their
+    N x S arrivals (Events.arrivals is None) and the signals, identical to
+    sample_world's; arrivals on demand with world_arrivals."""
+    L = load_library()
+    threads = threads or os.cpu_count() or 1
+    S, n = config.n_stations(), config.n_samples()
+    lam = config.lambda_rate * config.T
+    cap = int(min(cap, lam + 20 * np.sqrt(lam) + 64))
+    st = np.ascontiguousarray(config.stations, np.float64)
+    ids = np.zeros(cap, np.uint64)
+    x = np.zeros(cap)
+    t = np.zeros(cap)
+    sig = np.zeros((S, n), np.float64 if dtype == F64 else np.float32)
+    N = i64(0)
+    m = config._c()
+    rc = L.seis_world_generate_events(C.byref(m), _p(st), S, seed, cap, C.byref(N), _p(ids),
+                                      _p(x), _p(t), _p(sig), dtype, threads)
+    if rc:
+        raise RuntimeError(L.seis_world_last_error().decode())
+    k = N.value
+    return Events(ids[:k].copy(), x[:k].copy(), t[:k].copy(), None), sig
+
+
+def make_world_with_events_signals(config: ModelConfig, cx, ct, seed: int, dtype=F64,
+                                   threads: int = 0):
+    """make_world_with_events (worldgen.hpp:57-86) streamed (arrivals None)."""
+    L = load_library()
+    threads = threads or os.cpu_count() or 1
+    S, n = config.n_stations(), config.n_samples()
+    cx = np.ascontiguousarray(cx, np.float64)
+    ct = np.ascontiguousarray(ct, np.float64)
+    st = np.ascontiguousarray(config.stations, np.float64)
+    sig = np.zeros((S, n), np.float64 if dtype == F64 else np.float32)
+    m = config._c()
+    rc = L.seis_world_with_events_signals(C.byref(m), _p(st), S, len(cx), _p(cx), _p(ct), seed,
+                                          _p(sig), dtype, threads)
+    if rc:
+        raise RuntimeError(L.seis_world_last_error().decode())
+    return Events(np.arange(len(cx), dtype=np.uint64), cx.copy(), ct.copy(), None), sig
+
+
+def world_arrivals(config: ModelConfig, seed: int, i0: int, x, t, threads: int = 0,
+                   out: np.ndarray | None = None) -> np.ndarray:
+    """Arrivals [n][S] of events i0 .. i0 + n - 1 of a generated world (their
+    per-event streams, worldgen.hpp:34-38), x / t those events' coordinates."""
+    L = load_library()
+    threads = threads or os.cpu_count() or 1
+    S = config.n_stations()
+    x = np.ascontiguousarray(x, np.float64)
+    t = np.ascontiguousarray(t, np.float64)
+    n = len(x)
+    if out is None:
+        out = np.zeros((n, S))
+    st = np.ascontiguousarray(config.stations, np.float64)
+    m = config._c()
+    rc = L.seis_world_arrivals(C.byref(m), _p(st), S, seed, i0, n, _p(x), _p(t), _p(out),
+                               threads)
+    if rc:
+        raise RuntimeError(L.seis_world_last_error().decode())
+    return out
+
+
 # ------------------------------------------------------------ world files
 # "seis world v1": a binary world (model, events with arrivals, signals) in
 # place of the reference's CSV files (worldgen.hpp:157-161; 268 M rows at
@@ -565,6 +637,23 @@ class Engine:
         a = np.ascontiguousarray(ev.arrivals, np.float64).reshape(len(ids), S)
         _check(self.L.seis_set_hypothesis(self.h, len(ids), _p(ids), _p(x), _p(t), _p(a)),
                self.L)
+
+    def set_hypothesis_streamed(self, ids, x, t, rows, chunk: int = 1024):
+        """Load a hypothesis whose arrivals come in pieces: rows(i0, n) returns
+        the [n][S] arrival rows of input events i0 .. i0 + n - 1
+        (seis_set_hypothesis_begin / _rows / _end)."""
+        ids = np.ascontiguousarray(ids, np.uint64)
+        x = np.ascontiguousarray(x, np.float64)
+        t = np.ascontiguousarray(t, np.float64)
+        N = len(ids)
+        _check(self.L.seis_set_hypothesis_begin(self.h, N, _p(ids), _p(x), _p(t)), self.L)
+        try:
+            for i0 in range(0, N, chunk):
+                n = min(chunk, N - i0)
+                a = np.ascontiguousarray(rows(i0, n), np.float64)
+                _check(self.L.seis_set_hypothesis_rows(self.h, i0, n, _p(a)), self.L)
+        finally:
+            _check(self.L.seis_set_hypothesis_end(self.h), self.L)
 
     def get_hypothesis(self, arrivals: bool = True, out: Events | None = None) -> Events:
         """The resident hypothesis (id order). `out`: caller-owned buffers (for

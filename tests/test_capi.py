@@ -153,3 +153,30 @@ def test_cpp_binding_compiles_against_reference_headers(built):
         pytest.skip("GPU present: covered by test_gpu_baseline_parity")
     r = subprocess.run([exe, "cpu"], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0 and "OK cpu" in r.stdout, r.stdout + r.stderr
+
+
+def test_streaming_worldgen_bit_exact(built):
+    """f3: the streamed generator (no N x S arrival matrix) gives the same
+    events and signals as sample_world / make_world_with_events, and
+    world_arrivals regenerates any event range's arrivals bit-exactly"""
+    import paper_1612_00595_b200 as E
+    from oracle.oracle import stations_line
+    m = E.ModelConfig(lambda_rate=60 / 600.0, T=600.0, x_max=400.0, v=8.0,
+                      stations=stations_line(40, 400.0))
+    for dt in (E.F64, E.F32):
+        ev, sig = E.sample_world(m, 7, dtype=dt, threads=3)
+        ev2, sig2 = E.sample_world_events(m, 7, dtype=dt, threads=5)
+        assert ev2.arrivals is None and np.array_equal(ev.ids, ev2.ids)
+        assert np.array_equal(ev.x, ev2.x) and np.array_equal(ev.t, ev2.t)
+        assert np.array_equal(sig, sig2)
+        rows = E.world_arrivals(m, 7, 10, ev.x[10:25], ev.t[10:25], threads=2)
+        assert np.array_equal(rows, ev.arrivals[10:25])
+    cx, ct = [20.0, 380.0, 200.0, 5.0], [30.0, 100.0, 590.0, 300.0]
+    ev, sig = E.make_world_with_events(m, cx, ct, 9)
+    ev2, sig2 = E.make_world_with_events_signals(m, cx, ct, 9, threads=3)
+    assert np.array_equal(sig, sig2)
+    assert np.array_equal(E.world_arrivals(m, 9, 0, cx, ct), ev.arrivals)
+    # the reference's own generator on the default world (golden vectors)
+    g = golden_world("w2", default_model())
+    ev3, sig3 = E.sample_world_events(engine_model(default_model()), 2, threads=2)
+    assert np.array_equal(sig3, g.signals)
