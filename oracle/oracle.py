@@ -211,7 +211,7 @@ class Oracle:
         self._naive.argtypes = [P, P, P, i64, i64]
         self._serial = g("run_serial")
         self._serial.restype = P
-        self._serial.argtypes = [P, P, P, i64, i64]
+        self._serial.argtypes = [P, P, P, i64, P, P, P, P, i64, i64]
         for n in ("run_status",):
             getattr(L, pre + n).argtypes = [P]
         g("run_counts").argtypes = [P] + [P] * 6
@@ -355,7 +355,8 @@ class Oracle:
         if naive:
             h = self._naive(C.byref(m), _p(sig), C.byref(s), int(tape), int(rowlj))
         elif serial:
-            h = self._serial(C.byref(m), _p(sig), C.byref(s), int(tape), int(rowlj))
+            h = self._serial(C.byref(m), _p(sig), C.byref(s), init.N, _p(ids), _p(x), _p(t),
+                             _p(arr), int(tape), int(rowlj))
         else:
             h = self._run(C.byref(m), _p(sig), C.byref(s), init.N, _p(ids), _p(x), _p(t),
                           _p(arr), int(tape), int(rowlj))

@@ -568,7 +568,8 @@ sr_run* sr_run_naive(const so_model* mm, const double* signals, const so_sampler
 // run_serial (samplers.hpp:282-315) with every step taped (mh_step without a
 // constraint, proposals.hpp:265-293).
 sr_run* sr_run_serial(const so_model* mm, const double* signals, const so_sampler* s,
-                      int64_t want_tape, int64_t want_rowlj) {
+                      int64_t n_init, const uint64_t* ids, const double* x, const double* t,
+                      const double* arr, int64_t want_tape, int64_t want_rowlj) {
   auto* run = new sr_run;
   run->status = guarded([&] {
     if (s->rng_mode != 0) throw std::invalid_argument("reference supports rng_mode 0 only");
@@ -579,15 +580,19 @@ sr_run* sr_run_serial(const so_model* mm, const double* signals, const so_sample
     sc.validate();
     run->S = config.n_stations();
     const ObservedSignals sig = to_signals(config, signals);
-    World world{config, {}, sig};
+    // the reference starts empty (samplers.hpp:291); an initial hypothesis
+    // (the engine's resident one) starts in id order, births numbered above it
+    World world{config, to_events(run->S, n_init, ids, x, t, arr), sig};
+    detail::sort_by_id(world.events);
     const TimeRegion region = config.full_region();
     const ScoreOptions opts = default_score_options(config);
     const std::int64_t total = sc.epochs * sc.steps_per_epoch;
     Rng rng = derive_stream(sc.seed, streams::kChain, 0, 0, 0);
     run->row_step.push_back(0);
     run->row_lj.push_back(want_rowlj ? log_joint(world) : 0.0);
-    run->row_count.push_back(0);
+    run->row_count.push_back(static_cast<int64_t>(world.events.size()));
     std::uint64_t id_base = 0;
+    for (const Event& e : world.events) id_base = std::max(id_base, e.id + 1);
     std::int64_t done = 0;
     while (done < total) {
       const std::int64_t chunk = std::min(sc.record_every, total - done);

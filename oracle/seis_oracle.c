@@ -1387,7 +1387,8 @@ int so_match_events(int64_t nt, const uint64_t* tid, const double* tx, const dou
  * record_every steps. The final list is returned sorted by id (the engine's
  * order; the reference keeps list order, a permutation of it). */
 so_run* so_run_serial(const so_model* m, const double* signals, const so_sampler* sc,
-                      int64_t want_tape, int64_t want_rowlj) {
+                      int64_t n_init, const uint64_t* ids, const double* x, const double* t,
+                      const double* arr, int64_t want_tape, int64_t want_rowlj) {
   struct so_run* run = (struct so_run*)calloc(1, sizeof(struct so_run));
   const int64_t S = m->n_stations;
   run->S = S;
@@ -1418,11 +1419,27 @@ so_run* so_run_serial(const so_model* m, const double* signals, const so_sampler
   const int64_t total = sc->epochs * sc->steps_per_epoch;
   flat_t flat = {0, 0, 0, 0, 0};
   int64_t* idxbuf = (int64_t*)malloc(sizeof(int64_t) * (size_t)(total + 16));
+  /* the reference starts empty (samplers.hpp:291); an initial hypothesis (the
+   * engine's resident one) starts in id order, births numbered above it */
   evlist_t local = {0, 0, 0};
   uint64_t id_base = 0;
+  for (int64_t i = 0; i < n_init; ++i) {
+    ev_t e;
+    e.id = ids[i];
+    e.x = x[i];
+    e.t = t[i];
+    e.a = (double*)malloc(sizeof(double) * (size_t)S);
+    memcpy(e.a, arr + i * S, sizeof(double) * (size_t)S);
+    evl_push(&local, e);
+    if (ids[i] + 1 > id_base) id_base = ids[i] + 1;
+  }
+  if (local.n) qsort(local.e, (size_t)local.n, sizeof(ev_t), cmp_id);
   int64_t done = 0;
-  run_push_row(run, 0, 0.0, 0); /* log_joint(empty world) */
-  if (want_rowlj) run->row_lj[0] = so_log_joint(m, signals, 0, NULL, NULL, NULL, NULL);
+  run_push_row(run, 0, 0.0, local.n);
+  if (want_rowlj) {
+    flat_fill(&flat, &local, S);
+    run->row_lj[0] = so_log_joint(m, signals, local.n, flat.ids, flat.x, flat.t, flat.arr);
+  }
   while (done < total) {
     const int64_t chunk = sc->record_every < total - done ? sc->record_every : total - done;
     c.step_base = (uint32_t)done;

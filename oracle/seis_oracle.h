@@ -109,7 +109,8 @@ so_run* so_run_chromatic(const so_model* m, const double* signals, const so_samp
                          int64_t n_init, const uint64_t* ids, const double* x, const double* t,
                          const double* arr, int64_t want_tape, int64_t want_rowlj);
 so_run* so_run_serial(const so_model* m, const double* signals, const so_sampler* sc,
-                      int64_t want_tape, int64_t want_rowlj);
+                      int64_t n_init, const uint64_t* ids, const double* x, const double* t,
+                      const double* arr, int64_t want_tape, int64_t want_rowlj);
 so_run* so_run_naive(const so_model* m, const double* signals, const so_sampler* sc,
                      int64_t want_tape, int64_t want_rowlj);
 int so_run_status(const so_run* r);

@@ -414,16 +414,20 @@ __device__ void gen_proposal(const Dev& d, const Samp& sp, const PhaseArgs& pa, 
   }
 }
 
-template <typename YT, int MODE, int NTT, int MINB>
+template <typename YT, int MODE, int NTT, int MINB, int CAP>
 __global__ void __launch_bounds__(NTT, MINB)
     k_phase(const Dev d, const Samp sp, const PhaseArgs pa, Ctl* ctl, int stamp) {
   constexpr int NWT = NTT / 32;
   static_assert(NTT == NT, "diff_cache_overflow() places the cache for NT threads");
+  constexpr bool kBig = CAP > MAXOWN;  // run_serial's whole-world chain
   __shared__ double2 Ts[kTsSize];  // {dL, dI} per (dc, count) + a zero entry
-  __shared__ OwnEv own[MAXOWN];
-  __shared__ StartEv st[MAXOWN];
-  __shared__ int pold[MAXDIFF], pnew[MAXDIFF];
-  __shared__ int lfree[MAXOWN];
+  // the chain's arrays: static for a region chain, dynamic (after the
+  // partial sums, in place of the diff-window cache) for the serial chain
+  __shared__ OwnEv own_s[kBig ? 1 : CAP];
+  __shared__ StartEv st_s[kBig ? 1 : CAP];
+  __shared__ int pold_s[kBig ? 1 : 2 * CAP], pnew_s[kBig ? 1 : 2 * CAP];
+  __shared__ int lfree_s[kBig ? 1 : CAP], cur_of_s[kBig ? 1 : CAP];
+  __shared__ double s_logi_k_s[kBig ? 1 : CAP + 2];  // log(i), i <= CAP + 1 (proposal terms)
   __shared__ Prop prop[2][MSPEC];
   __shared__ double red_sig[NWT][MSPEC], red_arr[NWT][MSPEC];
 
@@ -433,7 +437,6 @@ __global__ void __launch_bounds__(NTT, MINB)
   __shared__ int s_specok;  // this round's proposals were generated during the last decision
   __shared__ unsigned long long s_births;
   __shared__ double s_delta[MSPEC], s_logr[MSPEC], s_prior[2];
-  __shared__ double s_logi_k[MAXOWN + 2];   // log(i), i <= MAXOWN + 1 (proposal terms)
   // dynamic: [LOGIWIN] log(i), i in [N - LOGIWIN/2, N + LOGIWIN/2), then the
   // per-lane partial sums of the tile-major pass
   extern __shared__ double s_logi_n[];
@@ -442,6 +445,17 @@ __global__ void __launch_bounds__(NTT, MINB)
   int(*acc_cnt)[NTT] = reinterpret_cast<int(*)[NTT]>(s_logi_n + LOGIWIN + 2 * MSPEC * NTT);
   DiffS* dcache =
       reinterpret_cast<DiffS*>(s_logi_n + LOGIWIN + 2 * MSPEC * NTT + MSPEC * NTT / 2);
+  // serial layout in dynamic smem: own | st | log i | pold | pnew | lfree | cur_of
+  char* const big = reinterpret_cast<char*>(dcache);
+  constexpr size_t kOffSt = CAP * sizeof(OwnEv), kOffLogi = kOffSt + CAP * sizeof(StartEv);
+  constexpr size_t kOffPold = kOffLogi + (CAP + 8) * sizeof(double);
+  OwnEv* const own = kBig ? reinterpret_cast<OwnEv*>(big) : own_s;
+  StartEv* const st = kBig ? reinterpret_cast<StartEv*>(big + kOffSt) : st_s;
+  double* const s_logi_k = kBig ? reinterpret_cast<double*>(big + kOffLogi) : s_logi_k_s;
+  int* const pold = kBig ? reinterpret_cast<int*>(big + kOffPold) : pold_s;
+  int* const pnew = kBig ? pold + 2 * CAP : pnew_s;
+  int* const lfree = kBig ? pold + 4 * CAP : lfree_s;
+  int* const cur_of = kBig ? pold + 5 * CAP : cur_of_s;
   __shared__ int s_accg[MSPEC], s_cnt[MSPEC];
   __shared__ long long s_nlocal;
 
@@ -467,7 +481,7 @@ __global__ void __launch_bounds__(NTT, MINB)
 
   fill_ts(Ts, d, tid, NTT);
   const int logi_base = N - LOGIWIN / 2;
-  for (int i = tid; i < MAXOWN + 2; i += NTT) s_logi_k[i] = i < d.logi_n ? d.logi[i] : 0.0;
+  for (int i = tid; i < CAP + 2; i += NTT) s_logi_k[i] = i < d.logi_n ? d.logi[i] : 0.0;
   for (int i = tid; i < LOGIWIN; i += NTT) {
     const int g = logi_base + i;
     s_logi_n[i] = (g >= 0 && g < d.logi_n) ? d.logi[g] : 0.0;
@@ -504,7 +518,7 @@ __global__ void __launch_bounds__(NTT, MINB)
     __syncthreads();
     if (inr) {
       const int pos = s_w[warp] + __popc(bal & ((1u << lane) - 1u));
-      if (pos < MAXOWN) {
+      if (pos < CAP) {
         own[pos].id = pa.tab.id[i];
         own[pos].x = pa.tab.x[i];
         own[pos].t = pa.tab.t[i];
@@ -520,7 +534,7 @@ __global__ void __launch_bounds__(NTT, MINB)
     if (tid == 0) s_nown = s_tmp;
     __syncthreads();
   }
-  if (s_nown > MAXOWN) {
+  if (s_nown > CAP) {
     if (tid == 0) set_err(ctl, ERR_OWN_OVERFLOW);
     return;
   }
@@ -607,7 +621,8 @@ __global__ void __launch_bounds__(NTT, MINB)
     }
     // the round's diff windows per station (proposal-major pass): rebuilt only
     // after an accept changed the region's diff, alongside generation
-    const bool use_dcache = (d.S_pad + 31) / 32 < 4 * NWT && d.S_pad <= kDiffCache && d.n < 65535;
+    const bool use_dcache =
+        !kBig && (d.S_pad + 31) / 32 < 4 * NWT && d.S_pad <= kDiffCache && d.n < 65535;
     const bool dc_build = use_dcache && s_np > 0 && s_dc_dirty;
     if (warp < m && lane == 0 && !(MODE == 0 && s_specok)) {  // one lane per warp: move types do not diverge
       const int step = i0 + warp;
@@ -918,7 +933,7 @@ __global__ void __launch_bounds__(NTT, MINB)
             }
           }
         }
-        if (ok && P.na >= 1 && nown - P.nr + P.na > MAXOWN) {
+        if (ok && P.na >= 1 && nown - P.nr + P.na > CAP) {
           set_err(ctl, ERR_OWN_OVERFLOW);
           ok = false;
         }
@@ -940,7 +955,11 @@ __global__ void __launch_bounds__(NTT, MINB)
         }
         // apply_change (density.hpp:171-180): erase by id, push_back added
         unsigned long long rid[2];
-        for (int r = 0; r < P.nr; ++r) rid[r] = own[P.rown[r]].id;
+        int rsrc[2] = {-1, -1};
+        for (int r = 0; r < P.nr; ++r) {
+          rid[r] = own[P.rown[r]].id;
+          if constexpr (kBig) rsrc[r] = own_src(own[P.rown[r]].sidx);
+        }
         for (int r = 0; r < P.nr; ++r) {
           int i = 0;
           while (i < nown && own[i].id != rid[r]) ++i;
@@ -953,21 +972,32 @@ __global__ void __launch_bounds__(NTT, MINB)
           e.x = P.ax[a];
           e.t = P.at[a];
           e.slot = P.dslot[a];
-          e.sidx = -1;
+          // serial chain: a modified start event keeps its start index, encoded
+          e.sidx = (!kBig || P.type == 0 || rsrc[a] < 0) ? -1 : -rsrc[a] - 2;
           own[nown++] = e;
         }
         n_local += P.na - P.nr;
         // own diff vs the phase-start snapshot (frozen-snapshot view) as
-        // (start version, current version) pairs
+        // (start version, current version) pairs, in start order, then the
+        // births; O(nstart + nown) through each event's start index
         np = 0;
+        if constexpr (kBig) {
+          for (int i = 0; i < nstart; ++i) cur_of[i] = -1;
+          for (int j = 0; j < nown; ++j)
+            if (own_src(own[j].sidx) >= 0) cur_of[own_src(own[j].sidx)] = j;
+        }
         for (int i = 0; i < nstart; ++i)
           if (!st[i].current) {
             int f = -1;
-            for (int j = 0; j < nown; ++j)
-              if (own[j].id == st[i].id) {
-                f = j;
-                break;
-              }
+            if constexpr (kBig) {
+              f = cur_of[i];
+            } else {  // a region chain holds few events: search by id
+              for (int j = 0; j < nown; ++j)
+                if (own[j].id == st[i].id) {
+                  f = j;
+                  break;
+                }
+            }
             pold[np] = st[i].slot;
             pnew[np++] = f >= 0 ? own[f].slot : -1;
           }
@@ -1066,15 +1096,24 @@ __global__ void __launch_bounds__(NTT, MINB)
   // ---- phase outputs (the barrier merge, samplers.hpp:459-462,471-482)
   if (tid == 0) {
     // fates of the phase-start versions
+    if constexpr (kBig) {
+      for (int i = 0; i < nstart; ++i) cur_of[i] = -1;
+      for (int j = 0; j < nown; ++j)
+        if (own_src(own[j].sidx) >= 0) cur_of[own_src(own[j].sidx)] = j;
+    }
     for (int i = 0; i < nstart; ++i) {
       const int tab = st[i].tab;
       pa.fate_stamp[tab] = stamp;
       int f = -1;
-      for (int j = 0; j < nown; ++j)
-        if (own[j].id == st[i].id) {
-          f = j;
-          break;
-        }
+      if constexpr (kBig) {
+        f = cur_of[i];
+      } else {
+        for (int j = 0; j < nown; ++j)
+          if (own[j].id == st[i].id) {
+            f = j;
+            break;
+          }
+      }
       pa.fate_alive[tab] = f >= 0;
       if (f >= 0) {
         pa.fate_x[tab] = own[f].x;
@@ -1083,7 +1122,7 @@ __global__ void __launch_bounds__(NTT, MINB)
       }
     }
     // births alive at phase end, sorted by id
-    OutEv* bo = pa.births + (size_t)slot_idx * MAXOWN;
+    OutEv* bo = pa.births + (size_t)slot_idx * CAP;  // (serial: one slot)
     int nb = 0;
     for (int j = 0; j < nown; ++j)
       if (own[j].id >= pa.next_base) {
@@ -1109,7 +1148,7 @@ __global__ void __launch_bounds__(NTT, MINB)
     // coverage diff for the commit, then this-phase versions that died (sign
     // 0): k_commit returns those slots to the pool, after every CTA of this
     // phase has stopped popping from it
-    DiffPair* dout = pa.diff + (size_t)slot_idx * MAXDOUT;
+    DiffPair* dout = pa.diff + (size_t)slot_idx * (3 * CAP);  // (serial: one slot)
     for (int q = 0; q < np; ++q) {
       dout[q].old_slot = pold[q];
       dout[q].new_slot = pnew[q];
@@ -1577,6 +1616,8 @@ thread_local std::string g_err;
 constexpr int kPhaseSmemTile = LOGIWIN * (int)sizeof(double) + MSPEC * NT * (2 * 8 + 4);
 // + the per-round diff-window cache of the proposal-major pass (few stations)
 constexpr int kPhaseSmem = kPhaseSmemTile + kDiffCache * (int)(sizeof(DiffS) + sizeof(DiffS4x));
+// run_serial's chain: + its arrays in place of the diff-window cache (unused)
+constexpr int kPhaseSmemSerial = kPhaseSmemTile + ChainSmem<kSerialCap>::bytes;
 // The tile-major pass (S_pad >= 2048: 64 station tiles and more) never builds
 // the diff-window cache, so its launches leave that shared memory to L1: the
 // band rows a warp's proposals share on a tile stay resident between them.
@@ -1796,7 +1837,7 @@ Ctl read_ctl(seis_engine* e) {
 
 const char* err_name(int e) {
   switch (e) {
-    case ERR_OWN_OVERFLOW: return "a region exceeded the per-region event limit (64)";
+    case ERR_OWN_OVERFLOW: return "a region exceeded the per-region event limit (64; run_serial: 1024)";
     case ERR_POOL_EXHAUSTED: return "arrival pool exhausted (live events + replaced versions > pool slots): raise event_capacity";
     case ERR_TAPE_UNKNOWN_ID: return "replay tape names an event the region does not hold";
     case ERR_TABLE_OVERFLOW: return "event table overflow: raise event_capacity";
@@ -1829,8 +1870,12 @@ namespace {
 // config[2]): a chain's rounds slow down more than sharing an SM gains.
 template <typename YT, int MODE>
 void launch_phase_t(seis_engine* e, int ncr, const Samp& sp, const PhaseArgs& pa, int stamp) {
-  k_phase<YT, MODE, NT, SEIS_MINB><<<ncr, NT, phase_smem(e->d), e->stream>>>(e->d, sp, pa, e->ctl,
-                                                                            stamp);
+  if (pa.serial)
+    k_phase<YT, MODE, NT, SEIS_MINB, kSerialCap><<<ncr, NT, kPhaseSmemSerial, e->stream>>>(
+        e->d, sp, pa, e->ctl, stamp);
+  else
+    k_phase<YT, MODE, NT, SEIS_MINB, MAXOWN><<<ncr, NT, phase_smem(e->d), e->stream>>>(
+        e->d, sp, pa, e->ctl, stamp);
 }
 
 void launch_phase(seis_engine* e, int mode, int ncr, const Samp& sp, const PhaseArgs& pa,
@@ -1850,8 +1895,11 @@ void launch_phase(seis_engine* e, int mode, int ncr, const Samp& sp, const Phase
 
 template <typename YT, int MODE>
 void set_phase_attrs() {
-  ck(cudaFuncSetAttribute(k_phase<YT, MODE, NT, SEIS_MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          kPhaseSmem),
+  ck(cudaFuncSetAttribute(k_phase<YT, MODE, NT, SEIS_MINB, MAXOWN>,
+                          cudaFuncAttributeMaxDynamicSharedMemorySize, kPhaseSmem),
+     "smem attribute");
+  ck(cudaFuncSetAttribute(k_phase<YT, MODE, NT, SEIS_MINB, kSerialCap>,
+                          cudaFuncAttributeMaxDynamicSharedMemorySize, kPhaseSmemSerial),
      "smem attribute");
 }
 }  // namespace
@@ -1917,7 +1965,7 @@ int seis_engine_create(const seis_model_cfg* cfg, const double* stations, int64_
     }
     // per-count terms with glibc log, exactly as density.hpp:288-297; counts
     // are uint16 (<= 65535) plus at most 2 * MAXOWN in-phase own versions
-    const int tab_n = std::min(e->cap, 65535) + 2 * MAXOWN + 8;
+    const int tab_n = std::min(e->cap, 65535) + 2 * kSerialCap + 8;
     std::vector<double> L(tab_n), I(tab_n);
     for (int c = 0; c < tab_n; ++c) {
       const double var = cfg->var_noise + c * cfg->var_event;
@@ -1940,7 +1988,7 @@ int seis_engine_create(const seis_model_cfg* cfg, const double* stations, int64_
     ck(cudaMemcpy(e->Lg, L.data(), tab_n * 8, cudaMemcpyHostToDevice), "H2D");
     ck(cudaMemcpy(e->Ig, I.data(), tab_n * 8, cudaMemcpyHostToDevice), "H2D");
     // log i and log i! for event counts: the live events plus a region's births
-    const int logi_n = e->cap + 2 * MAXOWN + 8;
+    const int logi_n = e->cap + 2 * kSerialCap + 8;
     e->h_logi.resize(logi_n);
     e->h_logfact.resize(logi_n);
     double acc = 0.0;
@@ -2525,13 +2573,17 @@ static int run_driver(seis_engine* e, const seis_sampler_cfg* sc, int32_t mode,
     // serial: the chain's list order between chunks ([0] = count, -1 = none yet)
     unsigned long long* order_io = nullptr;
     if (serial) {
-      order_io = static_cast<unsigned long long*>(alloc((MAXOWN + 1) * 8));
+      order_io = static_cast<unsigned long long*>(alloc((kSerialCap + 1) * 8));
       const unsigned long long none = ~0ull;
       ck(cudaMemcpy(order_io, &none, 8, cudaMemcpyHostToDevice), "H2D");
     }
-    OutEv* births = static_cast<OutEv*>(alloc((size_t)n_slots * MAXOWN * sizeof(OutEv)));
+    // per-slot outputs: MAXOWN births / MAXDOUT diff entries per region; the
+    // serial chain's one slot holds kSerialCap / 3 kSerialCap
+    const int cap_own = serial ? kSerialCap : MAXOWN;
+    OutEv* births = static_cast<OutEv*>(alloc((size_t)n_slots * cap_own * sizeof(OutEv)));
     int* diff_cnt = static_cast<int*>(alloc((size_t)n_slots * 4));
-    DiffPair* diff = static_cast<DiffPair*>(alloc((size_t)n_slots * MAXDOUT * sizeof(DiffPair)));
+    DiffPair* diff =
+        static_cast<DiffPair*>(alloc((size_t)n_slots * 3 * cap_own * sizeof(DiffPair)));
     // cost-ordered dispatch (k_order); SEIS_ORDER=0 disables it (A/B)
     const bool use_order = !serial && !(getenv("SEIS_ORDER") && atoi(getenv("SEIS_ORDER")) == 0);
     int* order_cnt = static_cast<int*>(alloc((size_t)n_slots * 4));

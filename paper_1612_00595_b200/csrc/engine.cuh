@@ -44,6 +44,14 @@ constexpr int MAXOWN = 64;       // events a region may hold during a phase
 constexpr int kMaxEvents = 1 << 22;  // event_capacity bound (table sizes; counts stay uint16)
 constexpr int MAXDIFF = 2 * MAXOWN;  // diff pairs a region may hold
 constexpr int MAXDOUT = 3 * MAXOWN;  // diff pairs + recycled slots per region
+// run_serial's one chain holds every event of the world: its k_phase variant
+// keeps up to kSerialCap events (and 2 / 3 x that in diff pairs / outputs) in
+// dynamic shared memory instead of the static MAXOWN arrays
+constexpr int kSerialCap = 1024;
+template <int CAP>
+struct ChainSmem {  // bytes of the chain arrays (own, st, pold, pnew, lfree, cur_of, log i)
+  static constexpr int bytes = CAP * (32 + 24 + 4 + 4) + 2 * CAP * 8 + (CAP + 8) * 8;
+};
 constexpr int TBL = 512;         // coverage counts whose {dL, dI} rows live in smem
 constexpr int kDiffCache = 2048;  // stations whose round diff windows k_phase caches in smem
 constexpr int kRowPad = 32;      // zero rows appended to y and cov (unpredicated chunk loads)

@@ -47,11 +47,15 @@ struct Prop {
   int dslot[2], inplace[2];
 };
 
+// sidx: the event's phase-start index i while its start version is current;
+// -(i + 2) once a move replaced that version (the event keeps its start
+// index); -1 for an event born this phase. sidx < 0 <=> a this-phase version.
 struct OwnEv {
   unsigned long long id;
   double x, t;
   int slot, sidx;
 };
+__device__ __forceinline__ int own_src(int sidx) { return sidx >= 0 ? sidx : -sidx - 2; }
 
 struct StartEv {
   unsigned long long id;

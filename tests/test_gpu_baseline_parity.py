@@ -393,3 +393,140 @@ def test_cpp_binding_run_sampler_on_gpu(E):
     r = subprocess.run([exe, "gpu"], capture_output=True, text=True, timeout=600)
     print(r.stdout)
     assert r.returncode == 0 and "OK gpu" in r.stdout, r.stdout + r.stderr
+
+
+# ------------------------------------------------------------------ run_serial at scale
+def _serial_world(oc, n_events=420, S=16, T=4000.0, seed=12):
+    m = O.Model(lambda_rate=n_events / T, T=T, x_max=100.0, v=2.0,
+                stations=O.stations_line(S, 100.0))
+    w = oc.sample_world(m, seed)
+    assert w.events.N >= 400
+    return m, w
+
+
+def _serial_sampler(E, s, record_log_joint=True):
+    return E.SamplerConfig(algorithm="serial", steps_per_epoch=s.steps_per_epoch,
+                           epochs=s.epochs, n_regions=s.n_regions, seed=s.seed,
+                           burn_in_fraction=s.burn_in_fraction, record_every=s.record_every,
+                           record_log_joint=record_log_joint)
+
+
+def test_serial_production_400_events_matches_oracle(E):
+    """run_serial (samplers.hpp:282-315) with more than 400 events in its one
+    chain (the whole-world chain keeps up to 1024 in dynamic shared memory):
+    every decision, delta, trace row and the final hypothesis against the
+    oracle running the same philox stream"""
+    oc = O.Oracle("c")
+    m, w = _serial_world(oc)
+    s = O.Sampler(steps_per_epoch=400, epochs=3, n_regions=1, seed=5, rng_mode=1,
+                  record_every=300, burn_in_fraction=0.0)
+    ro = oc.run_chromatic(w, s, init=w.events, tape=True, rowlj=True, serial=True)
+    eng = E.Engine(engine_model(m), w.signals, event_capacity=2048)
+    eng.set_hypothesis(_ev(E, w.events))
+    tr = eng.run_chromatic(_serial_sampler(E, s), decisions=len(ro["tape"]))
+    so, t = tr.step_out, ro["tape"]
+    assert np.array_equal(so["accepted"], t["accepted"])
+    sc = (t["scored"] == 1) & np.isfinite(t["delta"])
+    assert np.allclose(so["delta"][sc], t["delta"][sc], rtol=1e-11, atol=1e-9)
+    assert tr.total_accepted == ro["total_accepted"] and tr.total_accepted > 20
+    assert np.array_equal(tr.final.ids, ro["final"].ids)
+    assert np.array_equal(tr.final.arrivals, ro["final"].arr)
+    assert np.array_equal(tr.row_count, ro["row_count"]) and tr.row_count[0] >= 400
+    assert np.allclose(tr.row_log_joint, ro["row_lj"], rtol=1e-12, atol=1e-8)
+
+
+def test_serial_replay_reference_tape_400_events(E, ref):
+    """the reference's own serial chain (composed from its headers, from the
+    same 400+-event hypothesis) replayed: decisions identical except ties,
+    deltas within 1e-9, final hypothesis identical"""
+    m, w = _serial_world(ref)
+    s = O.Sampler(steps_per_epoch=300, epochs=2, n_regions=1, seed=8, record_every=200,
+                  burn_in_fraction=0.0)
+    r = ref.run_chromatic(w, s, init=w.events, tape=True, serial=True)
+    eng = E.Engine(engine_model(m), w.signals, event_capacity=2048)
+    eng.set_hypothesis(_ev(E, w.events))
+    tr = eng.run_chromatic(_serial_sampler(E, s, False), tape=r["tape"],
+                           tape_arrivals=r["tape_arr"])
+    t = r["tape"]
+    drawn = t["u_drawn"] == 1
+    tie = np.zeros(len(t), bool)
+    tie[drawn] = np.abs(t["log_r"][drawn] - np.log(t["u"][drawn])) < TIE
+    assert not ((tr.step_out["accepted"] != t["accepted"]) & ~tie).any()
+    sc = (t["scored"] == 1) & np.isfinite(t["delta"])
+    bad = [i for i in np.where(sc)[0] if not close(tr.step_out["delta"][i], t["delta"][i])]
+    assert not bad, bad[:5]
+    assert np.array_equal(tr.final.ids, r["final"].ids)
+    assert np.array_equal(tr.final.arrivals, r["final"].arr)
+    assert (t["accepted"] == 1).sum() > 20
+
+
+def _c2_epochs(alg, budget, k, n):
+    # experiment.hpp:92-119 sampler_config_for: equal step budgets
+    e = {"serial": budget / k, "naive": budget / (k * n), "chromatic-static": budget / (k * n),
+         "chromatic-dynamic": 1.0 + (budget / k - n) / (n + 1.0)}[alg]
+    return max(1, int(np.floor(e + 0.5)))
+
+
+def _c2(E, m, n_worlds, runs, budget, k, n, record_every, threshold=12.0, wseed0=1):
+    """acceptance.cpp:152-194 (criterion 2) on the engine: worlds from the
+    reference generator (bit-exact), every algorithm from the empty hypothesis
+    with experiment.hpp's step budgets and seeds, final hypotheses matched to
+    the truth, percentile-bootstrap CIs of the means (evaluation.hpp:136-169
+    with experiment.hpp:236-238's seeds)"""
+    oc = O.Oracle("c")
+    algs = ["serial", "naive", "chromatic-static", "chromatic-dynamic"]
+    vals = {a: ([], []) for a in algs}
+    for wi in range(n_worlds):
+        w = oc.sample_world(m, wseed0 + wi)
+        eng = E.Engine(engine_model(m), w.signals, event_capacity=4096)
+        truth = E.Events(w.events.ids, w.events.x, w.events.t, w.events.arr)
+        for r in range(runs):
+            seed = 1000 + wi * runs + r
+            for a in algs:
+                eng.set_hypothesis(E.Events(np.zeros(0, np.uint64), np.zeros(0), np.zeros(0),
+                                            np.zeros((0, m.S))))
+                sc = E.SamplerConfig(algorithm=a, steps_per_epoch=k, n_regions=n, seed=seed,
+                                     epochs=_c2_epochs(a, budget, k, n), burn_in_fraction=0.5,
+                                     record_every=record_every)
+                f = eng.run_chromatic(sc).final
+                rep = E.match_events(truth, f, threshold)
+                vals[a][0].append(rep.precision)
+                vals[a][1].append(rep.recall)
+    ci = {}
+    for ai, a in enumerate(algs):
+        for mi, name in enumerate(["precision", "recall"]):
+            ci[(a, name)] = E.bootstrap_ci(vals[a][mi], 0.95, 2000, wseed0 + 7700 + ai * 16 + mi)
+    return ci
+
+
+def _overlap(x, y):
+    return max(x.lo, y.lo) <= min(x.hi, y.hi)
+
+
+def test_c2_chromatic_dynamic_matches_serial_naive_worse(E):
+    """criterion 2 of the reference's acceptance suite, on the GPU engine:
+    10 worlds x 3 runs x 100 000 steps of the default world; the
+    chromatic-dynamic precision and recall CIs overlap the serial ones, naive
+    parallel is below serial with serial's mean outside naive's CI"""
+    ci = _c2(E, O.Model(), 10, 3, 100000, 500, 4, 5000)
+    sp, sr = ci[("serial", "precision")], ci[("serial", "recall")]
+    dp, dr = ci[("chromatic-dynamic", "precision")], ci[("chromatic-dynamic", "recall")]
+    npr = ci[("naive", "precision")]
+    detail = {k: (round(v.mean, 3), round(v.lo, 3), round(v.hi, 3)) for k, v in ci.items()}
+    assert _overlap(sp, dp) and _overlap(sr, dr), detail
+    assert npr.mean < sp.mean and not (npr.lo <= sp.mean <= npr.hi), detail
+
+
+def test_c2_serial_vs_chromatic_mapped_shape(E):
+    """the same comparison on a BASELINE-mapped shape (S = 96 stations, 32
+    time regions, l / tau = 1.2, ~40 events; serial holds them all in one
+    chain): chromatic-dynamic precision and recall CIs overlap serial's"""
+    S, T, nr, x_max, n_ev = 96, 1200.0, 32, 2000.0, 40.0
+    m = O.Model(lambda_rate=n_ev / T, T=T, x_max=x_max, v=1.2 * x_max * nr / T,
+                stations=O.stations_line(S, x_max))
+    ci = _c2(E, m, 4, 3, 76800, 100, nr, 1 << 30, threshold=240.0, wseed0=500)
+    sp, sr = ci[("serial", "precision")], ci[("serial", "recall")]
+    dp, dr = ci[("chromatic-dynamic", "precision")], ci[("chromatic-dynamic", "recall")]
+    detail = {k: (round(v.mean, 3), round(v.lo, 3), round(v.hi, 3)) for k, v in ci.items()}
+    print(detail)
+    assert _overlap(sp, dp) and _overlap(sr, dr), detail

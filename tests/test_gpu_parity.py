@@ -511,10 +511,10 @@ def test_capacity_and_region_limits_fail_loudly(E, oc):
     eng = E.Engine(engine_model(m), w.signals, event_capacity=2)
     with pytest.raises(RuntimeError):
         eng.run_chromatic(E.SamplerConfig(steps_per_epoch=400, epochs=6, n_regions=4, seed=1))
-    # the serial chain lives in one CTA: more than 64 events is refused
-    many = oc.sample_world(O.Model(lambda_rate=100 / 240.0), 5)
-    assert many.events.N > 64
-    eng2 = E.Engine(engine_model(many.model), many.signals, event_capacity=1024)
+    # the serial chain lives in one CTA: more than 1024 events is refused
+    many = oc.sample_world(O.Model(lambda_rate=1100 / 240.0), 5)
+    assert many.events.N > 1024
+    eng2 = E.Engine(engine_model(many.model), many.signals, event_capacity=2048)
     eng2.set_hypothesis(E.Events(many.events.ids, many.events.x, many.events.t, many.events.arr))
     with pytest.raises(RuntimeError, match="per-region event limit"):
         eng2.run_chromatic(E.SamplerConfig(algorithm="serial", steps_per_epoch=10, epochs=1))
