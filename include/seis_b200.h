@@ -120,6 +120,7 @@ typedef struct {
   int64_t final_events;
   int64_t speculative_discarded;        /* proposals evaluated ahead of an accept, then dropped */
   int64_t phases;                       /* region-sweep kernel launches (color phases) */
+  int64_t generated_versions;           /* live generated versions after the run (spec v2) */
 } seis_run_stats;
 
 /* reference PhaseRecord (samplers.hpp:87-95): one per committed region
@@ -146,6 +147,21 @@ void seis_engine_destroy(seis_engine* eng);
  * what fits in free HBM less 4 GiB), never below event_capacity. A phase needs
  * the live events plus the phase-start versions it replaced. */
 int64_t seis_engine_pool_slots(const seis_engine* eng);
+
+/* Arrival storage of the versions production runs create. SEIS_ARR_ROWS
+ * (philox stream spec v1): every version stores its S fp64 arrivals, exactly
+ * the reference's arithmetic. SEIS_ARR_COMPACT (spec v2, include/seis_philox.h):
+ * a birth's version is its location plus its philox key, arrivals computed as
+ * mean + sigma z; location and joint moves of such a version keep the
+ * residual z exactly, a first arrival move is one per-station override, a
+ * second one stores the row. Memory per version O(1) instead of 8 S bytes
+ * (configs 3 and 4 at their stated k). The default is COMPACT when the
+ * arrival pool cannot hold two stored rows per event of capacity, else ROWS.
+ * Replay mode always stores rows. */
+#define SEIS_ARR_ROWS 0
+#define SEIS_ARR_COMPACT 1
+int seis_set_arrival_storage(seis_engine* eng, int32_t mode);
+int32_t seis_get_arrival_storage(const seis_engine* eng);
 
 /* Replace the signals (same shape/dtype) — one host->device copy. */
 int seis_upload_signals(seis_engine* eng, const void* signals);

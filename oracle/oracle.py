@@ -34,7 +34,7 @@ class SoSampler(C.Structure):
     _fields_ = [("steps_per_epoch", i64), ("epochs", i64), ("n_regions", i64), ("seed", u64),
                 ("burn_in_fraction", f64), ("record_every", i64), ("weights", f64 * 5),
                 ("step_location_x", f64), ("step_location_t", f64), ("step_arrival", f64),
-                ("step_joint", f64), ("rng_mode", i64), ("dynamic", i64)]
+                ("step_joint", f64), ("rng_mode", i64), ("dynamic", i64), ("compact", i64)]
 
 
 TAPE_DTYPE = np.dtype([
@@ -94,12 +94,13 @@ class Sampler:
     step_joint: float = 1.0
     rng_mode: int = 0
     dynamic: int = 0
+    compact: int = 0  # rng_mode 1: generated arrival versions (philox stream spec v2)
 
     def c(self):
         return SoSampler(self.steps_per_epoch, self.epochs, self.n_regions, self.seed,
                          self.burn_in_fraction, self.record_every, (f64 * 5)(*self.weights),
                          self.step_location_x, self.step_location_t, self.step_arrival,
-                         self.step_joint, self.rng_mode, self.dynamic)
+                         self.step_joint, self.rng_mode, self.dynamic, self.compact)
 
 
 @dataclass

@@ -520,10 +520,18 @@ void so_signal_window(double lo, double hi, double tau, double T, double rate, i
 
 /* ------------------------------------------------------------- samplers.hpp */
 
+/* an event version; gen = 1: a generated version of arrival storage spec v2
+ * (include/seis_philox.h): its arrivals are arrival_mean(x, t, j) + sigma z_j
+ * with z_j the philox normal of its birth (key gseed, counter gsweep / gregion
+ * / gstep), plus ovr_d at station ovr_st; `a` always holds those values */
 typedef struct {
   uint64_t id;
   double x, t;
   double* a;
+  int gen, ovr_st;
+  uint64_t gseed;
+  uint32_t gsweep, gregion, gstep, pad_;
+  double ovr_d;
 } ev_t;
 
 typedef struct {
@@ -708,6 +716,16 @@ static ev_t shifted(const so_model* m, const ev_t* before, double nx, double nt)
   ev_t after = ev_copy(before, m->n_stations);
   after.x = nx;
   after.t = nt;
+  if (before->gen) { /* spec v2: the residual sigma z of the birth kept exactly */
+    for (int64_t j = 0; j < m->n_stations; ++j) {
+      after.a[j] = arrival_mean(m, after.x, after.t, j) +
+                   m->sigma_arrival * (double)seis_normal(before->gseed, before->gsweep,
+                                                         before->gregion, before->gstep,
+                                                         (uint32_t)j);
+      if (j == before->ovr_st) after.a[j] = after.a[j] + before->ovr_d;
+    }
+    return after;
+  }
   for (int64_t j = 0; j < m->n_stations; ++j)
     after.a[j] += arrival_mean(m, after.x, after.t, j) - arrival_mean(m, before->x, before->t, j);
   return after;
@@ -732,7 +750,16 @@ static void propose(chain_t* c, int type, const evlist_t* l, uint64_t new_id, in
   switch (type) {
     case 0: { /* birth, proposals.hpp:84-107 */
       ev_t e;
+      memset(&e, 0, sizeof e);
       e.id = new_id;
+      e.ovr_st = -1;
+      if (sc->rng_mode == 1 && sc->compact) { /* spec v2: a generated version */
+        e.gen = 1;
+        e.gseed = sc->seed;
+        e.gsweep = c->sweep;
+        e.gregion = c->region;
+        e.gstep = c->step;
+      }
       if (sc->rng_mode == 0) {
         e.t = so_uniform_range(&c->rng, c->rlo, c->rhi);
         e.x = so_uniform_range(&c->rng, 0.0, m->x_max);
@@ -801,7 +828,16 @@ static void propose(chain_t* c, int type, const evlist_t* l, uint64_t new_id, in
       }
       const ev_t* b = &l->e[idxbuf[pick]];
       ev_t after = ev_copy(b, S);
-      after.a[st] += draw_normal(c, 0, 0.0, sc->step_arrival);
+      const double da = draw_normal(c, 0, 0.0, sc->step_arrival);
+      after.a[st] += da;
+      if (b->gen) { /* spec v2: the first override stays generated, a second stores the row */
+        if (b->ovr_st < 0) {
+          after.ovr_st = (int)st;
+          after.ovr_d = da;
+        } else {
+          after.gen = 0;
+        }
+      }
       p->n_removed = 1;
       p->removed_idx[0] = idxbuf[pick];
       p->n_added = 1;
@@ -1030,6 +1066,8 @@ so_run* so_run_chromatic(const so_model* m, const double* signals, const so_samp
   uint64_t next_base = 0;
   for (int64_t i = 0; i < n_init; ++i) {
     ev_t e;
+    memset(&e, 0, sizeof e);
+    e.ovr_st = -1;
     e.id = ids[i];
     e.x = x[i];
     e.t = t[i];
@@ -1425,6 +1463,8 @@ so_run* so_run_serial(const so_model* m, const double* signals, const so_sampler
   uint64_t id_base = 0;
   for (int64_t i = 0; i < n_init; ++i) {
     ev_t e;
+    memset(&e, 0, sizeof e);
+    e.ovr_st = -1;
     e.id = ids[i];
     e.x = x[i];
     e.t = t[i];

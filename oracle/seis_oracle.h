@@ -39,6 +39,7 @@ typedef struct {
   double step_location_x, step_location_t, step_arrival, step_joint;
   int64_t rng_mode; /* 0: reference xoshiro streams, 1: philox stream spec v1 */
   int64_t dynamic;  /* 0: chromatic-static, 1: chromatic-dynamic */
+  int64_t compact;  /* rng_mode 1: arrival storage spec v2 (generated versions) */
 } so_sampler;
 
 /* one MH step of a chain, as seen by the driver */

@@ -206,7 +206,14 @@ __global__ void k_build_cov(Dev d, Table tab, Ctl* ctl) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= d.P2) return;
   for (int e = blockIdx.y; e < ctl->n_events; e += gridDim.y) {
-    const double2 a = reinterpret_cast<const double2*>(d.pool)[(size_t)tab.slot[e] * d.P2 + p];
+    const int sl = tab.slot[e];
+    double2 a;
+    if (sl >= 0) {
+      a = reinterpret_cast<const double2*>(d.pool)[(size_t)sl * d.P2 + p];
+    } else {  // generated version
+      a.x = 2 * p < d.S ? arr_of(d, sl, 2 * p) : 0.0;
+      a.y = 2 * p + 1 < d.S ? arr_of(d, sl, 2 * p + 1) : 0.0;
+    }
     const Win w0 = 2 * p < d.S ? make_win(d, a.x) : empty_win();
     const Win w1 = 2 * p + 1 < d.S ? make_win(d, a.y) : empty_win();
     const int lo = min(w0.lo < w0.hi ? w0.lo : INT_MAX, w1.lo < w1.hi ? w1.lo : INT_MAX);
@@ -414,7 +421,7 @@ __device__ void gen_proposal(const Dev& d, const Samp& sp, const PhaseArgs& pa, 
   }
 }
 
-template <typename YT, int MODE, int NTT, int MINB, int CAP>
+template <typename YT, int MODE, int NTT, int MINB, int CAP, bool GEN>
 __global__ void __launch_bounds__(NTT, MINB)
     k_phase(const Dev d, const Samp sp, const PhaseArgs pa, Ctl* ctl, int stamp) {
   constexpr int NWT = NTT / 32;
@@ -646,7 +653,7 @@ __global__ void __launch_bounds__(NTT, MINB)
       const int np_c = s_np;
       DiffS4x* ovf = const_cast<DiffS4x*>(diff_cache_overflow());
       for (int j = tid; j < d.S_pad; j += NTT)
-        diff_station(d, j, np_c, pold, pnew, dcache[j], ovf[j]);
+        diff_station<GEN>(d, j, np_c, pold, pnew, dcache[j], ovf[j]);
     }
     __syncthreads();  // S1: proposals (and diff windows) ready
     if (tid == 0) {
@@ -666,7 +673,7 @@ __global__ void __launch_bounds__(NTT, MINB)
         for (int tile = warp; tile < T_per; tile += NWT) {
           DiffW X;
           long long tq = kProfItems ? clock64() : 0;
-          diff_windows(d, tile * 32 + lane, np_now, pold, pnew, X);
+          diff_windows<GEN>(d, tile * 32 + lane, np_now, pold, pnew, X);
           if (kProfItems) {
             __syncwarp();
             const long long now = clock64();
@@ -694,7 +701,8 @@ __global__ void __launch_bounds__(NTT, MINB)
             in.whi = win_hi;
             double sig = 0.0, arr = 0.0;
             int cnt = 0;
-            score_item<MODE, YT>(d, P, in, tile, np_now, pold, pnew, X, true, Ts, sig, arr, cnt);
+            score_item<MODE, YT, GEN>(d, P, in, tile, np_now, pold, pnew, X, true, Ts, sig, arr,
+                                      cnt);
             // per-lane partial sums; the warp reduces them once per round
             acc_sig[q][tid] += sig;
             acc_arr[q][tid] += arr;
@@ -772,7 +780,7 @@ __global__ void __launch_bounds__(NTT, MINB)
               X.nwmax = 0;
             }
           }
-          score_item<MODE, YT>(d, P, in, tile, np_now, pold, pnew, X, use_dcache, Ts, sig, arr,
+          score_item<MODE, YT, GEN>(d, P, in, tile, np_now, pold, pnew, X, use_dcache, Ts, sig, arr,
                                cnt);
         }
         if (cur_q >= 0) {
@@ -914,13 +922,46 @@ __global__ void __launch_bounds__(NTT, MINB)
         // allocate destination slots; modify this-phase versions in place
         bool ok = true;
         for (int a = 0; a < P.na; ++a) {
-          if (a < P.nr && P.rsidx[a] < 0) {
+          // the new version's kind (spec v2): a birth of a compact run, and a
+          // location / joint move or a first arrival override of a generated
+          // version, stay generated; everything else is a stored row
+          int gen = 0;
+          if (MODE == 0 && GEN) {
+            if (P.type == 0) {
+              gen = pa.compact;
+            } else {
+              const int rs = P.rslot[a < P.nr ? a : 0];
+              if (rs < -1) gen = P.type == 3 ? (d.gv[-2 - rs].ovr_st < 0 ? 1 : 0) : 1;
+            }
+          }
+          P.dgen[a] = gen;
+          if (a < P.nr && P.rsidx[a] < 0 && (!GEN || (P.rslot[a] < -1) == (gen != 0))) {
             P.dslot[a] = P.rslot[a];
             P.inplace[a] = 1;
           } else {
             P.inplace[a] = 0;
-            if (nlfree > 0) {
-              P.dslot[a] = lfree[--nlfree];
+            int got = -1;  // a slot of the same kind freed earlier this phase
+            if (!GEN) {
+              if (nlfree > 0) got = lfree[--nlfree];
+            } else {
+              for (int k2 = nlfree - 1; k2 >= 0; --k2)
+                if ((lfree[k2] < -1) == (gen != 0)) {
+                  got = lfree[k2];
+                  lfree[k2] = lfree[--nlfree];
+                  break;
+                }
+            }
+            if (got != -1) {
+              P.dslot[a] = got;
+            } else if (gen) {
+              const int top = atomicSub(&ctl->gv_top, 1) - 1;
+              if (top < 0) {
+                atomicAdd(&ctl->gv_top, 1);
+                set_err(ctl, ERR_GEN_EXHAUSTED);
+                ok = false;
+                break;
+              }
+              P.dslot[a] = -2 - d.gv_free[top];
             } else {
               const int top = atomicSub(&ctl->free_top, 1) - 1;
               if (top < 0) {
@@ -950,7 +991,7 @@ __global__ void __launch_bounds__(NTT, MINB)
           const int sidx = P.rsidx[r];
           if (sidx >= 0)
             st[sidx].current = 0;
-          else if (r >= P.na)
+          else if (!(r < P.na && P.inplace[r]))
             lfree[nlfree++] = P.rslot[r];
         }
         // apply_change (density.hpp:171-180): erase by id, push_back added
@@ -1049,15 +1090,47 @@ __global__ void __launch_bounds__(NTT, MINB)
       const int step = (int)(pa.step_base + i0 + accq);  // chain step (philox counter)
       double2* pool2 = reinterpret_cast<double2*>(d.pool);
       const double2* st2 = reinterpret_cast<const double2*>(d.stations);
+      if (MODE == 0 && GEN && tid == 0) {  // generated versions: their descriptors (spec v2)
+        for (int a = 0; a < P.na; ++a) {
+          if (!P.dgen[a]) continue;
+          GenV g;
+          if (P.type == 0) {
+            g.seed = sp.seed;
+            g.sweep = (unsigned)pa.epoch;
+            g.region = (unsigned)region;
+            g.step = (unsigned)step;
+            g.ovr_st = -1;
+            g.ovr_d = 0.0;
+          } else {
+            g = load_gv(d, P.rslot[a]);  // (read before an in-place write)
+            if (P.type == 3) {
+              g.ovr_st = P.arr_st;
+              g.ovr_d = P.arr_da;
+            }
+          }
+          g.x = P.ax[a];
+          g.t = P.at[a];
+          d.gv[-2 - P.dslot[a]] = g;
+        }
+      }
       if (MODE == 0 && P.type == 3) {
-        if (P.inplace[0]) {
+        if (GEN && P.dgen[0]) {
+          // nothing to write: the override lives in the descriptor
+        } else if (P.inplace[0]) {
           if (tid == 0) {
             double& a = d.pool[(size_t)P.dslot[0] * d.S_pad + P.arr_st];
             a = a + P.arr_da;
           }
         } else {
+          const int rs = P.rslot[0];
           for (int p = tid; p < d.P2; p += NTT) {
-            double2 v = pool2[(size_t)P.rslot[0] * d.P2 + p];
+            double2 v;
+            if (!GEN || rs >= 0) {
+              v = pool2[(size_t)rs * d.P2 + p];
+            } else {  // a generated version with an override: materialised
+              v.x = 2 * p < d.S ? arr_of(d, rs, 2 * p) : 0.0;
+              v.y = 2 * p + 1 < d.S ? arr_of(d, rs, 2 * p + 1) : 0.0;
+            }
             if (2 * p == P.arr_st) v.x = v.x + P.arr_da;
             if (2 * p + 1 == P.arr_st) v.y = v.y + P.arr_da;
             pool2[(size_t)P.dslot[0] * d.P2 + p] = v;
@@ -1065,6 +1138,7 @@ __global__ void __launch_bounds__(NTT, MINB)
         }
       } else {
         for (int a = 0; a < P.na; ++a) {
+          if (MODE == 0 && GEN && P.dgen[a]) continue;
           for (int p = tid; p < d.P2; p += NTT) {
             const double2 s = st2[p];
             const double m0 = arrival_mean(d, P.ax[a], P.at[a], s.x);
@@ -1211,11 +1285,17 @@ __device__ __forceinline__ void commit_body(const Dev& d, int color, int ncol, i
         const double2 a = pool2[(size_t)so * d.P2 + p];
         if (2 * p < d.S) o0 = make_win(d, a.x);
         if (2 * p + 1 < d.S) o1 = make_win(d, a.y);
+      } else if (so != -1) {  // generated version
+        if (2 * p < d.S) o0 = make_win(d, arr_of(d, so, 2 * p));
+        if (2 * p + 1 < d.S) o1 = make_win(d, arr_of(d, so, 2 * p + 1));
       }
       if (sn >= 0) {
         const double2 a = pool2[(size_t)sn * d.P2 + p];
         if (2 * p < d.S) n0 = make_win(d, a.x);
         if (2 * p + 1 < d.S) n1 = make_win(d, a.y);
+      } else if (sn != -1) {
+        if (2 * p < d.S) n0 = make_win(d, arr_of(d, sn, 2 * p));
+        if (2 * p + 1 < d.S) n1 = make_win(d, arr_of(d, sn, 2 * p + 1));
       }
       if (weq(o0, n0)) o0 = n0 = empty_win();  // unchanged at this station
       if (weq(o1, n1)) o1 = n1 = empty_win();
@@ -1252,6 +1332,12 @@ __device__ __forceinline__ void commit_body(const Dev& d, int color, int ncol, i
           free_stack[top] = slot;
         else
           set_err(ctl, ERR_POOL_EXHAUSTED);  // never write outside the stack
+      } else if (slot != -1) {  // a generated version's entry
+        const int top = atomicAdd(&ctl->gv_top, 1);
+        if (top >= 0 && top < d.gv_cap)
+          d.gv_free[top] = -2 - slot;
+        else
+          set_err(ctl, ERR_GEN_EXHAUSTED);
       }
     }
 }
@@ -1446,7 +1532,7 @@ __global__ void __launch_bounds__(NT, 1)
   DiffW X0;  // no own diff: the batch scores against the resident hypothesis
   X0.nwmax = 0;
   for (int t = warp; t < T_per; t += NW)
-    score_item<1, YT>(d, P, in, t, 0, nullptr, nullptr, X0, true, Ts, sig, arr, cnt);
+    score_item<1, YT, true>(d, P, in, t, 0, nullptr, nullptr, X0, true, Ts, sig, arr, cnt);
   sig = warp_sum(sig);
   arr = warp_sum(arr);
   if (lane == 0) {
@@ -1511,7 +1597,7 @@ __global__ void k_lj_arrivals(const Dev d, Table tab, const Ctl* ctl, double* pa
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
        i += (size_t)gridDim.x * blockDim.x) {
     const int e = (int)(i / d.S), j = (int)(i % d.S);
-    const double a = d.pool[(size_t)tab.slot[e] * d.S_pad + j];
+    const double a = arr_of(d, tab.slot[e], j);
     acc += arr_logpdf(d, a, arrival_mean(d, tab.x[e], tab.t[e], d.stations[j]));
   }
   acc = warp_sum(acc);
@@ -1556,11 +1642,10 @@ __global__ void k_record(const Ctl* ctl, long long* count_out) { *count_out = ct
 
 // arrivals of hypothesis rows: pool slot rows <-> dense [m][S] (one launch,
 // one copy, instead of one copy per event)
-__global__ void k_gather_arrivals(const double* pool, const int* slot, int S, int S_pad, int m,
-                                  double* out) {
+__global__ void k_gather_arrivals(const Dev d, const int* slot, int m, double* out) {
   const int e = blockIdx.y;
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < S; j += gridDim.x * blockDim.x)
-    out[(size_t)e * S + j] = pool[(size_t)slot[e] * S_pad + j];
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < d.S; j += gridDim.x * blockDim.x)
+    out[(size_t)e * d.S + j] = arr_of(d, slot[e], j);  // stored row or generated version
 }
 
 // input rows [0, gridDim.y) of a chunk -> their pool slots
@@ -1704,6 +1789,11 @@ struct seis_engine {
   seis_model_cfg cfg{};
   int S = 0, S_pad = 0, P2 = 0, n = 0, dtype = 0, cap = 0;
   int pool_slots = 0;  // arrival versions: live events + this phase's retired ones
+  GenV* gv = nullptr;  // generated versions (spec v2) and their free stack
+  int* gv_free = nullptr;
+  int gv_cap = 0;
+  int compact = 0;     // production births make generated versions
+  bool gen_present = false;  // generated versions may be live (cleared by a hypothesis load)
   // the last run's Trace::phases (samplers.hpp:87-95,370,479) and the device
   // time of its trace rows since the run started (TraceRow/Snapshot wall_seconds)
   std::vector<seis_phase_record> phases;
@@ -1841,6 +1931,7 @@ const char* err_name(int e) {
     case ERR_POOL_EXHAUSTED: return "arrival pool exhausted (live events + replaced versions > pool slots): raise event_capacity";
     case ERR_TAPE_UNKNOWN_ID: return "replay tape names an event the region does not hold";
     case ERR_TABLE_OVERFLOW: return "event table overflow: raise event_capacity";
+    case ERR_GEN_EXHAUSTED: return "generated-version table exhausted (raise event_capacity)";
     case ERR_COUNT_OVERFLOW: return "more than 65535 events cover one (sample, station): uint16 coverage count overflow";
     default: return "device error";
   }
@@ -1868,14 +1959,22 @@ namespace {
 // One 512-thread CTA per region. Measured on configs 1 and 2: 256-thread
 // CTAs two or three per SM lose (1.44 M and 1.21 M vs 1.72 M proposals/s at
 // config[2]): a chain's rounds slow down more than sharing an SM gains.
+// Variants: the row-only production kernel (GEN = false) when the engine
+// holds no generated versions and makes none (the default storage); every
+// other launch (compact storage, replay, the serial chain) handles both kinds.
 template <typename YT, int MODE>
 void launch_phase_t(seis_engine* e, int ncr, const Samp& sp, const PhaseArgs& pa, int stamp) {
+  const bool rows_only = MODE == 0 && !pa.serial && !e->compact && !e->gen_present;
   if (pa.serial)
-    k_phase<YT, MODE, NT, SEIS_MINB, kSerialCap><<<ncr, NT, kPhaseSmemSerial, e->stream>>>(
-        e->d, sp, pa, e->ctl, stamp);
+    k_phase<YT, MODE, NT, SEIS_MINB, kSerialCap, true>
+        <<<ncr, NT, kPhaseSmemSerial, e->stream>>>(e->d, sp, pa, e->ctl, stamp);
+  else if (MODE == 0 && rows_only)
+    k_phase<YT, 0, NT, SEIS_MINB, MAXOWN, false>
+        <<<ncr, NT, phase_smem(e->d), e->stream>>>(e->d, sp, pa, e->ctl, stamp);
   else
-    k_phase<YT, MODE, NT, SEIS_MINB, MAXOWN><<<ncr, NT, phase_smem(e->d), e->stream>>>(
-        e->d, sp, pa, e->ctl, stamp);
+    k_phase<YT, MODE, NT, SEIS_MINB, MAXOWN, true>
+        <<<ncr, NT, phase_smem(e->d), e->stream>>>(e->d, sp, pa, e->ctl, stamp);
+  if (MODE == 0 && e->compact) e->gen_present = true;
 }
 
 void launch_phase(seis_engine* e, int mode, int ncr, const Samp& sp, const PhaseArgs& pa,
@@ -1895,10 +1994,14 @@ void launch_phase(seis_engine* e, int mode, int ncr, const Samp& sp, const Phase
 
 template <typename YT, int MODE>
 void set_phase_attrs() {
-  ck(cudaFuncSetAttribute(k_phase<YT, MODE, NT, SEIS_MINB, MAXOWN>,
+  ck(cudaFuncSetAttribute(k_phase<YT, MODE, NT, SEIS_MINB, MAXOWN, true>,
                           cudaFuncAttributeMaxDynamicSharedMemorySize, kPhaseSmem),
      "smem attribute");
-  ck(cudaFuncSetAttribute(k_phase<YT, MODE, NT, SEIS_MINB, kSerialCap>,
+  if (MODE == 0)
+    ck(cudaFuncSetAttribute(k_phase<YT, 0, NT, SEIS_MINB, MAXOWN, false>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, kPhaseSmem),
+       "smem attribute");
+  ck(cudaFuncSetAttribute(k_phase<YT, MODE, NT, SEIS_MINB, kSerialCap, true>,
                           cudaFuncAttributeMaxDynamicSharedMemorySize, kPhaseSmemSerial),
      "smem attribute");
 }
@@ -2008,6 +2111,13 @@ int seis_engine_create(const seis_model_cfg* cfg, const double* stations, int64_
       t.slot = dalloc<int>(e->cap);
     }
     e->free_stack = dalloc<int>(e->pool_slots);
+    // generated versions (spec v2): four entries per event of capacity; the
+    // compact storage is on by default when the pool cannot hold two stored
+    // rows per event (seis_set_arrival_storage overrides)
+    e->gv_cap = (int)std::min<int64_t>((int64_t)4 * e->cap + 4096, (int64_t)1 << 26);
+    e->gv = dalloc<GenV>(e->gv_cap);
+    e->gv_free = dalloc<int>(e->gv_cap);
+    e->compact = e->pool_slots < 2 * e->cap ? 1 : 0;
     e->ctl = dalloc<Ctl>(1);
     e->fate_stamp = dalloc<int>(e->cap);
     ck(cudaMemset(e->fate_stamp, 0, e->cap * 4), "memset");
@@ -2046,6 +2156,9 @@ int seis_engine_create(const seis_model_cfg* cfg, const double* stations, int64_
     d.logi = e->logi;
     d.logi_n = logi_n;
     d.pool_cap = e->pool_slots;
+    d.gv = e->gv;
+    d.gv_free = e->gv_free;
+    d.gv_cap = e->gv_cap;
     set_phase_attrs<float, 0>();
     set_phase_attrs<float, 1>();
     set_phase_attrs<double, 0>();
@@ -2128,9 +2241,19 @@ int hyp_begin(seis_engine* e, int64_t N, const uint64_t* ids, const double* x, c
       ck(cudaMemcpyAsync(e->free_stack, fs.data(), (size_t)nf * 4, cudaMemcpyHostToDevice,
                          e->stream),
          "H2D");
+    e->gen_present = false;
+    // every generated-version entry free (a loaded hypothesis is stored rows)
+    {
+      std::vector<int> gf(e->gv_cap);
+      for (int g = 0; g < e->gv_cap; ++g) gf[g] = e->gv_cap - 1 - g;  // top of stack = 0
+      ck(cudaMemcpyAsync(e->gv_free, gf.data(), (size_t)e->gv_cap * 4, cudaMemcpyHostToDevice,
+                         e->stream),
+         "H2D");
+    }
     Ctl c{};
     c.n_events = (int)N;
     c.free_top = nf;
+    c.gv_top = e->gv_cap;
     ck(cudaMemcpyAsync(e->ctl, &c, sizeof c, cudaMemcpyHostToDevice, e->stream), "H2D");
     ck(cudaMemsetAsync(e->cov, 0, (size_t)(e->n + kRowPad) * e->P2 * 4, e->stream), "memset");
     // (pageable sources: each copy returned once its data was staged)
@@ -2222,7 +2345,7 @@ int seis_get_hypothesis(seis_engine* e, int64_t cap, int64_t* n, uint64_t* ids, 
       for (int64_t r0 = 0; r0 < m; r0 += chunk) {
         const int64_t nr = std::min(chunk, m - r0);
         dim3 grid((unsigned)std::min(64, (e->S + 255) / 256), (unsigned)nr);
-        k_gather_arrivals<<<grid, 256, 0, e->stream>>>(e->pool, tb.slot + r0, e->S, e->S_pad,
+        k_gather_arrivals<<<grid, 256, 0, e->stream>>>(e->d, tb.slot + r0,
                                                        (int)nr, buf);
         ck(cudaGetLastError(), "k_gather_arrivals");
         ck(cudaMemcpyAsync(arrivals + (size_t)r0 * e->S, buf, (size_t)nr * e->S * 8,
@@ -2283,6 +2406,18 @@ int seis_get_snapshots(seis_engine* e, int64_t cap_snap, int64_t* n_snap, int64_
       ck(cudaMemcpy(t, e->snap_t, total * 8, cudaMemcpyDeviceToHost), "D2H");
     }
   });
+}
+
+int seis_set_arrival_storage(seis_engine* e, int32_t mode) {
+  return guarded([&] {
+    if (mode != SEIS_ARR_ROWS && mode != SEIS_ARR_COMPACT)
+      throw std::invalid_argument("arrival storage must be SEIS_ARR_ROWS or SEIS_ARR_COMPACT");
+    e->compact = mode == SEIS_ARR_COMPACT ? 1 : 0;
+  });
+}
+
+int32_t seis_get_arrival_storage(const seis_engine* e) {
+  return e && e->compact ? SEIS_ARR_COMPACT : SEIS_ARR_ROWS;
 }
 
 int seis_get_phases(seis_engine* e, int64_t cap, int64_t* n, seis_phase_record* out) {
@@ -2684,6 +2819,7 @@ static int run_driver(seis_engine* e, const seis_sampler_cfg* sc, int32_t mode,
       pa.diff_cnt = diff_cnt;
       pa.diff = diff;
       pa.free_stack = e->free_stack;
+      pa.compact = e->compact;
       pa.tape = d_tape;
       pa.tape_arr = d_tarr;
       pa.out = d_out;
@@ -2831,6 +2967,7 @@ static int run_driver(seis_engine* e, const seis_sampler_cfg* sc, int32_t mode,
       stats->final_events = c.n_events;
       stats->speculative_discarded = (int64_t)c.speculative;
       stats->phases = (int64_t)phase_ev.size();
+      stats->generated_versions = (int64_t)e->gv_cap - c.gv_top;
     }
   });
   for (auto ev : evs) cudaEventDestroy(ev);
@@ -2986,6 +3123,7 @@ extern "C" int seis_run_naive(seis_engine* e, const seis_sampler_cfg* sc, int32_
     pa.diff_cnt = diff_cnt;
     pa.diff = diff;
     pa.free_stack = e->free_stack;
+    pa.compact = e->compact;
     pa.tape = d_tape;
     pa.tape_arr = d_tarr;
     pa.out = d_out;
@@ -3076,6 +3214,7 @@ extern "C" int seis_run_naive(seis_engine* e, const seis_sampler_cfg* sc, int32_
       stats->kernel_launches = 3 + (sc->record_log_joint ? 3 : 0);
       stats->n_rows = n_cp;
       stats->phases = 1;
+      stats->generated_versions = (int64_t)e->gv_cap - c.gv_top;
       stats->final_events = c.n_events;
       stats->speculative_discarded = (int64_t)c.speculative;
     }

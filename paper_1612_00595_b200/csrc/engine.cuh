@@ -70,6 +70,20 @@ struct Win {
 // walking a station tile's rows reads coalesced lines at compile-time offsets.
 // Counts are uint16; two neighbouring stations share a uint32 word (the
 // commit's packed atomics): pair p = j >> 1 at ((p >> 4) * rows + r) * 16 + (p & 15).
+// Compact arrival versions ("philox stream spec v2", include/seis_philox.h):
+// an event version is either a stored row of the arrival pool (slot >= 0) or
+// a generated version (slot = -2 - g, g indexing the GenV table): the arrival
+// at station j is computed, arrival_mean(x, t, j) + sigma z_j with z_j the
+// philox normal of the birth that created it, plus at most one per-station
+// override. Slot -1 means "no version" (a birth's start, a death's end).
+struct GenV {
+  double x, t;                  // the version's location
+  unsigned long long seed;      // the birth's philox key ...
+  unsigned sweep, region, step; // ... and counter
+  int ovr_st;                   // station of the one override (-1: none)
+  double ovr_d;                 // its arrival delta
+};
+
 struct Dev {
   int S, S_pad, P2, n;
   int rows;                        // n + kRowPad
@@ -83,6 +97,8 @@ struct Dev {
   const void* y;                   // [S_pad / 32][rows][32] (station tiles)
   uint32_t* cov;                   // [S_pad / 32][rows][16] uint16 pairs
   double* pool;                    // [P][S_pad]
+  GenV* gv;                        // [gv_cap] generated versions
+  int* gv_free;                    // [gv_cap] free stack of GenV entries (top: Ctl::gv_top)
   const double* Lg;                // [tab_n] -0.5 (log 2pi + log var_c)
   const double* Ig;                // [tab_n] 0.5 / var_c
   const double2* Dg;               // [tab_n][4] {L[c+dc]-L[c], I[c+dc]-I[c]}, dc=-2,-1,1,2
@@ -90,6 +106,7 @@ struct Dev {
   const double* logi;              // [logi_n] log((double) i)
   int logi_n;
   int pool_cap;
+  int gv_cap;
 };
 
 struct Samp {
@@ -128,6 +145,7 @@ struct Ctl {
   int free_top;
   int err;
   int phase_stamp;
+  int gv_top, gv_pad;  // free stack of generated-version entries
   unsigned long long scored, changed, arrvals, accepted, id_mismatch, speculative;
   unsigned long long prof[8];  // clock64 cycles per round section (thread 0 of every CTA)
   unsigned long long tprof[2][8];  // per move type: warp-cycles in items, items
@@ -149,6 +167,7 @@ struct PhaseArgs {
   int* diff_cnt;                   // [n_slots]
   DiffPair* diff;                  // [n_slots][MAXDOUT]
   int* free_stack;
+  int compact;                     // births (and their moves) make generated versions
   const seis_tape_step* tape;
   const double* tape_arr;
   seis_step_out* out;
@@ -180,6 +199,7 @@ enum : int {
   ERR_TAPE_UNKNOWN_ID = 3,
   ERR_TABLE_OVERFLOW = 4,
   ERR_COUNT_OVERFLOW = 5,
+  ERR_GEN_EXHAUSTED = 6,
 };
 
 // the first device error of a run wins (later ones are consequences)
@@ -220,6 +240,28 @@ __device__ __forceinline__ double div_v(const Dev& d, double a) {
 
 __device__ __forceinline__ double arrival_mean(const Dev& d, double x, double t, double s) {
   return t + div_v(d, fabs(x - s));  // model.hpp:73-75
+}
+
+// generated version's arrival at station j (spec v2): (mean + sigma z) [+ override]
+__device__ __forceinline__ double gen_arrival(const Dev& d, const GenV& g, int j, double mean) {
+  double a = mean + d.sigma * (double)seis_normal(g.seed, g.sweep, g.region, g.step, (uint32_t)j);
+  if (j == g.ovr_st) a = a + g.ovr_d;
+  return a;
+}
+__device__ __forceinline__ GenV load_gv(const Dev& d, int slot) { return d.gv[-2 - slot]; }
+// any version's arrival at station j (slot != -1)
+__device__ __forceinline__ double arr_of(const Dev& d, int slot, int j) {
+  if (slot >= 0) return __ldg(d.pool + (size_t)slot * d.S_pad + j);
+  const GenV g = load_gv(d, slot);
+  return gen_arrival(d, g, j, arrival_mean(d, g.x, g.t, d.stations[j]));
+}
+
+// GEN = false: the kernel variant of runs that hold stored rows only (the
+// default arrival storage): the plain pool load, as before spec v2
+template <bool GEN>
+__device__ __forceinline__ double ver_arr(const Dev& d, int slot, int j) {
+  if constexpr (GEN) return arr_of(d, slot, j);
+  return __ldg(d.pool + (size_t)slot * d.S_pad + j);
 }
 
 __device__ __forceinline__ double arr_logpdf(const Dev& d, double a, double mean) {

@@ -45,6 +45,7 @@ struct Prop {
   int u_drawn, tape_acc;
   int accept;
   int dslot[2], inplace[2];
+  int dgen[2];  // the accepted version is a generated one (spec v2)
 };
 
 // sidx: the event's phase-start index i while its start version is current;
@@ -365,7 +366,7 @@ __device__ __forceinline__ void edges(const Dev& d, int j, Win A0, Win R0, const
 
 // Many effective diff windows at a station (> 4): the correction of the band
 // rows is accumulated in a per-thread scratch column first (rare).
-template <int NR, int NA, typename YT>
+template <int NR, int NA, typename YT, bool GEN>
 __device__ __forceinline__ void band_generic(const Dev& d, int j, bool v, int blo, int bhi,
                                           const Wins<NR> R, const Wins<NA> A, int np,
                                           const int* pold, const int* pnew,
@@ -379,8 +380,8 @@ __device__ __forceinline__ void band_generic(const Dev& d, int j, bool v, int bl
     const int c1 = min(bhi, c0 + BANDMAX);
     for (int i = 0; i < c1 - c0; ++i) corr[i] = 0;
     for (int q = 0; q < np && v; ++q) {
-      const Win wo = pold[q] >= 0 ? make_win(d, d.pool[(size_t)pold[q] * d.S_pad + j]) : empty_win();
-      const Win wn = pnew[q] >= 0 ? make_win(d, d.pool[(size_t)pnew[q] * d.S_pad + j]) : empty_win();
+      const Win wo = pold[q] != -1 ? make_win(d, ver_arr<GEN>(d, pold[q], j)) : empty_win();
+      const Win wn = pnew[q] != -1 ? make_win(d, ver_arr<GEN>(d, pnew[q], j)) : empty_win();
       if (weq(wo, wn)) continue;
       for (int r = max(wo.lo, c0); r < min(wo.hi, c1); ++r) corr[r - c0] -= 1;
       for (int r = max(wn.lo, c0); r < min(wn.hi, c1); ++r) corr[r - c0] += 1;
@@ -414,7 +415,7 @@ struct DiffW {
 
 // Walk the region's (start, current) pairs at station j with each batch of
 // four pairs' pool loads issued together; first four effective windows kept.
-template <int K>
+template <int K, bool GEN>
 __device__ __forceinline__ int diff_collect(const Dev& d, int j, int np, const int* pold,
                                             const int* pnew, Win (&w)[K], int (&sg)[K]) {
   int nw = 0;
@@ -430,15 +431,15 @@ __device__ __forceinline__ int diff_collect(const Dev& d, int j, int np, const i
     for (int k = 0; k < 4; ++k) {
       const int q = q0 + k;
       const int so = q < np ? pold[q] : -1, sn = q < np ? pnew[q] : -1;
-      vo[k] = so >= 0 ? __ldg(d.pool + (size_t)so * d.S_pad + j) : 0.0;
-      vn[k] = sn >= 0 ? __ldg(d.pool + (size_t)sn * d.S_pad + j) : 0.0;
+      vo[k] = so != -1 ? ver_arr<GEN>(d, so, j) : 0.0;
+      vn[k] = sn != -1 ? ver_arr<GEN>(d, sn, j) : 0.0;
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const int q = q0 + k;
       if (q >= np) break;
-      const Win wo = pold[q] >= 0 ? make_win(d, vo[k]) : empty_win();
-      const Win wn = pnew[q] >= 0 ? make_win(d, vn[k]) : empty_win();
+      const Win wo = pold[q] != -1 ? make_win(d, vo[k]) : empty_win();
+      const Win wn = pnew[q] != -1 ? make_win(d, vn[k]) : empty_win();
       if (weq(wo, wn)) continue;
       if (wo.hi > wo.lo) {
 #pragma unroll
@@ -463,9 +464,10 @@ __device__ __forceinline__ int diff_collect(const Dev& d, int j, int np, const i
   return nw;
 }
 
+template <bool GEN>
 __device__ __forceinline__ void diff_windows(const Dev& d, int j, int np, const int* pold,
                                              const int* pnew, DiffW& X) {
-  const int nw = diff_collect<4>(d, j, np, pold, pnew, X.D.w, X.sg);
+  const int nw = diff_collect<4, GEN>(d, j, np, pold, pnew, X.D.w, X.sg);
   X.nwmax = (int)__reduce_max_sync(0xffffffffu, (unsigned)nw);
 }
 
@@ -484,11 +486,12 @@ struct DiffS4x {
   int8_t sg[4];
 };
 
+template <bool GEN>
 __device__ __forceinline__ void diff_station(const Dev& d, int j, int np, const int* pold,
                                              const int* pnew, DiffS& o, DiffS4x& ov) {
   Win w[8];
   int sg[8];
-  o.n = diff_collect<8>(d, j, np, pold, pnew, w, sg);
+  o.n = diff_collect<8, GEN>(d, j, np, pold, pnew, w, sg);
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     o.lo[k] = (uint16_t)w[k].lo;
@@ -527,7 +530,7 @@ __device__ __forceinline__ void diff_from_cache(const DiffS& c, DiffW& X) {
 // the added/removed versions (arr += added - removed) and the per-sample
 // terms where the coverage changes (sig). Called by a whole warp
 // (j = tile base + lane) so the band reduction is warp-uniform.
-template <int NR, int NA, typename YT>
+template <int NR, int NA, typename YT, bool GEN>
 __device__ __forceinline__ void station_item(const Dev& d, const Prop& P, const PassIn& in,
                                              int j, int np, const int* pold, const int* pnew,
                                              DiffW X, bool haveX, const double2* Ts, double& sig,
@@ -538,14 +541,27 @@ __device__ __forceinline__ void station_item(const Dev& d, const Prop& P, const 
   Wins<NA> A;
   const double s = v ? d.stations[j] : 0.0;
   double ra[NR > 0 ? NR : 1];
+  // a generated removed version (spec v2): its arrival and, for a location /
+  // joint move, the moved version's arrival come from the same normal
+  double rz[NR > 0 ? NR : 1];
 #pragma unroll
   for (int q = 0; q < NR; ++q) {
     R.w[q] = empty_win();
     ra[q] = 0.0;
+    rz[q] = 0.0;
     if (v && q < P.nr) {
-      ra[q] = d.pool[(size_t)P.rslot[q] * d.S_pad + j];
+      const double mo = arrival_mean(d, P.rx[q], P.rt[q], s);
+      const int rs = P.rslot[q];
+      if (!GEN || rs >= 0) {
+        ra[q] = __ldg(d.pool + (size_t)rs * d.S_pad + j);
+      } else {
+        const GenV g = load_gv(d, rs);
+        rz[q] = d.sigma * (double)seis_normal(g.seed, g.sweep, g.region, g.step, (uint32_t)j);
+        ra[q] = mo + rz[q];
+        if (j == g.ovr_st) ra[q] = ra[q] + g.ovr_d;
+      }
       R.w[q] = clampw(make_win(d, ra[q]), in.wlo, in.whi);
-      arr -= arr_logpdf(d, ra[q], arrival_mean(d, P.rx[q], P.rt[q], s));
+      arr -= arr_logpdf(d, ra[q], mo);
     }
   }
 #pragma unroll
@@ -559,7 +575,13 @@ __device__ __forceinline__ void station_item(const Dev& d, const Prop& P, const 
                                                (uint32_t)j);
       } else if (in.src == SRC_SHIFT) {
         const int q = a < NR ? a : 0;
-        aa = ra[q] + (m - arrival_mean(d, P.rx[q], P.rt[q], s));
+        if (!GEN || P.rslot[q] >= 0) {  // stored row: shift by the mean (proposals.hpp:153-157)
+          aa = ra[q] + (m - arrival_mean(d, P.rx[q], P.rt[q], s));
+        } else {  // generated version (spec v2): residual kept exactly
+          const GenV g = load_gv(d, P.rslot[q]);
+          aa = m + rz[q];
+          if (j == g.ovr_st) aa = aa + g.ovr_d;
+        }
       } else {
         aa = in.rows[a][j];
       }
@@ -602,7 +624,7 @@ __device__ __forceinline__ void station_item(const Dev& d, const Prop& P, const 
   // built here, only for stations the proposal changes
   // (by value: a pointer or a reference selected between two DiffW objects
   // would put them in local memory)
-  if (!haveX) diff_windows(d, j, np, pold, pnew, X);
+  if (!haveX) diff_windows<GEN>(d, j, np, pold, pnew, X);
   const Wins<4>& D = X.D;
   const int(&sg)[4] = X.sg;
   const int nwmax = X.nwmax;
@@ -664,7 +686,7 @@ __device__ __forceinline__ void station_item(const Dev& d, const Prop& P, const 
     }
     band<NR, NA, 8, YT>(d, j, blo, bhi, R, A, D8, sg8, Ts, sig, cnt);
   } else {
-    band_generic<NR, NA, YT>(d, j, v, blo, bhi, R, A, np, pold, pnew, Ts, &sig, &cnt);
+    band_generic<NR, NA, YT, GEN>(d, j, v, blo, bhi, R, A, np, pold, pnew, Ts, &sig, &cnt);
   }
   if (kProfItems && NR + NA == 1) {
     __syncwarp();
@@ -677,14 +699,14 @@ __device__ __forceinline__ void station_item(const Dev& d, const Prop& P, const 
 
 // Arrival move (proposals.hpp:161-174) in production: only station st moves;
 // the warp's lanes take rows.
-template <typename YT>
+template <typename YT, bool GEN>
 __device__ __forceinline__ void arrival_item(const Dev& d, const Prop& P, const PassIn& in,
                                              int np, const int* pold, const int* pnew,
                                              const double2* Ts, double& sig, double& arr,
                                              int& cnt) {
   const int lane = threadIdx.x & 31;
   const int st = P.arr_st;
-  const double old_a = d.pool[(size_t)P.rslot[0] * d.S_pad + st];
+  const double old_a = ver_arr<GEN>(d, P.rslot[0], st);
   const double new_a = old_a + P.arr_da;
   const double mean = arrival_mean(d, P.rx[0], P.rt[0], d.stations[st]);
   if (lane == 0) arr += arr_logpdf(d, new_a, mean) - arr_logpdf(d, old_a, mean);
@@ -701,8 +723,8 @@ __device__ __forceinline__ void arrival_item(const Dev& d, const Prop& P, const 
     if (!dc) continue;
     int co = (int)c16[yix(d.rows, r, st)];
     for (int q = 0; q < np; ++q) {
-      if (pold[q] >= 0) co -= inw(r, make_win(d, d.pool[(size_t)pold[q] * d.S_pad + st]));
-      if (pnew[q] >= 0) co += inw(r, make_win(d, d.pool[(size_t)pnew[q] * d.S_pad + st]));
+      if (pold[q] != -1) co -= inw(r, make_win(d, ver_arr<GEN>(d, pold[q], st)));
+      if (pnew[q] != -1) co += inw(r, make_win(d, ver_arr<GEN>(d, pnew[q], st)));
     }
     sig += term(d, Ts, (double)y[yix(d.rows, r, st)], co, dc);
     ++cnt;
@@ -710,7 +732,7 @@ __device__ __forceinline__ void arrival_item(const Dev& d, const Prop& P, const 
 }
 
 // Dispatch one work item (tile of 32 stations) of proposal P.
-template <int MODE, typename YT>
+template <int MODE, typename YT, bool GEN>
 __device__ __forceinline__ void score_item(const Dev& d, const Prop& P, const PassIn& in,
                                            int tile, int np, const int* pold,
                                            const int* pnew, const DiffW& X, bool haveX,
@@ -719,18 +741,18 @@ __device__ __forceinline__ void score_item(const Dev& d, const Prop& P, const Pa
   if (P.skip) return;
   const int j = tile * 32 + (threadIdx.x & 31);
   if (MODE == 0 && P.type == 3) {
-    if (tile == 0) arrival_item<YT>(d, P, in, np, pold, pnew, Ts, sig, arr, cnt);
+    if (tile == 0) arrival_item<YT, GEN>(d, P, in, np, pold, pnew, Ts, sig, arr, cnt);
     return;
   }
   const int shape = P.nr * 3 + P.na;
   if (shape == 1)  // birth
-    station_item<0, 1, YT>(d, P, in, j, np, pold, pnew, X, haveX, Ts, sig, arr, cnt);
+    station_item<0, 1, YT, GEN>(d, P, in, j, np, pold, pnew, X, haveX, Ts, sig, arr, cnt);
   else if (shape == 3)  // death
-    station_item<1, 0, YT>(d, P, in, j, np, pold, pnew, X, haveX, Ts, sig, arr, cnt);
+    station_item<1, 0, YT, GEN>(d, P, in, j, np, pold, pnew, X, haveX, Ts, sig, arr, cnt);
   else if (shape == 4)  // location / arrival
-    station_item<1, 1, YT>(d, P, in, j, np, pold, pnew, X, haveX, Ts, sig, arr, cnt);
+    station_item<1, 1, YT, GEN>(d, P, in, j, np, pold, pnew, X, haveX, Ts, sig, arr, cnt);
   else  // joint pair, and any other change of <= 2 removed / 2 added events
-    station_item<2, 2, YT>(d, P, in, j, np, pold, pnew, X, haveX, Ts, sig, arr, cnt);
+    station_item<2, 2, YT, GEN>(d, P, in, j, np, pold, pnew, X, haveX, Ts, sig, arr, cnt);
 }
 
 }  // namespace seis

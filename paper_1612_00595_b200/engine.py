@@ -51,7 +51,7 @@ class _StatsC(C.Structure):
                 ("changed_samples", i64), ("arrival_values", i64), ("algorithmic_bytes", f64),
                 ("sweep_kernel_ms", f64), ("total_ms", f64), ("kernel_launches", i64),
                 ("n_rows", i64), ("final_events", i64), ("speculative_discarded", i64),
-                ("phases", i64)]
+                ("phases", i64), ("generated_versions", i64)]
 
 
 class _PhaseC(C.Structure):
@@ -80,7 +80,8 @@ EXPORTS = ("seis_last_error", "seis_engine_create", "seis_engine_destroy", "seis
            "seis_run_naive", "seis_run_serial", "seis_engine_pool_slots", "seis_eval_last_error",
            "seis_match_events", "seis_bootstrap_ci", "seis_get_phases", "seis_get_row_wall",
            "seis_set_hypothesis_begin", "seis_set_hypothesis_rows", "seis_set_hypothesis_end",
-           "seis_world_generate_events", "seis_world_with_events_signals", "seis_world_arrivals")
+           "seis_world_generate_events", "seis_world_with_events_signals", "seis_world_arrivals",
+           "seis_set_arrival_storage", "seis_get_arrival_storage")
 
 _LIB = None
 
@@ -123,6 +124,9 @@ def load_library(path: str | None = None) -> C.CDLL:
     L.seis_get_snapshots.argtypes = [P, i64, P, P, P, i64, P, P, P]
     L.seis_get_phases.argtypes = [P, i64, P, P]
     L.seis_set_hypothesis_begin.argtypes = [P, i64, P, P, P]
+    L.seis_set_arrival_storage.argtypes = [P, i32]
+    L.seis_get_arrival_storage.argtypes = [P]
+    L.seis_get_arrival_storage.restype = i32
     L.seis_set_hypothesis_rows.argtypes = [P, i64, i64, P]
     L.seis_set_hypothesis_end.argtypes = [P]
     L.seis_world_generate_events.argtypes = [P, P, i64, u64, i64, P, P, P, P, P, i32, i32]
@@ -637,6 +641,18 @@ class Engine:
         a = np.ascontiguousarray(ev.arrivals, np.float64).reshape(len(ids), S)
         _check(self.L.seis_set_hypothesis(self.h, len(ids), _p(ids), _p(x), _p(t), _p(a)),
                self.L)
+
+    @property
+    def arrival_storage(self) -> str:
+        """'rows' (philox stream spec v1: every version stores its S arrivals)
+        or 'compact' (spec v2: births and their moves as generated versions)."""
+        return "compact" if self.L.seis_get_arrival_storage(self.h) == 1 else "rows"
+
+    @arrival_storage.setter
+    def arrival_storage(self, mode: str):
+        if mode not in ("rows", "compact"):
+            raise ValueError("arrival storage must be 'rows' or 'compact'")
+        _check(self.L.seis_set_arrival_storage(self.h, 1 if mode == "compact" else 0), self.L)
 
     def set_hypothesis_streamed(self, ids, x, t, rows, chunk: int = 1024):
         """Load a hypothesis whose arrivals come in pieces: rows(i0, n) returns
