@@ -95,16 +95,44 @@ def config_block(c, args):
     return out
 
 
-def make_world(c, threads):
+def huge(c):
+    """configs whose N x S arrival matrix (10.5 GB at [3], 42 GB at [4]) is not
+    materialised on the host: streamed generation and hypothesis upload"""
+    return c["S"] * (c["events"] or 20000) * 8 > 4e9
+
+
+def make_world(c, threads, streamed=False):
+    """the config's world; streamed: events without their arrivals
+    (Events.arrivals None; world_arrivals regenerates them)"""
     import paper_1612_00595_b200 as E
     m = E.ModelConfig(**model_params(c))
     dt = E.F64 if c["dtype"] == "f64" else E.F32
     if c["events"] is None:
         cx, ct = E.thomas_events(*thomas_args(c))
-        ev, sig = E.make_world_with_events(m, cx, ct, 0, dtype=dt, threads=threads)
+        if streamed:
+            ev, sig = E.make_world_with_events_signals(m, cx, ct, 0, dtype=dt, threads=threads)
+        else:
+            ev, sig = E.make_world_with_events(m, cx, ct, 0, dtype=dt, threads=threads)
+    elif streamed:
+        ev, sig = E.sample_world_events(m, 0, dtype=dt, threads=threads)
     else:
         ev, sig = E.sample_world(m, 0, dtype=dt, threads=threads)
     return m, ev, sig
+
+
+def load_truth(E, eng, m, ev, threads, out=None):
+    """the truth hypothesis into the engine; streamed worlds regenerate the
+    arrival rows chunk by chunk (into `out` when given, e.g. a pinned buffer)"""
+    if ev.arrivals is not None:
+        eng.set_hypothesis(ev)
+        return
+    S = m.n_stations()
+    chunk = max(1, (512 << 20) // (8 * S))
+
+    def rows(i0, n):
+        dst = None if out is None else out[i0:i0 + n]
+        return E.world_arrivals(m, 0, i0, ev.x[i0:i0 + n], ev.t[i0:i0 + n], threads, out=dst)
+    eng.set_hypothesis_streamed(ev.ids, ev.x, ev.t, rows, chunk=chunk)
 
 
 def sampler_for(c, seed, epochs=1, algorithm="chromatic"):
@@ -321,7 +349,11 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--k", type=int, default=0,
                     help="override steps per region per sweep")
-    ap.add_argument("--capacity", type=int, default=0, help="event capacity (default 2N + 256)")
+    ap.add_argument("--capacity", type=int, default=0,
+                    help="event capacity (default 2N + 256; 16N + 4096 for configs 3/4)")
+    ap.add_argument("--storage", default="", choices=["", "rows", "compact"],
+                    help="arrival storage (default: the engine's choice, compact when the "
+                         "pool cannot hold two stored rows per event)")
     ap.add_argument("--start", default="truth", choices=["truth", "empty"],
                     help="truth: steady state from the world's events (default); empty: the "
                          "reference's own start (samplers.hpp:409), the chain evolving over "
@@ -343,11 +375,18 @@ def main():
         raise SystemExit("bench.py needs a GPU (the engine has no CPU fallback)")
     torch.cuda.set_device(local)
     threads = os.cpu_count() or 1
-    m, ev, sig = make_world(c, threads)
+    big = huge(c)
+    t_gen = time.perf_counter()
+    m, ev, sig = make_world(c, threads, streamed=big)
+    t_gen = time.perf_counter() - t_gen
     naive = args.algorithm == "naive"
     start = "empty" if naive else args.start
-    cap = args.capacity or int(max(1024, ev.N * 2 + 256))
+    # configs 3/4 at their k: the hypothesis swings far above the truth's
+    # count, so room for 16 N events
+    cap = args.capacity or int(max(1024, (16 * ev.N + 4096) if big else (ev.N * 2 + 256)))
     eng = E.Engine(m, sig, event_capacity=cap)
+    if args.storage:
+        eng.arrival_storage = args.storage
     truth = E.Events(ev.ids, ev.x, ev.t, ev.arrivals)
     empty = E.Events(np.zeros(0, np.uint64), np.zeros(0), np.zeros(0), np.zeros((0, c["S"])))
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
@@ -359,7 +398,7 @@ def main():
                                  row_cap=4)
 
     if start == "truth":
-        eng.set_hypothesis(truth)
+        load_truth(E, eng, m, ev, threads)
     # warm-up: W sweeps (one call per sweep for the L2-resident configs)
     if per_sweep:
         for i in range(args.warmup):
@@ -385,6 +424,7 @@ def main():
         acc["spec"] += st["speculative_discarded"]
         acc["phases"] += st["phases"]
         acc["final_events"] = st["final_events"]
+        acc["gen"] = st["generated_versions"]
 
     barrier(dist)
     torch.cuda.synchronize()
@@ -415,6 +455,12 @@ def main():
                    "scored_proposals_per_s": reduce_sum(dist, acc["scored"]) / (t_max / 1e3),
                    "parallelism": "replicas" if ws > 1 else "single",
                    "events": int(ev.N), "final_events": int(acc.get("final_events", 0)),
+                   "event_capacity": cap, "arrival_storage": eng.arrival_storage,
+                   "pool_slots": int(eng.pool_slots),
+                   "generated_versions_after": int(acc.get("gen", 0)),
+                   "world_generation_s": t_gen,
+                   "world_generation": "streamed (no N x S arrival matrix on the host)"
+                                       if big else "in memory",
                    "timing": ("one call per sweep, L2 flushed between timed sweeps (256 MiB "
                               "write)" if per_sweep else
                               f"one call of {args.steps} epochs; inputs larger than L2 "
@@ -450,22 +496,34 @@ def main():
         p_in.ids[...] = truth.ids
         p_in.x[...] = truth.x
         p_in.t[...] = truth.t
-        p_in.arrivals[...] = truth.arrivals
-        ocap = min(cap, 2 * ev.N + 1024)
+        if truth.arrivals is not None:
+            p_in.arrivals[...] = truth.arrivals
+        else:  # streamed world: the truth's arrivals generated into the pinned buffer
+            ch = max(1, (512 << 20) // (8 * S_))
+            for i0 in range(0, ev.N, ch):
+                n_ = min(ch, ev.N - i0)
+                E.world_arrivals(m, 0, i0, ev.x[i0:i0 + n_], ev.t[i0:i0 + n_], threads,
+                                 out=p_in.arrivals[i0:i0 + n_])
+        # the result read back every step: the final hypothesis with its
+        # arrivals (configs 0-2), or its events (id, x, t) for the streamed
+        # configs, whose arrivals stay on the device
+        out_arr = not big
+        ocap = min(cap, 2 * ev.N + 1024) if out_arr else cap
         p_out = E.Events(pinned((ocap,), np.uint64), pinned((ocap,), np.float64),
-                         pinned((ocap,), np.float64), pinned((ocap, S_), np.float64))
+                         pinned((ocap,), np.float64),
+                         pinned((ocap, S_), np.float64) if out_arr else None)
         h2d = sig.nbytes + ev.N * (24 + 8 * S_)
         d2h = 0
-        e2e_steps = max(3, min(args.steps, 10))
+        e2e_steps = max(3, min(args.steps, 10)) if not big else 3
 
         def e2e_step(i):
             eng.upload_signals(pin_np)
             eng.set_hypothesis(p_in)
             tr = run(seed0 + 500 + i, 1)
             try:
-                fin = eng.get_hypothesis(out=p_out)
+                fin = eng.get_hypothesis(arrivals=out_arr, out=p_out)
             except ValueError:  # the hypothesis outgrew the pinned buffer
-                fin = eng.get_hypothesis()
+                fin = eng.get_hypothesis(arrivals=out_arr)
             return tr.total_steps, len(fin.ids)
 
         e2e_step(-1)  # untimed: the engine's per-call scratch reaches its size
@@ -476,17 +534,21 @@ def main():
         for i in range(e2e_steps):
             n_steps, n_final = e2e_step(i)
             props += n_steps
-            d2h = n_final * (24 + 8 * S_)
+            d2h = n_final * (24 + (8 * S_ if out_arr else 0))
         torch.cuda.synchronize()
         wall = reduce_max(dist, time.perf_counter() - t0)
         res["e2e"] = {"value": reduce_sum(dist, props) / wall, "unit": "proposals/s",
                       "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                       "path": "seis_upload_signals + seis_set_hypothesis + seis_run_chromatic "
-                              "(one sweep) + seis_get_hypothesis, pinned host buffers, "
-                              "wall clock"}
+                              "(one sweep) + seis_get_hypothesis"
+                              + ("" if out_arr else " (id, x, t; arrivals stay on the device)")
+                              + ", pinned host buffers, wall clock"}
     if rank == 0 and ws == 1 and not args.no_cpu_baseline and start == "truth":
         from oracle import oracle as O
         if O.have_ref():
+            if ev.arrivals is None:  # streamed world: the truth's arrivals regenerated
+                ev = E.Events(ev.ids, ev.x, ev.t,
+                              E.world_arrivals(m, 0, 0, ev.x, ev.t, threads))
             ow = oracle_world(c, ev, sig)
             th = ref_threads(c, ev.N)
             r = cpu_baseline_ref(c, ow, args.cpu_seconds, th)

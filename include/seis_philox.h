@@ -25,6 +25,24 @@
  *            even) or w2w3 (i odd), so one Philox call feeds a station pair
  *            (birth: i = station j; location: 0 = x, 1 = t; arrival: 0;
  *            joint: 0..3)
+ *
+ * Arrival storage ("philox stream spec v2", seis_set_arrival_storage
+ * SEIS_ARR_COMPACT; spec v1 = SEIS_ARR_ROWS stores every version's S fp64
+ * arrivals and follows the reference's arithmetic, proposals.hpp:143-174):
+ *   birth at (x, t), step key (seed, sweep, region, step): a generated
+ *     version; arrival_j = arrival_mean(x, t, j) + sigma * (double) z_j with
+ *     z_j = seis_normal(seed, sweep, region, step, j) (the v1 birth values)
+ *   location / joint move of a generated version to (x', t'): generated,
+ *     same key and override; arrival_j = arrival_mean(x', t', j) + sigma z_j
+ *     (+ override): the residual is kept exactly instead of the reference's
+ *     a + (m' - m), which differs from it only by rounding
+ *   arrival move (station s, delta d) of a generated version without an
+ *     override: generated, override (s, d): arrival_s = (mean_s + sigma z_s) + d
+ *     (the v1 value a_s + d); with an override already: the version becomes a
+ *     stored row (its current arrivals, a_s + d at s), v1 rules from then on
+ *   stored rows (a loaded hypothesis, materialised versions): v1 rules
+ * The CPU oracle (oracle/seis_oracle.c, so_sampler.compact) implements the
+ * same rules; tests/test_gpu_compact.py checks production runs bit-exactly.
  */
 #ifndef SEIS_PHILOX_H
 #define SEIS_PHILOX_H
