@@ -143,9 +143,11 @@ int seis_engine_create(const seis_model_cfg* cfg, const double* stations, int64_
                        int64_t event_capacity, seis_engine** out);
 void seis_engine_destroy(seis_engine* eng);
 
-/* Arrival-version slots the engine allocated: min(2 * event_capacity + 2048,
- * what fits in free HBM less 4 GiB), never below event_capacity. A phase needs
- * the live events plus the phase-start versions it replaced. */
+/* Stored arrival rows the engine allocated: min(2 * event_capacity + 2048,
+ * what fits in free HBM less a reserve). Rows-mode runs need the live events
+ * plus the phase-start versions they replaced; fewer rows than events of
+ * capacity select the compact storage by default (generated versions need no
+ * row). A loaded hypothesis is stored rows: at most this many events. */
 int64_t seis_engine_pool_slots(const seis_engine* eng);
 
 /* Arrival storage of the versions production runs create. SEIS_ARR_ROWS

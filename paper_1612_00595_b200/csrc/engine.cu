@@ -468,9 +468,11 @@ __global__ void __launch_bounds__(NTT, MINB)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int slot_idx = pa.slot_order ? pa.slot_order[blockIdx.x] : (int)blockIdx.x;
+  if (pa.retry_pass && pa.retry[slot_idx] == 0) return;  // not handed over: done
   if (tid == 0) {  // a CTA that stops on an error leaves nothing for the barrier
     pa.births_cnt[slot_idx] = 0;
     pa.diff_cnt[slot_idx] = 0;
+    if (pa.ovf.slot) pa.ovf.slot[slot_idx] = -1;
     if (pa.births_total) pa.births_total[slot_idx] = 0;
   }
   const int region = pa.naive ? slot_idx : pa.color + slot_idx * sp.ncol;
@@ -542,6 +544,13 @@ __global__ void __launch_bounds__(NTT, MINB)
     __syncthreads();
   }
   if (s_nown > CAP) {
+    if (!kBig && pa.retry) {  // rerun by the whole-chain variant
+      if (tid == 0) {
+        pa.retry_free[(size_t)slot_idx * kRetryFree] = 0;
+        pa.retry[slot_idx] = 1;
+      }
+      return;
+    }
     if (tid == 0) set_err(ctl, ERR_OWN_OVERFLOW);
     return;
   }
@@ -588,6 +597,11 @@ __global__ void __launch_bounds__(NTT, MINB)
   if (tid == 0) {
     nown = nstart;
     np = nlfree = 0;
+    if (pa.retry_pass) {  // the slots the region kernel's attempt took
+      const int* rf = pa.retry_free + (size_t)slot_idx * kRetryFree;
+      for (int k2 = 0; k2 < rf[0]; ++k2) lfree[nlfree++] = rf[1 + k2];
+      pa.retry[slot_idx] = 0;
+    }
     n_local = N;
     births = n_acc = n_scored = n_arr = n_changed = n_spec = 0;
     for (int q = 0; q < 6; ++q) tprof[q] = 0;
@@ -975,6 +989,22 @@ __global__ void __launch_bounds__(NTT, MINB)
           }
         }
         if (ok && P.na >= 1 && nown - P.nr + P.na > CAP) {
+          if (!kBig && pa.retry) {
+            // hand the region to the whole-chain variant, with every version
+            // slot this chain took (the rerun reuses them first)
+            int* rf = pa.retry_free + (size_t)slot_idx * kRetryFree;
+            int nrf = 0;
+            for (int a = 0; a < P.na; ++a)
+              if (!P.inplace[a]) rf[1 + nrf++] = P.dslot[a];
+            for (int j = 0; j < nown; ++j)
+              if (own[j].sidx < 0) rf[1 + nrf++] = own[j].slot;
+            for (int k2 = 0; k2 < nlfree; ++k2) rf[1 + nrf++] = lfree[k2];
+            rf[0] = nrf;
+            pa.retry[slot_idx] = 1;
+            s_abort = 1;
+            adv = q + 1;
+            break;
+          }
           set_err(ctl, ERR_OWN_OVERFLOW);
           ok = false;
         }
@@ -1196,7 +1226,18 @@ __global__ void __launch_bounds__(NTT, MINB)
       }
     }
     // births alive at phase end, sorted by id
-    OutEv* bo = pa.births + (size_t)slot_idx * CAP;  // (serial: one slot)
+    // a rerun region writes past MAXOWN / MAXDOUT: an overflow area
+    if (kBig && pa.retry_pass && pa.ovf.slot) {
+      const int k = atomicAdd(pa.ovf.count, 1);
+      if (k >= kOvfRegions) {
+        set_err(ctl, ERR_OWN_OVERFLOW);
+        pa.births_cnt[slot_idx] = 0;
+        pa.diff_cnt[slot_idx] = 0;
+        return;  // (thread 0 alone from here on)
+      }
+      pa.ovf.slot[slot_idx] = k;
+    }
+    OutEv* bo = pa.births + births_off(pa.ovf, pa.n_slots, slot_idx);
     int nb = 0;
     for (int j = 0; j < nown; ++j)
       if (own[j].id >= pa.next_base) {
@@ -1222,7 +1263,7 @@ __global__ void __launch_bounds__(NTT, MINB)
     // coverage diff for the commit, then this-phase versions that died (sign
     // 0): k_commit returns those slots to the pool, after every CTA of this
     // phase has stopped popping from it
-    DiffPair* dout = pa.diff + (size_t)slot_idx * (3 * CAP);  // (serial: one slot)
+    DiffPair* dout = pa.diff + diff_off(pa.ovf, pa.n_slots, slot_idx);
     for (int q = 0; q < np; ++q) {
       dout[q].old_slot = pold[q];
       dout[q].new_slot = pnew[q];
@@ -1263,13 +1304,14 @@ inline dim3 commit_grid(int ncr, int n_sm) {
   return dim3((unsigned)ncr, (unsigned)split);
 }
 __device__ __forceinline__ void commit_body(const Dev& d, int color, int ncol, int nreg,
-                                            const int* diff_cnt, const DiffPair* diff,
-                                            int* free_stack, Ctl* ctl) {
+                                            int n_slots, const int* diff_cnt,
+                                            const DiffPair* diff, Ovf ovf, int* free_stack,
+                                            Ctl* ctl) {
   const int slot_idx = blockIdx.x;
   const int region = color + slot_idx * ncol;
   if (region >= nreg) return;
   const int nd = diff_cnt[slot_idx];
-  const DiffPair* de = diff + (size_t)slot_idx * MAXDOUT;
+  const DiffPair* de = diff + diff_off(ovf, n_slots, slot_idx);
   const double2* pool2 = reinterpret_cast<const double2*>(d.pool);
   // (diff entry, station pair) items over the whole CTA: a region's few
   // entries x P2 pairs, so every thread has work even when P2 is small
@@ -1342,9 +1384,9 @@ __device__ __forceinline__ void commit_body(const Dev& d, int color, int ncol, i
     }
 }
 
-__global__ void k_commit(Dev d, int color, int ncol, int nreg, const int* diff_cnt,
-                         const DiffPair* diff, int* free_stack, Ctl* ctl) {
-  commit_body(d, color, ncol, nreg, diff_cnt, diff, free_stack, ctl);
+__global__ void k_commit(Dev d, int color, int ncol, int nreg, int n_slots, const int* diff_cnt,
+                         const DiffPair* diff, Ovf ovf, int* free_stack, Ctl* ctl) {
+  commit_body(d, color, ncol, nreg, n_slots, diff_cnt, diff, ovf, free_stack, ctl);
 }
 
 // block-wide exclusive scan of one int per thread (any block size that is a
@@ -1385,7 +1427,7 @@ __device__ __forceinline__ void rebuild_body(Table in, Table out, int cap, int s
                                              const double* fate_x, const double* fate_t,
                                              const int* fate_slot, int n_slots,
                                              const int* births_cnt, const OutEv* births,
-                                             Ctl* ctl) {
+                                             Ovf ovf, Ctl* ctl) {
   const int N = ctl->n_events;
   int base = 0;
   for (int c0 = 0; c0 < N; c0 += blockDim.x) {
@@ -1414,7 +1456,7 @@ __device__ __forceinline__ void rebuild_body(Table in, Table out, int cap, int s
     int tot;
     const int pos = base + block_scan_excl(nb, &tot);
     for (int b = 0; b < nb; ++b) {
-      const OutEv& e = births[(size_t)s * MAXOWN + b];
+      const OutEv& e = births[births_off(ovf, n_slots, s) + b];
       if (pos + b < cap) {
         out.id[pos + b] = e.id;
         out.x[pos + b] = e.x;
@@ -1427,6 +1469,7 @@ __device__ __forceinline__ void rebuild_body(Table in, Table out, int cap, int s
   if (threadIdx.x == 0) {
     if (base > cap) set_err(ctl, ERR_TABLE_OVERFLOW);
     ctl->n_events = min(base, cap);
+    if (ovf.count) *ovf.count = 0;  // the next phase's overflow areas
   }
 }
 
@@ -1435,9 +1478,9 @@ __global__ void __launch_bounds__(1024) k_rebuild(Table in, Table out, int cap, 
                                                   const double* fate_x, const double* fate_t,
                                                   const int* fate_slot, int n_slots,
                                                   const int* births_cnt, const OutEv* births,
-                                                  Ctl* ctl) {
+                                                  Ovf ovf, Ctl* ctl) {
   rebuild_body(in, out, cap, stamp, fate_stamp, fate_alive, fate_x, fate_t, fate_slot, n_slots,
-               births_cnt, births, ctl);
+               births_cnt, births, ovf, ctl);
 }
 
 // The color barrier in one launch: the commit CTAs (grid.x < ncr) and, in the
@@ -1447,14 +1490,14 @@ __global__ void __launch_bounds__(kCommitThreads) k_barrier(Dev d, int color, in
                           const DiffPair* diff, int* free_stack, Ctl* ctl, Table in, Table out,
                           int cap, int stamp, const int* fate_stamp, const int* fate_alive,
                           const double* fate_x, const double* fate_t, const int* fate_slot,
-                          int n_slots, const int* births_cnt, const OutEv* births) {
+                          int n_slots, const int* births_cnt, const OutEv* births, Ovf ovf) {
   if (blockIdx.x == gridDim.x - 1) {
     if (blockIdx.y == 0)
       rebuild_body(in, out, cap, stamp, fate_stamp, fate_alive, fate_x, fate_t, fate_slot,
-                   n_slots, births_cnt, births, ctl);
+                   n_slots, births_cnt, births, ovf, ctl);
     return;
   }
-  commit_body(d, color, ncol, nreg, diff_cnt, diff, free_stack, ctl);
+  commit_body(d, color, ncol, nreg, n_slots, diff_cnt, diff, ovf, free_stack, ctl);
 }
 
 // ----------------------------------------------------------------- score batch
@@ -1927,7 +1970,7 @@ Ctl read_ctl(seis_engine* e) {
 
 const char* err_name(int e) {
   switch (e) {
-    case ERR_OWN_OVERFLOW: return "a region exceeded the per-region event limit (64; run_serial: 1024)";
+    case ERR_OWN_OVERFLOW: return "a region chain exceeded 1024 events (the per-chain event limit)";
     case ERR_POOL_EXHAUSTED: return "arrival pool exhausted (live events + replaced versions > pool slots): raise event_capacity";
     case ERR_TAPE_UNKNOWN_ID: return "replay tape names an event the region does not hold";
     case ERR_TABLE_OVERFLOW: return "event table overflow: raise event_capacity";
@@ -1965,7 +2008,7 @@ namespace {
 template <typename YT, int MODE>
 void launch_phase_t(seis_engine* e, int ncr, const Samp& sp, const PhaseArgs& pa, int stamp) {
   const bool rows_only = MODE == 0 && !pa.serial && !e->compact && !e->gen_present;
-  if (pa.serial)
+  if (pa.serial || pa.retry_pass)
     k_phase<YT, MODE, NT, SEIS_MINB, kSerialCap, true>
         <<<ncr, NT, kPhaseSmemSerial, e->stream>>>(e->d, sp, pa, e->ctl, stamp);
   else if (MODE == 0 && rows_only)
@@ -2053,15 +2096,17 @@ int seis_engine_create(const seis_model_cfg* cfg, const double* stations, int64_
       const size_t reserve = std::max<size_t>((size_t)6 << 30, total_b / 16);
       const size_t fit = free_b > reserve ? (free_b - reserve) / per : 0;
       const size_t want = 2 * (size_t)e->cap + 2048;
-      size_t slots = std::min<size_t>(want, std::max<size_t>(fit, (size_t)e->cap));
+      // may hold fewer rows than event_capacity: the engine then defaults to
+      // the compact storage (generated versions need no row)
+      size_t slots = std::max<size_t>(std::min<size_t>(want, fit), std::min<size_t>(want, 64));
       // SEIS_POOL_SLOTS (tests): a smaller pool, to exercise exhaustion
       if (const char* ov = getenv("SEIS_POOL_SLOTS"))
-        slots = std::max<size_t>((size_t)e->cap, std::min<size_t>(slots, (size_t)atoll(ov)));
+        slots = std::max<size_t>(1, std::min<size_t>(slots, (size_t)atoll(ov)));
       void* p = nullptr;
       while (cudaMalloc(&p, slots * per) != cudaSuccess) {
         (void)cudaGetLastError();
-        if (slots <= (size_t)e->cap) throw std::runtime_error("cudaMalloc: arrival pool out of memory");
-        slots = std::max<size_t>((size_t)e->cap, slots - slots / 8);
+        if (slots <= 64) throw std::runtime_error("cudaMalloc: arrival pool out of memory");
+        slots -= slots / 8;
       }
       e->pool_slots = (int)slots;
       e->pool = static_cast<double*>(p);
@@ -2199,6 +2244,9 @@ int hyp_begin(seis_engine* e, int64_t N, const uint64_t* ids, const double* x, c
   return guarded([&] {
     e->load_n = -1;
     if (N < 0 || N > e->cap) throw std::invalid_argument("hypothesis larger than event_capacity");
+    if (N > e->pool_slots)
+      throw std::invalid_argument("hypothesis rows exceed the arrival pool (" +
+                                  std::to_string(e->pool_slots) + " rows fit in HBM)");
     std::vector<int64_t> order(N);
     for (int64_t i = 0; i < N; ++i) order[i] = i;
     std::sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return ids[a] < ids[b]; });
@@ -2714,15 +2762,31 @@ static int run_driver(seis_engine* e, const seis_sampler_cfg* sc, int32_t mode,
     }
     // per-slot outputs: MAXOWN births / MAXDOUT diff entries per region; the
     // serial chain's one slot holds kSerialCap / 3 kSerialCap
-    const int cap_own = serial ? kSerialCap : MAXOWN;
-    OutEv* births = static_cast<OutEv*>(alloc((size_t)n_slots * cap_own * sizeof(OutEv)));
+    // (region slots: + kOvfRegions overflow areas for chains rerun past MAXOWN)
+    const size_t n_births =
+        serial ? (size_t)kSerialCap : (size_t)n_slots * MAXOWN + (size_t)kOvfRegions * kSerialCap;
+    const size_t n_diff = serial ? (size_t)3 * kSerialCap
+                                 : (size_t)n_slots * MAXDOUT + (size_t)kOvfRegions * 3 * kSerialCap;
+    OutEv* births = static_cast<OutEv*>(alloc(n_births * sizeof(OutEv)));
     int* diff_cnt = static_cast<int*>(alloc((size_t)n_slots * 4));
-    DiffPair* diff =
-        static_cast<DiffPair*>(alloc((size_t)n_slots * 3 * cap_own * sizeof(DiffPair)));
+    DiffPair* diff = static_cast<DiffPair*>(alloc(n_diff * sizeof(DiffPair)));
+    Ovf ovf{nullptr, nullptr};
+    if (!serial) {
+      ovf.slot = static_cast<int*>(alloc((size_t)n_slots * 4));
+      ovf.count = static_cast<int*>(alloc(4));
+      ck(cudaMemsetAsync(ovf.count, 0, 4, e->stream), "memset");
+    }
     // cost-ordered dispatch (k_order); SEIS_ORDER=0 disables it (A/B)
     const bool use_order = !serial && !(getenv("SEIS_ORDER") && atoi(getenv("SEIS_ORDER")) == 0);
     int* order_cnt = static_cast<int*>(alloc((size_t)n_slots * 4));
     int* order = static_cast<int*>(alloc((size_t)n_slots * 4));
+    int* retry = nullptr;
+    int* retry_free = nullptr;
+    if (!serial) {
+      retry = static_cast<int*>(alloc((size_t)n_slots * 4));
+      retry_free = static_cast<int*>(alloc((size_t)n_slots * kRetryFree * 4));
+      ck(cudaMemsetAsync(retry, 0, (size_t)n_slots * 4, e->stream), "memset");
+    }
     seis_tape_step* d_tape = nullptr;
     double* d_tarr = nullptr;
     seis_step_out* d_out = nullptr;
@@ -2848,7 +2912,16 @@ static int run_driver(seis_engine* e, const seis_sampler_cfg* sc, int32_t mode,
         pa.slot_order = order;
         ++launches;
       }
+      pa.retry = retry;
+      pa.retry_free = retry_free;
+      pa.ovf = ovf;
       launch_phase(e, mode, ncr, spk, pa, stamp);
+      if (retry) {  // regions that outgrew the region kernel's chain arrays
+        PhaseArgs pr = pa;
+        pr.retry_pass = 1;
+        launch_phase(e, mode, ncr, spk, pr, stamp);
+        ++launches;
+      }
       if (timing) {
         ck(cudaEventRecord(b, e->stream), "event");
         phase_ev.emplace_back(a, b);
@@ -2860,7 +2933,7 @@ static int run_driver(seis_engine* e, const seis_sampler_cfg* sc, int32_t mode,
       k_barrier<<<bg, kCommitThreads, 0, e->stream>>>(
           e->d, color, std::max(ncol, 1), nreg, diff_cnt, diff, e->free_stack, e->ctl,
           e->tab[e->cur], e->tab[nxt], e->cap, stamp, e->fate_stamp, e->fate_alive, e->fate_x,
-          e->fate_t, e->fate_slot, ncr, births_cnt, births);
+          e->fate_t, e->fate_slot, ncr, births_cnt, births, ovf);
       ck(cudaGetLastError(), "k_barrier");
       launches += 2;
       if (!serial)  // Trace::phases, one record per committed region (samplers.hpp:479)
@@ -3084,9 +3157,13 @@ extern "C" int seis_run_naive(seis_engine* e, const seis_sampler_cfg* sc, int32_
     sp.ncol = 1;
     sp.mspec = spec_depth();
     int* births_cnt = static_cast<int*>(alloc((size_t)nreg * 4));
-    OutEv* births = static_cast<OutEv*>(alloc((size_t)nreg * MAXOWN * sizeof(OutEv)));
+    OutEv* births = static_cast<OutEv*>(alloc(
+        ((size_t)nreg * MAXOWN + (size_t)kOvfRegions * kSerialCap) * sizeof(OutEv)));
     int* diff_cnt = static_cast<int*>(alloc((size_t)nreg * 4));
-    DiffPair* diff = static_cast<DiffPair*>(alloc((size_t)nreg * MAXDOUT * sizeof(DiffPair)));
+    DiffPair* diff = static_cast<DiffPair*>(alloc(
+        ((size_t)nreg * MAXDOUT + (size_t)kOvfRegions * 3 * kSerialCap) * sizeof(DiffPair)));
+    Ovf ovf{static_cast<int*>(alloc((size_t)nreg * 4)), static_cast<int*>(alloc(4))};
+    ck(cudaMemsetAsync(ovf.count, 0, 4, e->stream), "memset");
     seis_tape_step* d_tape = nullptr;
     double* d_tarr = nullptr;
     seis_step_out* d_out = nullptr;
@@ -3141,16 +3218,27 @@ extern "C" int seis_run_naive(seis_engine* e, const seis_sampler_cfg* sc, int32_
     ck(cudaEventCreate(&evp1), "event");
     ck(cudaEventRecord(ev0, e->stream), "event");
     ck(cudaEventRecord(evp0, e->stream), "event");
+    int* retry = static_cast<int*>(alloc((size_t)nreg * 4));
+    int* retry_free = static_cast<int*>(alloc((size_t)nreg * kRetryFree * 4));
+    ck(cudaMemsetAsync(retry, 0, (size_t)nreg * 4, e->stream), "memset");
+    pa.retry = retry;
+    pa.retry_free = retry_free;
+    pa.ovf = ovf;
     launch_phase(e, mode, nreg, sp, pa, stamp);
+    {  // regions that outgrew the region kernel's chain arrays
+      PhaseArgs pr = pa;
+      pr.retry_pass = 1;
+      launch_phase(e, mode, nreg, sp, pr, stamp);
+    }
     ck(cudaEventRecord(evp1, e->stream), "event");
     ck(cudaGetLastError(), "k_phase (naive)");
     // the union: coverage of every region's events, table of all births
-    k_commit<<<commit_grid(nreg, e->n_sm), kCommitThreads, 0, e->stream>>>(e->d, 0, 1, nreg, diff_cnt, diff, e->free_stack,
-                                          e->ctl);
+    k_commit<<<commit_grid(nreg, e->n_sm), kCommitThreads, 0, e->stream>>>(
+        e->d, 0, 1, nreg, nreg, diff_cnt, diff, ovf, e->free_stack, e->ctl);
     const int nxt = e->cur ^ 1;
     k_rebuild<<<1, 1024, 0, e->stream>>>(e->tab[e->cur], e->tab[nxt], e->cap, stamp,
                                           e->fate_stamp, e->fate_alive, e->fate_x, e->fate_t,
-                                          e->fate_slot, nreg, births_cnt, births, e->ctl);
+                                          e->fate_slot, nreg, births_cnt, births, ovf, e->ctl);
     ck(cudaGetLastError(), "naive commit");
     e->cur = nxt;
     // the union's final snapshot (samplers.hpp:388-391 at the last checkpoint;
@@ -3211,7 +3299,7 @@ extern "C" int seis_run_naive(seis_engine* e, const seis_sampler_cfg* sc, int32_
       stats->sweep_kernel_ms = ms;
       ck(cudaEventElapsedTime(&ms, ev0, ev1), "elapsed");
       stats->total_ms = ms;
-      stats->kernel_launches = 3 + (sc->record_log_joint ? 3 : 0);
+      stats->kernel_launches = 4 + (sc->record_log_joint ? 3 : 0);
       stats->n_rows = n_cp;
       stats->phases = 1;
       stats->generated_versions = (int64_t)e->gv_cap - c.gv_top;

@@ -52,6 +52,25 @@ template <int CAP>
 struct ChainSmem {  // bytes of the chain arrays (own, st, pold, pnew, lfree, cur_of, log i)
   static constexpr int bytes = CAP * (32 + 24 + 4 + 4) + 2 * CAP * 8 + (CAP + 8) * 8;
 };
+constexpr int kRetryFree = 3 * MAXOWN;  // version slots a region chain can hand to its rerun
+constexpr int kOvfRegions = 512;        // reruns per phase with outputs past MAXOWN / MAXDOUT
+
+// Per-slot phase outputs (births alive at the end, diff entries): region
+// slots at stride MAXOWN / MAXDOUT; a rerun region (whole-chain variant)
+// writes to one of kOvfRegions overflow areas of kSerialCap / 3 kSerialCap
+// after them, its index in slot[s] (-1: the regular area)
+struct Ovf {
+  int* slot;   // [n_slots] (null: no overflow areas, e.g. the serial chain)
+  int* count;  // overflow areas handed out this phase (reset by the barrier)
+};
+__host__ __device__ __forceinline__ size_t births_off(const Ovf& o, int n_slots, int s) {
+  const int k = o.slot ? o.slot[s] : -1;
+  return k < 0 ? (size_t)s * MAXOWN : (size_t)n_slots * MAXOWN + (size_t)k * kSerialCap;
+}
+__host__ __device__ __forceinline__ size_t diff_off(const Ovf& o, int n_slots, int s) {
+  const int k = o.slot ? o.slot[s] : -1;
+  return k < 0 ? (size_t)s * MAXDOUT : (size_t)n_slots * MAXDOUT + (size_t)k * 3 * kSerialCap;
+}
 constexpr int TBL = 512;         // coverage counts whose {dL, dI} rows live in smem
 constexpr int kDiffCache = 2048;  // stations whose round diff windows k_phase caches in smem
 constexpr int kRowPad = 32;      // zero rows appended to y and cov (unpredicated chunk loads)
@@ -186,6 +205,15 @@ struct PhaseArgs {
   long long step_base;             // chain step of this launch's first step
   int* births_total;               // [n_slots] accepted births of the phase (may be null)
   unsigned long long* order_io;    // serial: [0] count, [1..] ids in list order (may be null)
+  // regions outgrowing the MAXOWN chain arrays: the region kernel hands the
+  // slot (and every version slot its chain took, retry_free[slot][0] = count)
+  // to a second launch of the whole-chain variant (kSerialCap events), which
+  // reruns the chain from the phase-start state (retry_pass = 1: only
+  // flagged slots run); the counter-based stream makes the rerun identical
+  int* retry;
+  int* retry_free;
+  int retry_pass;
+  Ovf ovf;
   // dispatch order: CTA b runs region slot slot_order[b] (k_order: slots with
   // more phase-start events first, so the cheap event-free chains fill the
   // last wave); null = identity

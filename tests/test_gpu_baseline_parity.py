@@ -530,3 +530,41 @@ def test_c2_serial_vs_chromatic_mapped_shape(E):
     detail = {k: (round(v.mean, 3), round(v.lo, 3), round(v.hi, 3)) for k, v in ci.items()}
     print(detail)
     assert _overlap(sp, dp) and _overlap(sr, dr), detail
+
+
+# ------------------------------------------------------------------ regions past 64 events
+@pytest.mark.parametrize("n_ev", [230, 420])
+def test_region_chains_past_64_events_production(E, n_ev):
+    """a region chain holds no fixed 64-event limit: the region kernel hands a
+    region whose events outgrow its arrays (at the phase start, 420 events in
+    4 regions, or mid-chain by births, 230) to the whole-chain variant, which
+    reruns it from the phase-start state; every decision, delta and the final
+    hypothesis against the oracle (the reference has no per-region limit,
+    samplers.hpp:445-463)"""
+    oc = O.Oracle("c")
+    m = O.Model(lambda_rate=n_ev / 240.0)
+    w = oc.sample_world(m, 31)
+    s = O.Sampler(steps_per_epoch=300, epochs=2, n_regions=4, seed=4, dynamic=1, rng_mode=1,
+                  record_every=1 << 30)
+    ro = oc.run_chromatic(w, s, init=w.events, tape=True)
+    eng = E.Engine(engine_model(m), w.signals, event_capacity=4096)
+    eng.set_hypothesis(_ev(E, w.events))
+    tr = eng.run_chromatic(engine_sampler(s), decisions=len(ro["tape"]))
+    so, t = tr.step_out, ro["tape"]
+    assert np.array_equal(so["accepted"], t["accepted"])
+    sc = (t["scored"] == 1) & np.isfinite(t["delta"])
+    assert np.allclose(so["delta"][sc], t["delta"][sc], rtol=1e-11, atol=1e-9)
+    assert np.array_equal(tr.final.ids, ro["final"].ids)
+    assert np.array_equal(tr.final.arrivals, ro["final"].arr)
+    per_region = np.bincount(np.minimum((w.events.t / 60.0).astype(int), 3), minlength=4)
+    assert per_region.max() > 50
+
+
+def test_region_chains_past_64_events_reference_replay(E, ref):
+    m = O.Model(lambda_rate=420 / 240.0)
+    w = ref.sample_world(m, 32)
+    s = O.Sampler(steps_per_epoch=200, epochs=2, n_regions=4, seed=2, dynamic=1,
+                  record_every=1 << 30)
+    r = ref.run_chromatic(w, s, init=w.events, tape=True)
+    _replay(E, m, w, r["tape"], r["tape_arr"], s, r["final"], init=w.events, dtype=np.float64,
+            cap=4096)

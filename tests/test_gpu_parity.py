@@ -516,7 +516,7 @@ def test_capacity_and_region_limits_fail_loudly(E, oc):
     assert many.events.N > 1024
     eng2 = E.Engine(engine_model(many.model), many.signals, event_capacity=2048)
     eng2.set_hypothesis(E.Events(many.events.ids, many.events.x, many.events.t, many.events.arr))
-    with pytest.raises(RuntimeError, match="per-region event limit"):
+    with pytest.raises(RuntimeError, match="per-chain event limit"):
         eng2.run_chromatic(E.SamplerConfig(algorithm="serial", steps_per_epoch=10, epochs=1))
 
 
