@@ -36,10 +36,12 @@
  *     same key and override; arrival_j = arrival_mean(x', t', j) + sigma z_j
  *     (+ override): the residual is kept exactly instead of the reference's
  *     a + (m' - m), which differs from it only by rounding
- *   arrival move (station s, delta d) of a generated version without an
- *     override: generated, override (s, d): arrival_s = (mean_s + sigma z_s) + d
- *     (the v1 value a_s + d); with an override already: the version becomes a
- *     stored row (its current arrivals, a_s + d at s), v1 rules from then on
+ *   arrival move (station s, delta d) of a generated version with fewer
+ *     than 8 overrides: generated, override (s, d) appended; arrival_j =
+ *     (mean_j + sigma z_j) + the deltas of the overrides at j in acceptance
+ *     order (the v1 values a_s + d); with 8 overrides already: the version
+ *     becomes a stored row (its current arrivals, a_s + d at s), v1 rules
+ *     from then on
  *   stored rows (a loaded hypothesis, materialised versions): v1 rules
  * The CPU oracle (oracle/seis_oracle.c, so_sampler.compact) implements the
  * same rules; tests/test_gpu_compact.py checks production runs bit-exactly.

@@ -523,15 +523,17 @@ void so_signal_window(double lo, double hi, double tau, double T, double rate, i
 /* an event version; gen = 1: a generated version of arrival storage spec v2
  * (include/seis_philox.h): its arrivals are arrival_mean(x, t, j) + sigma z_j
  * with z_j the philox normal of its birth (key gseed, counter gsweep / gregion
- * / gstep), plus ovr_d at station ovr_st; `a` always holds those values */
+ * / gstep), plus its overrides (ovr_d[k] at station ovr_st[k], in order);
+ * `a` always holds those values */
 typedef struct {
   uint64_t id;
   double x, t;
   double* a;
-  int gen, ovr_st;
+  int gen, n_ovr;
   uint64_t gseed;
   uint32_t gsweep, gregion, gstep, pad_;
-  double ovr_d;
+  int ovr_st[8]; /* kGenOvr overrides, in acceptance order */
+  double ovr_d[8];
 } ev_t;
 
 typedef struct {
@@ -722,7 +724,8 @@ static ev_t shifted(const so_model* m, const ev_t* before, double nx, double nt)
                    m->sigma_arrival * (double)seis_normal(before->gseed, before->gsweep,
                                                          before->gregion, before->gstep,
                                                          (uint32_t)j);
-      if (j == before->ovr_st) after.a[j] = after.a[j] + before->ovr_d;
+      for (int k = 0; k < before->n_ovr; ++k)
+        if (before->ovr_st[k] == j) after.a[j] = after.a[j] + before->ovr_d[k];
     }
     return after;
   }
@@ -752,7 +755,6 @@ static void propose(chain_t* c, int type, const evlist_t* l, uint64_t new_id, in
       ev_t e;
       memset(&e, 0, sizeof e);
       e.id = new_id;
-      e.ovr_st = -1;
       if (sc->rng_mode == 1 && sc->compact) { /* spec v2: a generated version */
         e.gen = 1;
         e.gseed = sc->seed;
@@ -830,10 +832,11 @@ static void propose(chain_t* c, int type, const evlist_t* l, uint64_t new_id, in
       ev_t after = ev_copy(b, S);
       const double da = draw_normal(c, 0, 0.0, sc->step_arrival);
       after.a[st] += da;
-      if (b->gen) { /* spec v2: the first override stays generated, a second stores the row */
-        if (b->ovr_st < 0) {
-          after.ovr_st = (int)st;
-          after.ovr_d = da;
+      if (b->gen) { /* spec v2: up to 8 overrides stay generated, the next stores the row */
+        if (b->n_ovr < 8) {
+          after.ovr_st[after.n_ovr] = (int)st;
+          after.ovr_d[after.n_ovr] = da;
+          after.n_ovr++;
         } else {
           after.gen = 0;
         }
@@ -1067,7 +1070,6 @@ so_run* so_run_chromatic(const so_model* m, const double* signals, const so_samp
   for (int64_t i = 0; i < n_init; ++i) {
     ev_t e;
     memset(&e, 0, sizeof e);
-    e.ovr_st = -1;
     e.id = ids[i];
     e.x = x[i];
     e.t = t[i];
@@ -1464,7 +1466,6 @@ so_run* so_run_serial(const so_model* m, const double* signals, const so_sampler
   for (int64_t i = 0; i < n_init; ++i) {
     ev_t e;
     memset(&e, 0, sizeof e);
-    e.ovr_st = -1;
     e.id = ids[i];
     e.x = x[i];
     e.t = t[i];

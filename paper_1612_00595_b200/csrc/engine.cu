@@ -945,7 +945,7 @@ __global__ void __launch_bounds__(NTT, MINB)
               gen = pa.compact;
             } else {
               const int rs = P.rslot[a < P.nr ? a : 0];
-              if (rs < -1) gen = P.type == 3 ? (d.gv[-2 - rs].ovr_st < 0 ? 1 : 0) : 1;
+              if (rs < -1) gen = P.type == 3 ? (d.gv[-2 - rs].n_ovr < kGenOvr ? 1 : 0) : 1;
             }
           }
           P.dgen[a] = gen;
@@ -1129,13 +1129,13 @@ __global__ void __launch_bounds__(NTT, MINB)
             g.sweep = (unsigned)pa.epoch;
             g.region = (unsigned)region;
             g.step = (unsigned)step;
-            g.ovr_st = -1;
-            g.ovr_d = 0.0;
+            g.n_ovr = 0;
           } else {
-            g = load_gv(d, P.rslot[a]);  // (read before an in-place write)
+            g = *gv_of(d, P.rslot[a]);  // (read before an in-place write)
             if (P.type == 3) {
-              g.ovr_st = P.arr_st;
-              g.ovr_d = P.arr_da;
+              g.ovr_st[g.n_ovr] = P.arr_st;
+              g.ovr_d[g.n_ovr] = P.arr_da;
+              ++g.n_ovr;
             }
           }
           g.x = P.ax[a];

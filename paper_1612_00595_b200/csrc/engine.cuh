@@ -93,15 +93,24 @@ struct Win {
 // an event version is either a stored row of the arrival pool (slot >= 0) or
 // a generated version (slot = -2 - g, g indexing the GenV table): the arrival
 // at station j is computed, arrival_mean(x, t, j) + sigma z_j with z_j the
-// philox normal of the birth that created it, plus at most one per-station
-// override. Slot -1 means "no version" (a birth's start, a death's end).
+// philox normal of the birth that created it, plus up to kGenOvr per-station
+// overrides (accepted arrival moves). Slot -1 means "no version" (a birth's start, a death's end).
+constexpr int kGenOvr = 8;  // per-station arrival overrides a generated version keeps
 struct GenV {
   double x, t;                  // the version's location
   unsigned long long seed;      // the birth's philox key ...
   unsigned sweep, region, step; // ... and counter
-  int ovr_st;                   // station of the one override (-1: none)
-  double ovr_d;                 // its arrival delta
+  int n_ovr;                    // overrides, in the order the arrival moves were accepted
+  int ovr_st[kGenOvr];
+  double ovr_d[kGenOvr];
 };
+// (mean + sigma z) + the overrides at station j, in order
+__device__ __forceinline__ double gen_apply_ovr(const GenV* g, int j, double a) {
+  const int n = g->n_ovr;
+  for (int k = 0; k < n; ++k)
+    if (g->ovr_st[k] == j) a = a + g->ovr_d[k];
+  return a;
+}
 
 struct Dev {
   int S, S_pad, P2, n;
@@ -271,17 +280,17 @@ __device__ __forceinline__ double arrival_mean(const Dev& d, double x, double t,
 }
 
 // generated version's arrival at station j (spec v2): (mean + sigma z) [+ override]
-__device__ __forceinline__ double gen_arrival(const Dev& d, const GenV& g, int j, double mean) {
-  double a = mean + d.sigma * (double)seis_normal(g.seed, g.sweep, g.region, g.step, (uint32_t)j);
-  if (j == g.ovr_st) a = a + g.ovr_d;
-  return a;
+__device__ __forceinline__ double gen_arrival(const Dev& d, const GenV* g, int j, double mean) {
+  double a =
+      mean + d.sigma * (double)seis_normal(g->seed, g->sweep, g->region, g->step, (uint32_t)j);
+  return gen_apply_ovr(g, j, a);
 }
-__device__ __forceinline__ GenV load_gv(const Dev& d, int slot) { return d.gv[-2 - slot]; }
+__device__ __forceinline__ const GenV* gv_of(const Dev& d, int slot) { return d.gv + (-2 - slot); }
 // any version's arrival at station j (slot != -1)
 __device__ __forceinline__ double arr_of(const Dev& d, int slot, int j) {
   if (slot >= 0) return __ldg(d.pool + (size_t)slot * d.S_pad + j);
-  const GenV g = load_gv(d, slot);
-  return gen_arrival(d, g, j, arrival_mean(d, g.x, g.t, d.stations[j]));
+  const GenV* g = gv_of(d, slot);
+  return gen_arrival(d, g, j, arrival_mean(d, g->x, g->t, d.stations[j]));
 }
 
 // GEN = false: the kernel variant of runs that hold stored rows only (the

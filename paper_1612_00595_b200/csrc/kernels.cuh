@@ -555,10 +555,10 @@ __device__ __forceinline__ void station_item(const Dev& d, const Prop& P, const 
       if (!GEN || rs >= 0) {
         ra[q] = __ldg(d.pool + (size_t)rs * d.S_pad + j);
       } else {
-        const GenV g = load_gv(d, rs);
-        rz[q] = d.sigma * (double)seis_normal(g.seed, g.sweep, g.region, g.step, (uint32_t)j);
+        const GenV* g = gv_of(d, rs);
+        rz[q] = d.sigma * (double)seis_normal(g->seed, g->sweep, g->region, g->step, (uint32_t)j);
         ra[q] = mo + rz[q];
-        if (j == g.ovr_st) ra[q] = ra[q] + g.ovr_d;
+        ra[q] = gen_apply_ovr(g, j, ra[q]);
       }
       R.w[q] = clampw(make_win(d, ra[q]), in.wlo, in.whi);
       arr -= arr_logpdf(d, ra[q], mo);
@@ -578,9 +578,9 @@ __device__ __forceinline__ void station_item(const Dev& d, const Prop& P, const 
         if (!GEN || P.rslot[q] >= 0) {  // stored row: shift by the mean (proposals.hpp:153-157)
           aa = ra[q] + (m - arrival_mean(d, P.rx[q], P.rt[q], s));
         } else {  // generated version (spec v2): residual kept exactly
-          const GenV g = load_gv(d, P.rslot[q]);
+          const GenV* g = gv_of(d, P.rslot[q]);
           aa = m + rz[q];
-          if (j == g.ovr_st) aa = aa + g.ovr_d;
+          aa = gen_apply_ovr(g, j, aa);
         }
       } else {
         aa = in.rows[a][j];

@@ -1,8 +1,8 @@
 """GPU parity of the compact arrival storage ("philox stream spec v2",
 include/seis_philox.h): births of a production run and their location /
 joint moves are generated versions (location + philox key, arrivals computed
-as mean + sigma z), a first arrival move is a per-station override, a second
-one stores the row. The CPU oracle implements the same spec (so_sampler
+as mean + sigma z), arrival moves are per-station overrides (up to 8; the
+ninth stores the row). The CPU oracle implements the same spec (so_sampler
 compact = 1); every decision, delta, trace row (log_joint included), the
 final hypothesis with all its arrivals, and deltas scored against a
 hypothesis holding generated versions must match it."""
@@ -142,3 +142,19 @@ def test_compact_versions_scored_and_continued(E):
     s2 = O.Sampler(steps_per_epoch=100, epochs=3, n_regions=4, seed=6, dynamic=1, rng_mode=1)
     tr2 = eng.run_chromatic(engine_sampler(s2))
     assert tr2.total_steps > 0
+
+
+def test_compact_overrides_fill_and_materialise(E):
+    """arrival moves dominate: generated versions collect up to 8 overrides,
+    the ninth accepted arrival move stores the version as a row (spec v2);
+    both paths against the oracle, bit for bit"""
+    m = default_model()
+    w = golden_world("w1", m)
+    s = O.Sampler(steps_per_epoch=600, epochs=4, n_regions=4, seed=12, rng_mode=1,
+                  record_every=800, burn_in_fraction=0.0, compact=1,
+                  weights=(0.15, 0.05, 0.1, 0.6, 0.1))
+    eng, tr, ro = _run(E, m, w, s, algorithm="serial")
+    assert tr.total_accepted > 200
+    s2 = O.Sampler(steps_per_epoch=300, epochs=6, n_regions=4, seed=13, dynamic=1, rng_mode=1,
+                   record_every=1000, compact=1, weights=(0.15, 0.05, 0.1, 0.6, 0.1))
+    _run(E, m, w, s2)
