@@ -71,10 +71,27 @@ __host__ __device__ __forceinline__ size_t diff_off(const Ovf& o, int n_slots, i
   const int k = o.slot ? o.slot[s] : -1;
   return k < 0 ? (size_t)s * MAXDOUT : (size_t)n_slots * MAXDOUT + (size_t)k * 3 * kSerialCap;
 }
-constexpr int TBL = 512;         // coverage counts whose {dL, dI} rows live in smem
+#ifndef SEIS_TBL
+#define SEIS_TBL 512
+#endif
+constexpr int TBL = SEIS_TBL;    // coverage counts whose {dL, dI} rows live in smem
 constexpr int kDiffCache = 2048;  // stations whose round diff windows k_phase caches in smem
+constexpr int kTileFlags = 24576;  // station tiles whose diff flags the tile-major pass keeps
+// Tile-major pass: per warp, the next tile's station coordinates and arrival
+// rows (the round's first two diff pairs, the first removed version of each
+// of up to three proposals) are copied to shared memory with cp.async while
+// the warp scores the current tile (two buffers of kStageRows x 32 doubles)
+constexpr int kStageRows = 8;
+constexpr int kStageBytes = NW * 2 * kStageRows * 32 * 8;
+#ifndef SEIS_STAGE
+#define SEIS_STAGE 0
+#endif
+constexpr bool kStageOn = SEIS_STAGE;
 constexpr int kRowPad = 32;      // zero rows appended to y and cov (unpredicated chunk loads)
-constexpr int LOGIWIN = 1024;    // log(i) window around the phase-start event count
+#ifndef SEIS_LOGIWIN
+#define SEIS_LOGIWIN 1024
+#endif
+constexpr int LOGIWIN = SEIS_LOGIWIN;  // log(i) window around the phase-start event count
 constexpr int BANDMAX = 256;     // rows of the generic diff-correction scratch
 constexpr double kLog2Pi = 1.8378770664093454835606594728112;
 
@@ -124,6 +141,13 @@ struct Dev {
   const double* stations;          // [S_pad]
   const void* y;                   // [S_pad / 32][rows][32] (station tiles)
   uint32_t* cov;                   // [S_pad / 32][rows][16] uint16 pairs
+  // per-sample term cache, same tiling as y: the likelihood change of one more
+  // (tpos) / one fewer (tneg) event covering the sample at its committed count,
+  // term(c, +-1) of density.hpp:286-301; rebuilt after every commit (k_terms),
+  // read by the dense band of births and deaths where the region's own diff is
+  // empty at the station
+  const double* tpos;              // [S_pad / 32][rows][32]
+  const double* tneg;
   double* pool;                    // [P][S_pad]
   GenV* gv;                        // [gv_cap] generated versions
   int* gv_free;                    // [gv_cap] free stack of GenV entries (top: Ctl::gv_top)

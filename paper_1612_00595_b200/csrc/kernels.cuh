@@ -90,6 +90,19 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// cp.async (LDGSTS): one 8-byte element per lane, global -> shared, no register
+__device__ __forceinline__ void cp_async8(const double* smem_dst, const double* gsrc) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 // Per-sample likelihood change for coverage c -> c + dc (density.hpp:286-301):
 // (L[c+dc] - y^2 I[c+dc]) - (L[c] - y^2 I[c]) = dL - y^2 dI with the per-count
 // differences precomputed on the host from glibc log (one 16-byte lookup).
@@ -284,6 +297,41 @@ __device__ __forceinline__ void band1(const Dev& d, int j, Win W, const Wins<ND>
   sig += s;
 }
 
+// The dense band where the region's own diff is empty at every station of the
+// tile: the rows' terms at the committed counts were computed by k_terms
+// (Dev::tpos / tneg, the same expression on the same table entries), so the
+// lane sums its window's cached terms in band1's order (bit-identical sums):
+// one 8-byte load and one add per row instead of two loads, a table lookup, a
+// conversion and three fp64 operations.
+template <int SIGN>
+__device__ __forceinline__ void band1_terms(const Dev& d, int j, Win W, double& sig) {
+  constexpr int RU = SEIS_BAND_RU;
+  const int len = W.hi - W.lo;
+  const int trips = (int)__reduce_max_sync(0xffffffffu, (unsigned)len);
+  const int span = (trips + RU - 1) / RU * RU;
+  const int base = min(W.lo, d.rows - span);
+  const int sh = W.lo - base;
+  const double* __restrict__ tp = (SIGN > 0 ? d.tpos : d.tneg) + yix(d.rows, base, j);
+  double s = 0.0;
+  if (trips == RU && __all_sync(0xffffffffu, len == RU && sh == 0)) {
+    double v[RU];  // every lane's window is exactly one batch
+#pragma unroll
+    for (int k = 0; k < RU; ++k) v[k] = __ldg(tp + k * 32);
+#pragma unroll
+    for (int k = 0; k < RU; ++k) s += v[k];
+  } else {
+    for (int i0 = 0; i0 < trips; i0 += RU) {
+      double v[RU];
+#pragma unroll
+      for (int k = 0; k < RU; ++k) v[k] = __ldg(tp + k * 32);
+      tp += RU * 32;
+#pragma unroll
+      for (int k = 0; k < RU; ++k) s += (unsigned)(i0 + k - sh) < (unsigned)len ? v[k] : 0.0;
+    }
+  }
+  sig += s;
+}
+
 // A one-event move (location / arrival, NR = NA = 1) whose windows overlap
 // changes only the rows of their symmetric difference: each lane walks its own
 // <= 2 edge intervals (a uniform trip count across the warp) instead of the
@@ -415,9 +463,13 @@ struct DiffW {
 
 // Walk the region's (start, current) pairs at station j with each batch of
 // four pairs' pool loads issued together; first four effective windows kept.
+// stg (tile-major pass): this lane's column of the warp's stage buffer, rows
+// 1..4 = the arrivals of pold[0], pnew[0], pold[1], pnew[1] where those are
+// stored rows
 template <int K, bool GEN>
 __device__ __forceinline__ int diff_collect(const Dev& d, int j, int np, const int* pold,
-                                            const int* pnew, Win (&w)[K], int (&sg)[K]) {
+                                            const int* pnew, Win (&w)[K], int (&sg)[K],
+                                            const double* stg = nullptr) {
   int nw = 0;
 #pragma unroll
   for (int k = 0; k < K; ++k) {
@@ -431,8 +483,13 @@ __device__ __forceinline__ int diff_collect(const Dev& d, int j, int np, const i
     for (int k = 0; k < 4; ++k) {
       const int q = q0 + k;
       const int so = q < np ? pold[q] : -1, sn = q < np ? pnew[q] : -1;
-      vo[k] = so != -1 ? ver_arr<GEN>(d, so, j) : 0.0;
-      vn[k] = sn != -1 ? ver_arr<GEN>(d, sn, j) : 0.0;
+      if (stg && q0 == 0 && k < 2) {
+        vo[k] = so >= 0 ? stg[(1 + 2 * k) * 32] : (so != -1 ? ver_arr<GEN>(d, so, j) : 0.0);
+        vn[k] = sn >= 0 ? stg[(2 + 2 * k) * 32] : (sn != -1 ? ver_arr<GEN>(d, sn, j) : 0.0);
+      } else {
+        vo[k] = so != -1 ? ver_arr<GEN>(d, so, j) : 0.0;
+        vn[k] = sn != -1 ? ver_arr<GEN>(d, sn, j) : 0.0;
+      }
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -466,8 +523,9 @@ __device__ __forceinline__ int diff_collect(const Dev& d, int j, int np, const i
 
 template <bool GEN>
 __device__ __forceinline__ void diff_windows(const Dev& d, int j, int np, const int* pold,
-                                             const int* pnew, DiffW& X) {
-  const int nw = diff_collect<4, GEN>(d, j, np, pold, pnew, X.D.w, X.sg);
+                                             const int* pnew, DiffW& X,
+                                             const double* stg = nullptr) {
+  const int nw = diff_collect<4, GEN>(d, j, np, pold, pnew, X.D.w, X.sg, stg);
   X.nwmax = (int)__reduce_max_sync(0xffffffffu, (unsigned)nw);
 }
 
@@ -530,16 +588,19 @@ __device__ __forceinline__ void diff_from_cache(const DiffS& c, DiffW& X) {
 // the added/removed versions (arr += added - removed) and the per-sample
 // terms where the coverage changes (sig). Called by a whole warp
 // (j = tile base + lane) so the band reduction is warp-uniform.
+// stg / stg_r (tile-major pass, else null): this lane's staged station
+// coordinate (row 0) and the staged arrival of the first removed version
 template <int NR, int NA, typename YT, bool GEN>
 __device__ __forceinline__ void station_item(const Dev& d, const Prop& P, const PassIn& in,
                                              int j, int np, const int* pold, const int* pnew,
                                              DiffW X, bool haveX, const double2* Ts, double& sig,
-                                             double& arr, int& cnt) {
+                                             double& arr, int& cnt, const double* stg,
+                                             const double* stg_r) {
   const long long t_item = kProfItems ? clock64() : 0;
   const bool v = j < d.S;
   Wins<NR> R;
   Wins<NA> A;
-  const double s = v ? d.stations[j] : 0.0;
+  const double s = v ? (stg ? stg[0] : d.stations[j]) : 0.0;
   double ra[NR > 0 ? NR : 1];
   // a generated removed version (spec v2): its arrival and, for a location /
   // joint move, the moved version's arrival come from the same normal
@@ -553,7 +614,7 @@ __device__ __forceinline__ void station_item(const Dev& d, const Prop& P, const 
       const double mo = arrival_mean(d, P.rx[q], P.rt[q], s);
       const int rs = P.rslot[q];
       if (!GEN || rs >= 0) {
-        ra[q] = __ldg(d.pool + (size_t)rs * d.S_pad + j);
+        ra[q] = (q == 0 && stg_r) ? *stg_r : __ldg(d.pool + (size_t)rs * d.S_pad + j);
       } else {
         const GenV* g = gv_of(d, rs);
         rz[q] = d.sigma * (double)seis_normal(g->seed, g->sweep, g->region, g->step, (uint32_t)j);
@@ -642,7 +703,10 @@ __device__ __forceinline__ void station_item(const Dev& d, const Prop& P, const 
     int sg0[1];
     if (NR + NA == 1) {
       const Win W = NA ? A.w[0] : R.w[0];
-      band1<NA ? 1 : -1, 0, YT>(d, j, W, D0, sg0, Ts, sig);
+      if (d.tpos)
+        band1_terms<NA ? 1 : -1>(d, j, W, sig);
+      else
+        band1<NA ? 1 : -1, 0, YT>(d, j, W, D0, sg0, Ts, sig);
       cnt += W.hi - W.lo;
     }
     else if (NR == 1 && NA == 1 && P.nr == 1 && P.na == 1)
@@ -737,7 +801,9 @@ __device__ __forceinline__ void score_item(const Dev& d, const Prop& P, const Pa
                                            int tile, int np, const int* pold,
                                            const int* pnew, const DiffW& X, bool haveX,
                                            const double2* Ts,
-                                           double& sig, double& arr, int& cnt) {
+                                           double& sig, double& arr, int& cnt,
+                                           const double* stg = nullptr,
+                                           const double* stg_r = nullptr) {
   if (P.skip) return;
   const int j = tile * 32 + (threadIdx.x & 31);
   if (MODE == 0 && P.type == 3) {
@@ -746,13 +812,17 @@ __device__ __forceinline__ void score_item(const Dev& d, const Prop& P, const Pa
   }
   const int shape = P.nr * 3 + P.na;
   if (shape == 1)  // birth
-    station_item<0, 1, YT, GEN>(d, P, in, j, np, pold, pnew, X, haveX, Ts, sig, arr, cnt);
+    station_item<0, 1, YT, GEN>(d, P, in, j, np, pold, pnew, X, haveX, Ts, sig, arr, cnt, stg,
+                                stg_r);
   else if (shape == 3)  // death
-    station_item<1, 0, YT, GEN>(d, P, in, j, np, pold, pnew, X, haveX, Ts, sig, arr, cnt);
+    station_item<1, 0, YT, GEN>(d, P, in, j, np, pold, pnew, X, haveX, Ts, sig, arr, cnt, stg,
+                                stg_r);
   else if (shape == 4)  // location / arrival
-    station_item<1, 1, YT, GEN>(d, P, in, j, np, pold, pnew, X, haveX, Ts, sig, arr, cnt);
+    station_item<1, 1, YT, GEN>(d, P, in, j, np, pold, pnew, X, haveX, Ts, sig, arr, cnt, stg,
+                                stg_r);
   else  // joint pair, and any other change of <= 2 removed / 2 added events
-    station_item<2, 2, YT, GEN>(d, P, in, j, np, pold, pnew, X, haveX, Ts, sig, arr, cnt);
+    station_item<2, 2, YT, GEN>(d, P, in, j, np, pold, pnew, X, haveX, Ts, sig, arr, cnt, stg,
+                                stg_r);
 }
 
 }  // namespace seis
