@@ -712,6 +712,10 @@ constexpr int kPhaseSmemTile = LOGIWIN * (int)sizeof(double) + MSPEC * NT * (2 *
 constexpr int kPhaseSmem = kPhaseSmemTile + kDiffCache * (int)(sizeof(DiffS) + sizeof(DiffS4x));
 // run_serial's chain: + its arrays in place of the diff-window cache (unused)
 constexpr int kPhaseSmemSerial = kPhaseSmemTile + ChainSmem<kSerialCap>::bytes;
+// tile-major launches: + per-tile flags, the cp.async stage and cached-term buffers
+constexpr int kPhaseSmemTM = kPhaseSmemTile + kTileFlags + (kStageOn ? kStageBytes : 0) +
+                             (kTermBuf ? kTermBufBytes : 0);
+static_assert(kPhaseSmemTM + 48 * 1024 <= 227 * 1024, "k_phase shared memory");
 // The tile-major pass (S_pad >= 2048: 64 station tiles and more) never builds
 // the diff-window cache, so its launches leave that shared memory to L1: the
 // band rows a warp's proposals share on a tile stay resident between them.
@@ -722,7 +726,7 @@ inline int phase_smem(const Dev& d) {
   // tile-major: + one flag byte per station tile
   return (dcache || full) ? kPhaseSmem
                           : kPhaseSmemTile + std::min(kTileFlags, (d.S_pad / 32 + 15) & ~15) +
-                                (kStageOn ? kStageBytes : 0);
+                                (kStageOn ? kStageBytes : 0) + (kTermBuf ? kTermBufBytes : 0);
 }
 
 int fail(int code, const std::string& m) {
@@ -1051,10 +1055,10 @@ template <typename YT, int MODE, bool TM>
 void set_phase_attrs_tm() {
 #ifdef SEIS_FAST_BUILD
   if constexpr (std::is_same<YT, float>::value && MODE == 0)
-    ck(phase_set_smem<float, 0, MAXOWN, false, TM>(kPhaseSmem), "smem attribute");
+    ck(phase_set_smem<float, 0, MAXOWN, false, TM>(TM ? std::max(kPhaseSmem, kPhaseSmemTM) : kPhaseSmem), "smem attribute");
 #else
-  ck(phase_set_smem<YT, MODE, MAXOWN, true, TM>(kPhaseSmem), "smem attribute");
-  if (MODE == 0) ck(phase_set_smem<YT, 0, MAXOWN, false, TM>(kPhaseSmem), "smem attribute");
+  ck(phase_set_smem<YT, MODE, MAXOWN, true, TM>(TM ? std::max(kPhaseSmem, kPhaseSmemTM) : kPhaseSmem), "smem attribute");
+  if (MODE == 0) ck(phase_set_smem<YT, 0, MAXOWN, false, TM>(TM ? std::max(kPhaseSmem, kPhaseSmemTM) : kPhaseSmem), "smem attribute");
   ck(phase_set_smem<YT, MODE, kSerialCap, true, TM>(kPhaseSmemSerial), "smem attribute");
 #endif
 }
@@ -1678,6 +1682,13 @@ static int spec_depth() {
   const int m = v ? atoi(v) : kSpecDefault;
   return m < 1 ? 1 : (m > MSPEC ? MSPEC : m);
 }
+// Rounds that stop at their first scored proposal: the default of tile-major
+// launches (config[2]: 3.70 M -> proposals/s with three proposals scored per
+// round, measured against SEIS_FIRST=0); SEIS_FIRST overrides (A/B).
+static int first_scored(const seis_engine* e) {
+  if (const char* v = getenv("SEIS_FIRST")) return atoi(v) != 0;
+  return tile_major(e->d) ? 1 : 0;
+}
 
 static int run_driver(seis_engine* e, const seis_sampler_cfg* sc, int32_t mode,
                       const seis_tape_step* tape, int64_t n_tape, const double* tape_arr,
@@ -1740,6 +1751,7 @@ static int run_driver(seis_engine* e, const seis_sampler_cfg* sc, int32_t mode,
     sp.joint_t_sd = sc->step_joint / e->cfg.v;
     sp.ncol = ncol;
     sp.mspec = spec_depth();
+    sp.first_scored = first_scored(e);
     const int bcap = (int)sc->n_regions + 4;
     // the timed region starts before the partition kernel: everything the run
     // launches (partition, id base, counters, phases, barriers, rows) is inside
@@ -2186,6 +2198,7 @@ extern "C" int seis_run_naive(seis_engine* e, const seis_sampler_cfg* sc, int32_
     sp.joint_t_sd = sc->step_joint / e->cfg.v;
     sp.ncol = 1;
     sp.mspec = spec_depth();
+    sp.first_scored = first_scored(e);
     int* births_cnt = static_cast<int*>(alloc((size_t)nreg * 4));
     OutEv* births = static_cast<OutEv*>(alloc(
         ((size_t)nreg * MAXOWN + (size_t)kOvfRegions * kSerialCap) * sizeof(OutEv)));

@@ -87,6 +87,19 @@ constexpr int kStageBytes = NW * 2 * kStageRows * 32 * 8;
 #define SEIS_STAGE 0
 #endif
 constexpr bool kStageOn = SEIS_STAGE;
+// Tile-major pass: the cached-term rows of a dense band (Dev::tpos / tneg)
+// are copied to a per-warp buffer of kTermRows x 32 doubles with cp.async and
+// summed one item later (phase.cuh)
+#ifndef SEIS_TERMBUF
+#define SEIS_TERMBUF 0
+#endif
+constexpr bool kTermBuf = SEIS_TERMBUF != 0;  // 1: cp.async buffer, 2: registers
+#ifndef SEIS_PAIR
+#define SEIS_PAIR 1
+#endif
+constexpr bool kPairOn = SEIS_PAIR;  // tile pairs for births / deaths without own diff (phase.cuh)
+constexpr int kTermRows = 20;  // = SEIS_BAND_RU: longer windows are summed in place
+constexpr int kTermBufBytes = SEIS_TERMBUF == 1 ? NW * kTermRows * 32 * 8 : 0;
 constexpr int kRowPad = 32;      // zero rows appended to y and cov (unpredicated chunk loads)
 #ifndef SEIS_LOGIWIN
 #define SEIS_LOGIWIN 1024
@@ -169,6 +182,7 @@ struct Samp {
   double step_lx, step_lt, step_arr, step_joint, joint_t_sd;
   int ncol;
   int mspec;  // speculative proposals per round, 1..MSPEC
+  int first_scored;  // end every round at its first scored proposal (phase.cuh)
 };
 
 struct Table {

@@ -332,6 +332,69 @@ __device__ __forceinline__ void band1_terms(const Dev& d, int j, Win W, double& 
   sig += s;
 }
 
+// Two station tiles of one production birth (BIRTH) or death, where the
+// region's own diff has no window on either tile: station_item's setup
+// (density.hpp:239-262: arrival of the added / removed version, its window,
+// its log-density) and the cached-term band for both tiles side by side, so
+// the two philox / fp64 chains interleave and twice the rows are in flight.
+// Per tile the operations and their order are station_item's + band1_terms':
+// the sums are bit-identical to scoring the tiles one after the other.
+// (Four tiles side by side, and a K-tile template of this function, measured
+// slower: address arithmetic and spills at the 128-register budget.)
+template <bool BIRTH>
+__device__ __forceinline__ void dense_pair_terms(const Dev& d, const Prop& P, const PassIn& in,
+                                                 int jA, int jB, double& sigA, double& sigB,
+                                                 double& arrA, double& arrB, int& cnt) {
+  constexpr int H = SEIS_BAND_RU / 2;
+  const bool vA = jA < d.S, vB = jB < d.S;
+  const double sA = vA ? d.stations[jA] : 0.0, sB = vB ? d.stations[jB] : 0.0;
+  const double ex = BIRTH ? P.ax[0] : P.rx[0], et = BIRTH ? P.at[0] : P.rt[0];
+  const double mA = arrival_mean(d, ex, et, sA), mB = arrival_mean(d, ex, et, sB);
+  double aA, aB;
+  if (BIRTH) {
+    aA = mA + d.sigma * (double)seis_normal(in.seed, in.sweep, in.region, in.step, (uint32_t)jA);
+    aB = mB + d.sigma * (double)seis_normal(in.seed, in.sweep, in.region, in.step, (uint32_t)jB);
+  } else {
+    const double* row = d.pool + (size_t)P.rslot[0] * d.S_pad;
+    aA = __ldg(row + jA);
+    aB = __ldg(row + jB);
+  }
+  const Win WA = vA ? clampw(make_win(d, aA), in.wlo, in.whi) : empty_win();
+  const Win WB = vB ? clampw(make_win(d, aB), in.wlo, in.whi) : empty_win();
+  const double lA = vA ? arr_logpdf(d, aA, mA) : 0.0, lB = vB ? arr_logpdf(d, aB, mB) : 0.0;
+  arrA = BIRTH ? lA : 0.0 - lA;
+  arrB = BIRTH ? lB : 0.0 - lB;
+  const int lenA = WA.hi - WA.lo, lenB = WB.hi - WB.lo;
+  cnt += lenA + lenB;
+  if (__all_sync(0xffffffffu, lenA == 2 * H && lenB == 2 * H)) {
+    const double* __restrict__ tA = (BIRTH ? d.tpos : d.tneg) + yix(d.rows, WA.lo, jA);
+    const double* __restrict__ tB = (BIRTH ? d.tpos : d.tneg) + yix(d.rows, WB.lo, jB);
+    double a = 0.0, b = 0.0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      double v[2 * H];
+#pragma unroll
+      for (int k = 0; k < H; ++k) {
+        v[k] = __ldg(tA + (h * H + k) * 32);
+        v[H + k] = __ldg(tB + (h * H + k) * 32);
+      }
+#pragma unroll
+      for (int k = 0; k < H; ++k) {
+        a += v[k];
+        b += v[H + k];
+      }
+    }
+    sigA = a;
+    sigB = b;
+  } else {
+    double a = 0.0, b = 0.0;
+    band1_terms<BIRTH ? 1 : -1>(d, jA, WA, a);
+    band1_terms<BIRTH ? 1 : -1>(d, jB, WB, b);
+    sigA = a;
+    sigB = b;
+  }
+}
+
 // A one-event move (location / arrival, NR = NA = 1) whose windows overlap
 // changes only the rows of their symmetric difference: each lane walks its own
 // <= 2 edge intervals (a uniform trip count across the warp) instead of the
@@ -588,6 +651,9 @@ __device__ __forceinline__ void diff_from_cache(const DiffS& c, DiffW& X) {
 // the added/removed versions (arr += added - removed) and the per-sample
 // terms where the coverage changes (sig). Called by a whole warp
 // (j = tile base + lane) so the band reduction is warp-uniform.
+// defer_w (tile-major pass): where the dense band would sum the cached terms
+// (band1_terms), the window is handed back instead (lo >= 0) and the caller
+// sums it one item later from rows copied with cp.async.
 // stg / stg_r (tile-major pass, else null): this lane's staged station
 // coordinate (row 0) and the staged arrival of the first removed version
 template <int NR, int NA, typename YT, bool GEN>
@@ -595,7 +661,7 @@ __device__ __forceinline__ void station_item(const Dev& d, const Prop& P, const 
                                              int j, int np, const int* pold, const int* pnew,
                                              DiffW X, bool haveX, const double2* Ts, double& sig,
                                              double& arr, int& cnt, const double* stg,
-                                             const double* stg_r) {
+                                             const double* stg_r, Win* defer_w) {
   const long long t_item = kProfItems ? clock64() : 0;
   const bool v = j < d.S;
   Wins<NR> R;
@@ -703,9 +769,11 @@ __device__ __forceinline__ void station_item(const Dev& d, const Prop& P, const 
     int sg0[1];
     if (NR + NA == 1) {
       const Win W = NA ? A.w[0] : R.w[0];
-      if (d.tpos)
+      if (d.tpos && defer_w) {
+        *defer_w = W;  // the caller sums the cached terms (tile-major pass: one item later)
+      } else if (d.tpos) {
         band1_terms<NA ? 1 : -1>(d, j, W, sig);
-      else
+      } else
         band1<NA ? 1 : -1, 0, YT>(d, j, W, D0, sg0, Ts, sig);
       cnt += W.hi - W.lo;
     }
@@ -803,7 +871,8 @@ __device__ __forceinline__ void score_item(const Dev& d, const Prop& P, const Pa
                                            const double2* Ts,
                                            double& sig, double& arr, int& cnt,
                                            const double* stg = nullptr,
-                                           const double* stg_r = nullptr) {
+                                           const double* stg_r = nullptr,
+                                           Win* defer_w = nullptr) {
   if (P.skip) return;
   const int j = tile * 32 + (threadIdx.x & 31);
   if (MODE == 0 && P.type == 3) {
@@ -813,16 +882,16 @@ __device__ __forceinline__ void score_item(const Dev& d, const Prop& P, const Pa
   const int shape = P.nr * 3 + P.na;
   if (shape == 1)  // birth
     station_item<0, 1, YT, GEN>(d, P, in, j, np, pold, pnew, X, haveX, Ts, sig, arr, cnt, stg,
-                                stg_r);
+                                stg_r, defer_w);
   else if (shape == 3)  // death
     station_item<1, 0, YT, GEN>(d, P, in, j, np, pold, pnew, X, haveX, Ts, sig, arr, cnt, stg,
-                                stg_r);
+                                stg_r, defer_w);
   else if (shape == 4)  // location / arrival
     station_item<1, 1, YT, GEN>(d, P, in, j, np, pold, pnew, X, haveX, Ts, sig, arr, cnt, stg,
-                                stg_r);
+                                stg_r, defer_w);
   else  // joint pair, and any other change of <= 2 removed / 2 added events
     station_item<2, 2, YT, GEN>(d, P, in, j, np, pold, pnew, X, haveX, Ts, sig, arr, cnt, stg,
-                                stg_r);
+                                stg_r, defer_w);
 }
 
 }  // namespace seis

@@ -241,6 +241,8 @@ __global__ void __launch_bounds__(NTT, MINB)
   double* const stage = reinterpret_cast<double*>(
       tile_nw + min(kTileFlags, ((d.S_pad + 31) / 32 + 15) & ~15));
   __shared__ int s_stage_slot[NWT][kStageRows];
+  // ... and the warps' cached-term row buffers (tile-major pass)
+  double* const tbuf = stage + (kStageOn ? kStageBytes / 8 : 0);
   // serial layout in dynamic smem: own | st | log i | pold | pnew | lfree | cur_of
   char* const big = reinterpret_cast<char*>(dcache);
   constexpr size_t kOffSt = CAP * sizeof(OwnEv), kOffLogi = kOffSt + CAP * sizeof(StartEv);
@@ -409,7 +411,7 @@ __global__ void __launch_bounds__(NTT, MINB)
   const int T_per = (d.S_pad + 31) / 32;  // tiles of 32 stations
   int round = 0;
   for (int i0 = 0; i0 < (int)sp.k; ++round) {
-    const int m = min(sp.mspec, (int)sp.k - i0);
+    int m = min(sp.mspec, (int)sp.k - i0);
     const int buf = round & 1;
     __syncthreads();  // S0: previous round's write-back and state are visible
     if (tid == 0) {
@@ -461,6 +463,16 @@ __global__ void __launch_bounds__(NTT, MINB)
         diff_station<GEN>(d, j, np_c, pold, pnew, dcache[j], ovf[j]);
     }
     __syncthreads();  // S1: proposals (and diff windows) ready
+    // first_scored: the round ends with its first proposal that needs scoring
+    // (the skipped ones before it are rejected for free, the ones after it
+    // are regenerated): no proposal is ever scored and then discarded, while
+    // generation stays parallel. Pays where a round's items are long
+    // (tile-major launches); speculation pays where they are short.
+    if (sp.first_scored) {
+      int f = 0;
+      while (f < m - 1 && prop[buf][f].skip) ++f;
+      m = f + 1;
+    }
     if (tid == 0) {
       const long long now = clock64();
       tprof[0] += now - tc;
@@ -524,9 +536,64 @@ __global__ void __launch_bounds__(NTT, MINB)
           }
           cp_async_commit();
         };
+        // cached-term bands one item late: the rows of a birth's / death's
+        // window are copied to the warp's buffer with cp.async when its
+        // window is known and summed after the next item's setup, so their
+        // L2 / HBM latency runs under that setup
+        const bool tbuf_on = !kBig && kTermBuf && d.tpos != nullptr;
+        double* const tb = tbuf + (size_t)warp * kTermRows * 32 + lane;
+        int pend_q = -1, pend_len = 0;
+        auto drain = [&]() {
+          double s2 = 0.0;
+          cp_async_wait<0>();
+#pragma unroll
+          for (int k = 0; k < kTermRows; ++k) s2 += k < pend_len ? tb[k * 32] : 0.0;
+          acc_sig[pend_q][tid] += s2;
+          pend_q = -1;
+        };
+        // Tile pairs: when every scored proposal of the round is a production
+        // birth or death and the region's diff has no window on two of the
+        // warp's tiles, both are scored together (dense_pair_terms): two
+        // independent setup chains and twice the cached-term loads in flight
+        bool pair_round = kPairOn && !stage_on && !tbuf_on && MODE == 0 && any_dense &&
+                          d.tpos != nullptr;
+        for (int q = 0; q < m && pair_round; ++q) {
+          const Prop& P = prop[buf][q];
+          if (P.skip) continue;
+          if (!(P.type == 0 || (P.type == 1 && (!GEN || P.rslot[0] >= 0)))) pair_round = false;
+        }
         int sbuf = 0;
         if (stage_on && warp < tile_end) stage_issue(warp, 0);
-        for (int tile = warp; tile < tile_end; tile += NWT, sbuf ^= 1) {
+        int tstep = NWT;
+        for (int tile = warp; tile < tile_end; tile += tstep, sbuf ^= 1) {
+          tstep = NWT;
+          if (pair_round && tile + NWT < tile_end &&
+              (np_now == 0 || (tw_fresh && tile_nw[tile] == 0 && tile_nw[tile + NWT] == 0))) {
+            const int jA = tile * 32 + lane, jB = jA + NWT * 32;
+#pragma unroll 1
+            for (int q = 0; q < m; ++q) {
+              const Prop& P = prop[buf][q];
+              if (P.skip) continue;
+              PassIn in;
+              in.seed = sp.seed;
+              in.sweep = (uint32_t)pa.epoch;
+              in.region = (uint32_t)region;
+              in.step = (uint32_t)(pa.step_base + i0 + q);
+              in.wlo = win_lo;
+              in.whi = win_hi;
+              double sA = 0.0, sB = 0.0, aA = 0.0, aB = 0.0;
+              int cnt = 0;
+              if (P.type == 0)
+                dense_pair_terms<true>(d, P, in, jA, jB, sA, sB, aA, aB, cnt);
+              else
+                dense_pair_terms<false>(d, P, in, jA, jB, sA, sB, aA, aB, cnt);
+              acc_sig[q][tid] = (acc_sig[q][tid] + sA) + sB;  // tile order
+              acc_arr[q][tid] = (acc_arr[q][tid] + aA) + aB;
+              acc_cnt[q][tid] += cnt;
+            }
+            tstep = 2 * NWT;
+            continue;
+          }
           DiffW X;
           long long tq = kProfItems ? clock64() : 0;
           const double* stg = nullptr;
@@ -579,8 +646,28 @@ __global__ void __launch_bounds__(NTT, MINB)
                 (stg && q < kStageRows - 5 && s_stage_slot[warp][5 + q] >= 0)
                     ? stg + (5 + q) * 32
                     : nullptr;
+            Win dw;
+            dw.lo = -1;
             score_item<MODE, YT, GEN>(d, P, in, tile, np_now, pold, pnew, X, true, Ts, sig, arr,
-                                      cnt, stg, stg_r);
+                                      cnt, stg, stg_r, tbuf_on ? &dw : nullptr);
+            if (tbuf_on && dw.lo >= 0) {  // (uniform) a dense band over cached terms
+              const int len = dw.hi - dw.lo;
+              const int j = tile * 32 + lane;
+              if (__all_sync(0xffffffffu, len <= kTermRows)) {
+                if (pend_q >= 0) drain();
+                const double* src = (P.na ? d.tpos : d.tneg) + yix(d.rows, dw.lo, j);
+#pragma unroll
+                for (int k = 0; k < kTermRows; ++k)
+                  if (k < len) cp_async8(tb + k * 32, src + k * 32);
+                cp_async_commit();
+                pend_q = q;
+                pend_len = len;
+              } else if (P.na) {
+                band1_terms<1>(d, j, dw, sig);
+              } else {
+                band1_terms<-1>(d, j, dw, sig);
+              }
+            }
             // per-lane partial sums; the warp reduces them once per round
             acc_sig[q][tid] += sig;
             acc_arr[q][tid] += arr;
@@ -595,6 +682,7 @@ __global__ void __launch_bounds__(NTT, MINB)
             }
           }
         }
+        if (pend_q >= 0) drain();
         for (int q = 0; q < m; ++q) {
           const double sg = warp_sum(acc_sig[q][tid]);
           const double ar = warp_sum(acc_arr[q][tid]);

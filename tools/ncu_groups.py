@@ -4,19 +4,20 @@
 import csv
 import sys
 
-G = [("kernels.cuh", 226, 285, "band1 (dense band)"), ("kernels.cuh", 138, 209, "band"),
-     ("kernels.cuh", 293, 365, "edges"), ("kernels.cuh", 369, 403, "band_generic"),
-     ("kernels.cuh", 405, 527, "diff windows"), ("kernels.cuh", 529, 700, "station_item setup"),
-     ("kernels.cuh", 700, 735, "arrival_item"), ("kernels.cuh", 735, 760, "score_item dispatch"),
-     ("kernels.cuh", 1, 137, "kernels.cuh helpers (term, warp_sum)"),
-     ("seis_philox.h", 1, 400, "philox + Box-Muller"), ("engine.cuh", 245, 253, "make_win"),
-     ("engine.cuh", 263, 265, "inw"), ("engine.cuh", 255, 262, "yix/pix"),
-     ("engine.cuh", 273, 280, "arrival_mean / div_v"), ("engine.cuh", 282, 302, "ver_arr / arr_of"),
-     ("engine.cuh", 304, 314, "arr_logpdf"), ("engine.cu", 686, 743, "tile-major loop"),
-     ("engine.cu", 744, 811, "proposal-major loop"), ("engine.cu", 234, 423, "gen_proposal"),
-     ("engine.cu", 424, 620, "k_phase prologue"), ("engine.cu", 621, 685, "round head"),
-     ("engine.cu", 812, 1115, "decision"), ("engine.cu", 1116, 1200, "write-back"),
-     ("engine.cu", 1200, 1290, "phase outputs")]
+G = [("kernels.cuh", 307, 334, "band1_terms (cached terms)"),
+     ("kernels.cuh", 239, 299, "band1 (dense band, own diff)"), ("kernels.cuh", 151, 222, "band"),
+     ("kernels.cuh", 341, 414, "edges"), ("kernels.cuh", 418, 452, "band_generic"),
+     ("kernels.cuh", 453, 586, "diff windows"), ("kernels.cuh", 587, 771, "station_item setup"),
+     ("kernels.cuh", 772, 804, "arrival_item"), ("kernels.cuh", 805, 840, "score_item dispatch"),
+     ("kernels.cuh", 1, 150, "kernels.cuh helpers (term, warp_sum, cp.async)"),
+     ("seis_philox.h", 1, 400, "philox + Box-Muller"), ("engine.cuh", 278, 287, "make_win"),
+     ("engine.cuh", 296, 299, "inw"), ("engine.cuh", 288, 295, "yix/pix"),
+     ("engine.cuh", 306, 313, "arrival_mean / div_v"), ("engine.cuh", 314, 336, "ver_arr / arr_of"),
+     ("engine.cuh", 337, 350, "arr_logpdf"), ("phase.cuh", 485, 640, "tile-major loop"),
+     ("phase.cuh", 641, 713, "proposal-major loop"), ("phase.cuh", 16, 205, "gen_proposal"),
+     ("phase.cuh", 206, 412, "k_phase prologue"), ("phase.cuh", 413, 484, "round head"),
+     ("phase.cuh", 714, 1015, "decision"), ("phase.cuh", 1016, 1102, "write-back"),
+     ("phase.cuh", 1103, 1200, "phase outputs")]
 rows = list(csv.reader(open(sys.argv[1])))
 f, hdr = None, None
 acc = {g[3]: [0, 0] for g in G}
