@@ -350,7 +350,7 @@ def main():
     ap.add_argument("--k", type=int, default=0,
                     help="override steps per region per sweep")
     ap.add_argument("--capacity", type=int, default=0,
-                    help="event capacity (default 2N + 256; 16N + 4096 for configs 3/4)")
+                    help="event capacity (default 2N + 256; 2 M for configs 3/4)")
     ap.add_argument("--storage", default="", choices=["", "rows", "compact"],
                     help="arrival storage (default: the engine's choice, compact when the "
                          "pool cannot hold two stored rows per event)")
@@ -381,9 +381,10 @@ def main():
     t_gen = time.perf_counter() - t_gen
     naive = args.algorithm == "naive"
     start = "empty" if naive else args.start
-    # configs 3/4 at their k: the hypothesis swings far above the truth's
-    # count, so room for 16 N events
-    cap = args.capacity or int(max(1024, (16 * ev.N + 4096) if big else (ev.N * 2 + 256)))
+    # configs 3/4 at their k: the hypothesis swings between 4 k and 425 k events
+    # from 20 k true ones (profiles/r02_explosion_config{3,4}.log),
+    # so room for 2 M events (compact arrival storage: no row per event)
+    cap = args.capacity or int(2_000_000 if big else max(1024, ev.N * 2 + 256))
     eng = E.Engine(m, sig, event_capacity=cap)
     if args.storage:
         eng.arrival_storage = args.storage

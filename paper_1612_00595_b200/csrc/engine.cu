@@ -1800,17 +1800,20 @@ static int run_driver(seis_engine* e, const seis_sampler_cfg* sc, int32_t mode,
       const unsigned long long none = ~0ull;
       ck(cudaMemcpy(order_io, &none, 8, cudaMemcpyHostToDevice), "H2D");
     }
+    // overflow areas (80 KB each) for region chains rerun past MAXOWN events:
+    // the explosive phases of configs 3/4 rerun thousands of regions
+    const int ovf_cap = serial ? 0 : std::max(kOvfRegions, std::min(n_slots, 8192));
     // per-slot outputs: MAXOWN births / MAXDOUT diff entries per region; the
     // serial chain's one slot holds kSerialCap / 3 kSerialCap
     // (region slots: + kOvfRegions overflow areas for chains rerun past MAXOWN)
     const size_t n_births =
-        serial ? (size_t)kSerialCap : (size_t)n_slots * MAXOWN + (size_t)kOvfRegions * kSerialCap;
+        serial ? (size_t)kSerialCap : (size_t)n_slots * MAXOWN + (size_t)ovf_cap * kSerialCap;
     const size_t n_diff = serial ? (size_t)3 * kSerialCap
-                                 : (size_t)n_slots * MAXDOUT + (size_t)kOvfRegions * 3 * kSerialCap;
+                                 : (size_t)n_slots * MAXDOUT + (size_t)ovf_cap * 3 * kSerialCap;
     OutEv* births = static_cast<OutEv*>(alloc(n_births * sizeof(OutEv)));
     int* diff_cnt = static_cast<int*>(alloc((size_t)n_slots * 4));
     DiffPair* diff = static_cast<DiffPair*>(alloc(n_diff * sizeof(DiffPair)));
-    Ovf ovf{nullptr, nullptr};
+    Ovf ovf{nullptr, nullptr, ovf_cap};
     if (!serial) {
       ovf.slot = static_cast<int*>(alloc((size_t)n_slots * 4));
       ovf.count = static_cast<int*>(alloc(4));
@@ -2199,13 +2202,16 @@ extern "C" int seis_run_naive(seis_engine* e, const seis_sampler_cfg* sc, int32_
     sp.ncol = 1;
     sp.mspec = spec_depth();
     sp.first_scored = first_scored(e);
+    // every region of the one launch may outgrow MAXOWN events (long chains
+    // from the empty start): an overflow area each, up to 32768 regions
+    const int ovf_cap = std::max(kOvfRegions, std::min((int)nreg, 32768));
     int* births_cnt = static_cast<int*>(alloc((size_t)nreg * 4));
     OutEv* births = static_cast<OutEv*>(alloc(
-        ((size_t)nreg * MAXOWN + (size_t)kOvfRegions * kSerialCap) * sizeof(OutEv)));
+        ((size_t)nreg * MAXOWN + (size_t)ovf_cap * kSerialCap) * sizeof(OutEv)));
     int* diff_cnt = static_cast<int*>(alloc((size_t)nreg * 4));
     DiffPair* diff = static_cast<DiffPair*>(alloc(
-        ((size_t)nreg * MAXDOUT + (size_t)kOvfRegions * 3 * kSerialCap) * sizeof(DiffPair)));
-    Ovf ovf{static_cast<int*>(alloc((size_t)nreg * 4)), static_cast<int*>(alloc(4))};
+        ((size_t)nreg * MAXDOUT + (size_t)ovf_cap * 3 * kSerialCap) * sizeof(DiffPair)));
+    Ovf ovf{static_cast<int*>(alloc((size_t)nreg * 4)), static_cast<int*>(alloc(4)), ovf_cap};
     ck(cudaMemsetAsync(ovf.count, 0, 4, e->stream), "memset");
     seis_tape_step* d_tape = nullptr;
     double* d_tarr = nullptr;

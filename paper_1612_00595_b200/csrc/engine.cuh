@@ -53,7 +53,7 @@ struct ChainSmem {  // bytes of the chain arrays (own, st, pold, pnew, lfree, cu
   static constexpr int bytes = CAP * (32 + 24 + 4 + 4) + 2 * CAP * 8 + (CAP + 8) * 8;
 };
 constexpr int kRetryFree = 3 * MAXOWN;  // version slots a region chain can hand to its rerun
-constexpr int kOvfRegions = 512;        // reruns per phase with outputs past MAXOWN / MAXDOUT
+constexpr int kOvfRegions = 512;        // reruns per phase with outputs past MAXOWN / MAXDOUT (at least; Ovf::cap)
 
 // Per-slot phase outputs (births alive at the end, diff entries): region
 // slots at stride MAXOWN / MAXDOUT; a rerun region (whole-chain variant)
@@ -62,6 +62,7 @@ constexpr int kOvfRegions = 512;        // reruns per phase with outputs past MA
 struct Ovf {
   int* slot;   // [n_slots] (null: no overflow areas, e.g. the serial chain)
   int* count;  // overflow areas handed out this phase (reset by the barrier)
+  int cap;     // overflow areas allocated: kOvfRegions, or every region of a naive launch
 };
 __host__ __device__ __forceinline__ size_t births_off(const Ovf& o, int n_slots, int s) {
   const int k = o.slot ? o.slot[s] : -1;

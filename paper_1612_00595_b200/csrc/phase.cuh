@@ -1182,7 +1182,7 @@ __global__ void __launch_bounds__(NTT, MINB)
     // a rerun region writes past MAXOWN / MAXDOUT: an overflow area
     if (kBig && pa.retry_pass && pa.ovf.slot) {
       const int k = atomicAdd(pa.ovf.count, 1);
-      if (k >= kOvfRegions) {
+      if (k >= pa.ovf.cap) {
         set_err(ctl, ERR_OWN_OVERFLOW);
         pa.births_cnt[slot_idx] = 0;
         pa.diff_cnt[slot_idx] = 0;

@@ -560,3 +560,33 @@ def test_production_burn_in_from_empty_many_windows(E, oc, steps):
     s = O.Sampler(steps_per_epoch=steps, epochs=3, n_regions=6, seed=13, dynamic=0, rng_mode=1)
     tr, ro = _prod_vs_oracle(E, oc, m, w, s)
     assert tr.final.ids.size > 10
+
+
+@pytest.mark.parametrize("toggle", ["SEIS_TERMS", "SEIS_FIRST"])
+def test_tile_major_fast_paths_equal_the_direct_paths(E, oc, monkeypatch, toggle):
+    """The tile-major pass's shortcuts must not change a result: the per-sample
+    term cache (k_terms, summed by band1_terms / dense_pair_terms instead of
+    the direct band; SEIS_TERMS=0 disables it) and rounds that end at their
+    first scored proposal (SEIS_FIRST=0: three proposals scored per round).
+    With the shortcut off and on: every delta and decision bit-identical
+    (same operations in the same order), the final hypothesis identical, and
+    both equal to the oracle (density.hpp:214-305, samplers.hpp:115-138)."""
+    m = _mapped_model(S=4200, T=300.0, n_regions=12, x_max=4000.0, lam_events=14)
+    w = oc.sample_world(m, 23)
+    w32 = O.World(m, w.events, w.signals.astype(np.float32).astype(np.float64))
+    s = O.Sampler(steps_per_epoch=20, epochs=2, n_regions=12, seed=33, dynamic=1, rng_mode=1)
+    outs = []
+    for val in ("0", "1"):
+        monkeypatch.setenv(toggle, val)
+        tr, ro = _prod_vs_oracle(E, oc, m, w32, s, init=w.events, dtype=np.float32)
+        outs.append(tr)
+    a, b = outs
+    assert np.array_equal(a.step_out["accepted"], b.step_out["accepted"])
+    if toggle == "SEIS_TERMS":  # same operations in the same order
+        assert np.array_equal(a.step_out["delta"], b.step_out["delta"])
+    else:  # the per-lane partial sums take the tiles in pairs: last-bit differences
+        fin = np.isfinite(a.step_out["delta"])
+        assert np.array_equal(fin, np.isfinite(b.step_out["delta"]))
+        assert np.allclose(a.step_out["delta"][fin], b.step_out["delta"][fin], rtol=1e-12,
+                           atol=1e-9)
+    assert np.array_equal(a.final.arrivals, b.final.arrivals)
