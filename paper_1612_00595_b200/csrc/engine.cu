@@ -712,9 +712,8 @@ constexpr int kPhaseSmemTile = LOGIWIN * (int)sizeof(double) + MSPEC * NT * (2 *
 constexpr int kPhaseSmem = kPhaseSmemTile + kDiffCache * (int)(sizeof(DiffS) + sizeof(DiffS4x));
 // run_serial's chain: + its arrays in place of the diff-window cache (unused)
 constexpr int kPhaseSmemSerial = kPhaseSmemTile + ChainSmem<kSerialCap>::bytes;
-// tile-major launches: + per-tile flags, the cp.async stage and cached-term buffers
-constexpr int kPhaseSmemTM = kPhaseSmemTile + kTileFlags + (kStageOn ? kStageBytes : 0) +
-                             (kTermBuf ? kTermBufBytes : 0);
+// tile-major launches: + per-tile flags
+constexpr int kPhaseSmemTM = kPhaseSmemTile + kTileFlags;
 static_assert(kPhaseSmemTM + 48 * 1024 <= 227 * 1024, "k_phase shared memory");
 // The tile-major pass (S_pad >= 2048: 64 station tiles and more) never builds
 // the diff-window cache, so its launches leave that shared memory to L1: the
@@ -725,8 +724,7 @@ inline int phase_smem(const Dev& d) {
   const bool dcache = (d.S_pad + 31) / 32 < 4 * NW && d.S_pad <= kDiffCache && d.n < 65535;
   // tile-major: + one flag byte per station tile
   return (dcache || full) ? kPhaseSmem
-                          : kPhaseSmemTile + std::min(kTileFlags, (d.S_pad / 32 + 15) & ~15) +
-                                (kStageOn ? kStageBytes : 0) + (kTermBuf ? kTermBufBytes : 0);
+                          : kPhaseSmemTile + std::min(kTileFlags, (d.S_pad / 32 + 15) & ~15);
 }
 
 int fail(int code, const std::string& m) {

@@ -78,29 +78,10 @@ __host__ __device__ __forceinline__ size_t diff_off(const Ovf& o, int n_slots, i
 constexpr int TBL = SEIS_TBL;    // coverage counts whose {dL, dI} rows live in smem
 constexpr int kDiffCache = 2048;  // stations whose round diff windows k_phase caches in smem
 constexpr int kTileFlags = 24576;  // station tiles whose diff flags the tile-major pass keeps
-// Tile-major pass: per warp, the next tile's station coordinates and arrival
-// rows (the round's first two diff pairs, the first removed version of each
-// of up to three proposals) are copied to shared memory with cp.async while
-// the warp scores the current tile (two buffers of kStageRows x 32 doubles)
-constexpr int kStageRows = 8;
-constexpr int kStageBytes = NW * 2 * kStageRows * 32 * 8;
-#ifndef SEIS_STAGE
-#define SEIS_STAGE 0
-#endif
-constexpr bool kStageOn = SEIS_STAGE;
-// Tile-major pass: the cached-term rows of a dense band (Dev::tpos / tneg)
-// are copied to a per-warp buffer of kTermRows x 32 doubles with cp.async and
-// summed one item later (phase.cuh)
-#ifndef SEIS_TERMBUF
-#define SEIS_TERMBUF 0
-#endif
-constexpr bool kTermBuf = SEIS_TERMBUF != 0;  // 1: cp.async buffer, 2: registers
 #ifndef SEIS_PAIR
 #define SEIS_PAIR 1
 #endif
 constexpr bool kPairOn = SEIS_PAIR;  // tile pairs for births / deaths without own diff (phase.cuh)
-constexpr int kTermRows = 20;  // = SEIS_BAND_RU: longer windows are summed in place
-constexpr int kTermBufBytes = SEIS_TERMBUF == 1 ? NW * kTermRows * 32 * 8 : 0;
 constexpr int kRowPad = 32;      // zero rows appended to y and cov (unpredicated chunk loads)
 #ifndef SEIS_LOGIWIN
 #define SEIS_LOGIWIN 1024

@@ -90,19 +90,6 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// cp.async (LDGSTS): one 8-byte element per lane, global -> shared, no register
-__device__ __forceinline__ void cp_async8(const double* smem_dst, const double* gsrc) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem_dst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gsrc) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() {
-  asm volatile("cp.async.commit_group;" ::: "memory");
-}
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
 // Per-sample likelihood change for coverage c -> c + dc (density.hpp:286-301):
 // (L[c+dc] - y^2 I[c+dc]) - (L[c] - y^2 I[c]) = dL - y^2 dI with the per-count
 // differences precomputed on the host from glibc log (one 16-byte lookup).
@@ -152,7 +139,10 @@ __device__ __forceinline__ void band(const Dev& d, int j, int blo, int bhi, cons
                                      const Wins<NA>& A, const Wins<ND>& D,
                                      const int (&sg)[ND > 0 ? ND : 1], const double2* Ts,
                                      double& sig, int& cnt) {
-  constexpr int RU = 4;
+#ifndef SEIS_BANDG_RU
+#define SEIS_BANDG_RU 4
+#endif
+  constexpr int RU = SEIS_BANDG_RU;
   constexpr int stride = 32;  // next row of the station tile
   const YT* __restrict__ y = reinterpret_cast<const YT*>(d.y) + yix(d.rows, 0, j);
   const uint16_t* __restrict__ c16 = reinterpret_cast<const uint16_t*>(d.cov) + yix(d.rows, 0, j);
@@ -332,28 +322,43 @@ __device__ __forceinline__ void band1_terms(const Dev& d, int j, Win W, double& 
   sig += s;
 }
 
-// Two station tiles of one production birth (BIRTH) or death, where the
-// region's own diff has no window on either tile: station_item's setup
-// (density.hpp:239-262: arrival of the added / removed version, its window,
-// its log-density) and the cached-term band for both tiles side by side, so
-// the two philox / fp64 chains interleave and twice the rows are in flight.
-// Per tile the operations and their order are station_item's + band1_terms':
-// the sums are bit-identical to scoring the tiles one after the other.
-// (Four tiles side by side, and a K-tile template of this function, measured
-// slower: address arithmetic and spills at the 128-register budget.)
+// Two neighbouring station tiles (stations j0 .. j0 + 63, j0 a multiple of
+// 64) of one production birth (BIRTH) or death, where the region's own diff
+// has no window on either tile: station_item's setup (density.hpp:239-262:
+// arrival of the added / removed version, its window, its log-density) and
+// the cached-term band for both tiles side by side, so the two fp64 chains
+// interleave and twice the rows are in flight. The 64 birth normals are the
+// two normals of 32 Philox calls (draw 16 + (j >> 1), seis_philox.h): each
+// lane makes one call and the lanes exchange the values by shuffle, where
+// tile by tile every lane makes its own call per tile and neighbouring lanes
+// repeat each other's. Per tile the values, operations and their order are
+// station_item's + band1_terms': the sums are bit-identical to scoring the
+// tiles one after the other. (Four tiles side by side, and a K-tile template
+// of this function, measured slower: address arithmetic and spills at the
+// 128-register budget.)
 template <bool BIRTH>
 __device__ __forceinline__ void dense_pair_terms(const Dev& d, const Prop& P, const PassIn& in,
-                                                 int jA, int jB, double& sigA, double& sigB,
+                                                 int j0, double& sigA, double& sigB,
                                                  double& arrA, double& arrB, int& cnt) {
   constexpr int H = SEIS_BAND_RU / 2;
+  const int lane = threadIdx.x & 31;
+  const int jA = j0 + lane, jB = jA + 32;
   const bool vA = jA < d.S, vB = jB < d.S;
   const double sA = vA ? d.stations[jA] : 0.0, sB = vB ? d.stations[jB] : 0.0;
   const double ex = BIRTH ? P.ax[0] : P.rx[0], et = BIRTH ? P.at[0] : P.rt[0];
   const double mA = arrival_mean(d, ex, et, sA), mB = arrival_mean(d, ex, et, sB);
   double aA, aB;
   if (BIRTH) {
-    aA = mA + d.sigma * (double)seis_normal(in.seed, in.sweep, in.region, in.step, (uint32_t)jA);
-    aB = mB + d.sigma * (double)seis_normal(in.seed, in.sweep, in.region, in.step, (uint32_t)jB);
+    // this lane's call: the normals of stations j0 + 2 lane and j0 + 2 lane + 1
+    float z0, z1;
+    seis_normal_pair(in.seed, in.sweep, in.region, in.step, (uint32_t)((j0 >> 1) + lane), &z0,
+                     &z1);
+    const int h = lane >> 1;
+    const float a0 = __shfl_sync(0xffffffffu, z0, h), a1 = __shfl_sync(0xffffffffu, z1, h);
+    const float b0 = __shfl_sync(0xffffffffu, z0, 16 + h),
+                b1 = __shfl_sync(0xffffffffu, z1, 16 + h);
+    aA = mA + d.sigma * (double)((lane & 1) ? a1 : a0);
+    aB = mB + d.sigma * (double)((lane & 1) ? b1 : b0);
   } else {
     const double* row = d.pool + (size_t)P.rslot[0] * d.S_pad;
     aA = __ldg(row + jA);
@@ -526,13 +531,9 @@ struct DiffW {
 
 // Walk the region's (start, current) pairs at station j with each batch of
 // four pairs' pool loads issued together; first four effective windows kept.
-// stg (tile-major pass): this lane's column of the warp's stage buffer, rows
-// 1..4 = the arrivals of pold[0], pnew[0], pold[1], pnew[1] where those are
-// stored rows
 template <int K, bool GEN>
 __device__ __forceinline__ int diff_collect(const Dev& d, int j, int np, const int* pold,
-                                            const int* pnew, Win (&w)[K], int (&sg)[K],
-                                            const double* stg = nullptr) {
+                                            const int* pnew, Win (&w)[K], int (&sg)[K]) {
   int nw = 0;
 #pragma unroll
   for (int k = 0; k < K; ++k) {
@@ -546,13 +547,8 @@ __device__ __forceinline__ int diff_collect(const Dev& d, int j, int np, const i
     for (int k = 0; k < 4; ++k) {
       const int q = q0 + k;
       const int so = q < np ? pold[q] : -1, sn = q < np ? pnew[q] : -1;
-      if (stg && q0 == 0 && k < 2) {
-        vo[k] = so >= 0 ? stg[(1 + 2 * k) * 32] : (so != -1 ? ver_arr<GEN>(d, so, j) : 0.0);
-        vn[k] = sn >= 0 ? stg[(2 + 2 * k) * 32] : (sn != -1 ? ver_arr<GEN>(d, sn, j) : 0.0);
-      } else {
-        vo[k] = so != -1 ? ver_arr<GEN>(d, so, j) : 0.0;
-        vn[k] = sn != -1 ? ver_arr<GEN>(d, sn, j) : 0.0;
-      }
+      vo[k] = so != -1 ? ver_arr<GEN>(d, so, j) : 0.0;
+      vn[k] = sn != -1 ? ver_arr<GEN>(d, sn, j) : 0.0;
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -586,9 +582,8 @@ __device__ __forceinline__ int diff_collect(const Dev& d, int j, int np, const i
 
 template <bool GEN>
 __device__ __forceinline__ void diff_windows(const Dev& d, int j, int np, const int* pold,
-                                             const int* pnew, DiffW& X,
-                                             const double* stg = nullptr) {
-  const int nw = diff_collect<4, GEN>(d, j, np, pold, pnew, X.D.w, X.sg, stg);
+                                             const int* pnew, DiffW& X) {
+  const int nw = diff_collect<4, GEN>(d, j, np, pold, pnew, X.D.w, X.sg);
   X.nwmax = (int)__reduce_max_sync(0xffffffffu, (unsigned)nw);
 }
 
@@ -651,22 +646,16 @@ __device__ __forceinline__ void diff_from_cache(const DiffS& c, DiffW& X) {
 // the added/removed versions (arr += added - removed) and the per-sample
 // terms where the coverage changes (sig). Called by a whole warp
 // (j = tile base + lane) so the band reduction is warp-uniform.
-// defer_w (tile-major pass): where the dense band would sum the cached terms
-// (band1_terms), the window is handed back instead (lo >= 0) and the caller
-// sums it one item later from rows copied with cp.async.
-// stg / stg_r (tile-major pass, else null): this lane's staged station
-// coordinate (row 0) and the staged arrival of the first removed version
 template <int NR, int NA, typename YT, bool GEN>
 __device__ __forceinline__ void station_item(const Dev& d, const Prop& P, const PassIn& in,
                                              int j, int np, const int* pold, const int* pnew,
                                              DiffW X, bool haveX, const double2* Ts, double& sig,
-                                             double& arr, int& cnt, const double* stg,
-                                             const double* stg_r, Win* defer_w) {
+                                             double& arr, int& cnt) {
   const long long t_item = kProfItems ? clock64() : 0;
   const bool v = j < d.S;
   Wins<NR> R;
   Wins<NA> A;
-  const double s = v ? (stg ? stg[0] : d.stations[j]) : 0.0;
+  const double s = v ? d.stations[j] : 0.0;
   double ra[NR > 0 ? NR : 1];
   // a generated removed version (spec v2): its arrival and, for a location /
   // joint move, the moved version's arrival come from the same normal
@@ -680,7 +669,7 @@ __device__ __forceinline__ void station_item(const Dev& d, const Prop& P, const 
       const double mo = arrival_mean(d, P.rx[q], P.rt[q], s);
       const int rs = P.rslot[q];
       if (!GEN || rs >= 0) {
-        ra[q] = (q == 0 && stg_r) ? *stg_r : __ldg(d.pool + (size_t)rs * d.S_pad + j);
+        ra[q] = __ldg(d.pool + (size_t)rs * d.S_pad + j);
       } else {
         const GenV* g = gv_of(d, rs);
         rz[q] = d.sigma * (double)seis_normal(g->seed, g->sweep, g->region, g->step, (uint32_t)j);
@@ -769,11 +758,9 @@ __device__ __forceinline__ void station_item(const Dev& d, const Prop& P, const 
     int sg0[1];
     if (NR + NA == 1) {
       const Win W = NA ? A.w[0] : R.w[0];
-      if (d.tpos && defer_w) {
-        *defer_w = W;  // the caller sums the cached terms (tile-major pass: one item later)
-      } else if (d.tpos) {
+      if (d.tpos)
         band1_terms<NA ? 1 : -1>(d, j, W, sig);
-      } else
+      else
         band1<NA ? 1 : -1, 0, YT>(d, j, W, D0, sg0, Ts, sig);
       cnt += W.hi - W.lo;
     }
@@ -799,7 +786,13 @@ __device__ __forceinline__ void station_item(const Dev& d, const Prop& P, const 
     else
       band<NR, NA, 2, YT>(d, j, blo, bhi, R, A, D2, sg2, Ts, sig, cnt);
   } else if (nwmax <= 4) {
-    band<NR, NA, 4, YT>(d, j, blo, bhi, R, A, D, sg, Ts, sig, cnt);
+    if (NR + NA == 1) {  // a dense move: the whole window in one batch, as with two windows
+      const Win W = NA ? A.w[0] : R.w[0];
+      band1<NA ? 1 : -1, 4, YT>(d, j, W, D, sg, Ts, sig);
+      cnt += W.hi - W.lo;
+    } else {
+      band<NR, NA, 4, YT>(d, j, blo, bhi, R, A, D, sg, Ts, sig, cnt);
+    }
   } else if (nwmax <= 8 && haveX && diff_cache_active(d, np)) {
     // five to eight windows at some station of the tile (a region that has
     // accepted several births this phase, as during burn-in from an empty
@@ -869,10 +862,7 @@ __device__ __forceinline__ void score_item(const Dev& d, const Prop& P, const Pa
                                            int tile, int np, const int* pold,
                                            const int* pnew, const DiffW& X, bool haveX,
                                            const double2* Ts,
-                                           double& sig, double& arr, int& cnt,
-                                           const double* stg = nullptr,
-                                           const double* stg_r = nullptr,
-                                           Win* defer_w = nullptr) {
+                                           double& sig, double& arr, int& cnt) {
   if (P.skip) return;
   const int j = tile * 32 + (threadIdx.x & 31);
   if (MODE == 0 && P.type == 3) {
@@ -881,17 +871,13 @@ __device__ __forceinline__ void score_item(const Dev& d, const Prop& P, const Pa
   }
   const int shape = P.nr * 3 + P.na;
   if (shape == 1)  // birth
-    station_item<0, 1, YT, GEN>(d, P, in, j, np, pold, pnew, X, haveX, Ts, sig, arr, cnt, stg,
-                                stg_r, defer_w);
+    station_item<0, 1, YT, GEN>(d, P, in, j, np, pold, pnew, X, haveX, Ts, sig, arr, cnt);
   else if (shape == 3)  // death
-    station_item<1, 0, YT, GEN>(d, P, in, j, np, pold, pnew, X, haveX, Ts, sig, arr, cnt, stg,
-                                stg_r, defer_w);
+    station_item<1, 0, YT, GEN>(d, P, in, j, np, pold, pnew, X, haveX, Ts, sig, arr, cnt);
   else if (shape == 4)  // location / arrival
-    station_item<1, 1, YT, GEN>(d, P, in, j, np, pold, pnew, X, haveX, Ts, sig, arr, cnt, stg,
-                                stg_r, defer_w);
+    station_item<1, 1, YT, GEN>(d, P, in, j, np, pold, pnew, X, haveX, Ts, sig, arr, cnt);
   else  // joint pair, and any other change of <= 2 removed / 2 added events
-    station_item<2, 2, YT, GEN>(d, P, in, j, np, pold, pnew, X, haveX, Ts, sig, arr, cnt, stg,
-                                stg_r, defer_w);
+    station_item<2, 2, YT, GEN>(d, P, in, j, np, pold, pnew, X, haveX, Ts, sig, arr, cnt);
 }
 
 }  // namespace seis

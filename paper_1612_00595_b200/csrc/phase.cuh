@@ -237,12 +237,6 @@ __global__ void __launch_bounds__(NTT, MINB)
   // tile-major pass (never together with the diff-window cache): one flag per
   // station tile in its place (region chains only)
   unsigned char* const tile_nw = reinterpret_cast<unsigned char*>(dcache);
-  // ... and after the flags the warps' cp.async stage buffers
-  double* const stage = reinterpret_cast<double*>(
-      tile_nw + min(kTileFlags, ((d.S_pad + 31) / 32 + 15) & ~15));
-  __shared__ int s_stage_slot[NWT][kStageRows];
-  // ... and the warps' cached-term row buffers (tile-major pass)
-  double* const tbuf = stage + (kStageOn ? kStageBytes / 8 : 0);
   // serial layout in dynamic smem: own | st | log i | pold | pnew | lfree | cur_of
   char* const big = reinterpret_cast<char*>(dcache);
   constexpr size_t kOffSt = CAP * sizeof(OwnEv), kOffLogi = kOffSt + CAP * sizeof(StartEv);
@@ -496,6 +490,9 @@ __global__ void __launch_bounds__(NTT, MINB)
         // a round whose proposals are all skipped (null, constrained out)
         // visits no tile; production arrival moves alone visit only tile 0
         bool any_dense = false, any_arr = false;
+        // every scored proposal a production birth or death of a stored /
+        // generated version whose arrivals a lane can compute: tile pairs
+        bool pair_round = kPairOn && MODE == 0 && d.tpos != nullptr;
         for (int q = 0; q < m; ++q) {
           const Prop& P = prop[buf][q];
           if (P.skip) continue;
@@ -503,73 +500,23 @@ __global__ void __launch_bounds__(NTT, MINB)
             any_arr = true;
           else
             any_dense = true;
+          if (!(P.type == 0 || (P.type == 1 && (!GEN || P.rslot[0] >= 0)))) pair_round = false;
         }
+        pair_round = pair_round && any_dense;
         const int tile_end = any_dense ? T_per : (any_arr ? 1 : 0);
         const bool tw_ok = !kBig && T_per <= kTileFlags;
         const bool tw_fresh = tw_ok && any_dense && !tw_dirty;
-        // cp.async staging of the next tile's inputs (region chains with the
-        // flag area; kernels.cuh): the staged slot of each buffer row, -1 = none
-        const bool stage_on = tw_ok && kStageOn;
-        double* const stg_w = stage + (size_t)warp * 2 * kStageRows * 32 + lane;
-        if (stage_on) {
-          if (lane < kStageRows) {
-            int vslot = -1;
-            if (lane >= 1 && lane <= 4) {
-              const int pr = (lane - 1) >> 1;
-              if (pr < np_now) vslot = ((lane - 1) & 1) ? pnew[pr] : pold[pr];
-            } else if (lane >= 5 && lane - 5 < m) {
-              const Prop& P = prop[buf][lane - 5];
-              if (!P.skip && P.nr >= 1 && !(MODE == 0 && P.type == 3)) vslot = P.rslot[0];
-            }
-            s_stage_slot[warp][lane] = vslot < 0 ? -1 : vslot;  // stored rows only
-          }
-          __syncwarp();
-        }
-        auto stage_issue = [&](int tt, int bi) {
-          const int jj = tt * 32 + lane;
-          double* dst = stg_w + bi * kStageRows * 32;
-          cp_async8(dst, d.stations + jj);
-#pragma unroll
-          for (int k = 1; k < kStageRows; ++k) {
-            const int sl = s_stage_slot[warp][k];
-            if (sl >= 0) cp_async8(dst + k * 32, d.pool + (size_t)sl * d.S_pad + jj);
-          }
-          cp_async_commit();
-        };
-        // cached-term bands one item late: the rows of a birth's / death's
-        // window are copied to the warp's buffer with cp.async when its
-        // window is known and summed after the next item's setup, so their
-        // L2 / HBM latency runs under that setup
-        const bool tbuf_on = !kBig && kTermBuf && d.tpos != nullptr;
-        double* const tb = tbuf + (size_t)warp * kTermRows * 32 + lane;
-        int pend_q = -1, pend_len = 0;
-        auto drain = [&]() {
-          double s2 = 0.0;
-          cp_async_wait<0>();
-#pragma unroll
-          for (int k = 0; k < kTermRows; ++k) s2 += k < pend_len ? tb[k * 32] : 0.0;
-          acc_sig[pend_q][tid] += s2;
-          pend_q = -1;
-        };
-        // Tile pairs: when every scored proposal of the round is a production
-        // birth or death and the region's diff has no window on two of the
-        // warp's tiles, both are scored together (dense_pair_terms): two
-        // independent setup chains and twice the cached-term loads in flight
-        bool pair_round = kPairOn && !stage_on && !tbuf_on && MODE == 0 && any_dense &&
-                          d.tpos != nullptr;
-        for (int q = 0; q < m && pair_round; ++q) {
-          const Prop& P = prop[buf][q];
-          if (P.skip) continue;
-          if (!(P.type == 0 || (P.type == 1 && (!GEN || P.rslot[0] >= 0)))) pair_round = false;
-        }
-        int sbuf = 0;
-        if (stage_on && warp < tile_end) stage_issue(warp, 0);
-        int tstep = NWT;
-        for (int tile = warp; tile < tile_end; tile += tstep, sbuf ^= 1) {
-          tstep = NWT;
-          if (pair_round && tile + NWT < tile_end &&
-              (np_now == 0 || (tw_fresh && tile_nw[tile] == 0 && tile_nw[tile + NWT] == 0))) {
-            const int jA = tile * 32 + lane, jB = jA + NWT * 32;
+        // A warp owns pairs of neighbouring station tiles (2u, 2u + 1), u =
+        // warp, warp + NWT, ...: 64 consecutive stations, whose birth normals
+        // come from 32 Philox calls, one per lane (dense_pair_terms).
+        for (int u = warp; 2 * u < tile_end; u += NWT) {
+          const int t0 = 2 * u;
+          // Tile pairs: when every scored proposal of the round is a production
+          // birth or death and the region's diff has no window on either tile,
+          // both are scored together: two independent setup chains and twice
+          // the cached-term rows in flight
+          if (pair_round && t0 + 1 < tile_end &&
+              (np_now == 0 || (tw_fresh && tile_nw[t0] == 0 && tile_nw[t0 + 1] == 0))) {
 #pragma unroll 1
             for (int q = 0; q < m; ++q) {
               const Prop& P = prop[buf][q];
@@ -584,105 +531,74 @@ __global__ void __launch_bounds__(NTT, MINB)
               double sA = 0.0, sB = 0.0, aA = 0.0, aB = 0.0;
               int cnt = 0;
               if (P.type == 0)
-                dense_pair_terms<true>(d, P, in, jA, jB, sA, sB, aA, aB, cnt);
+                dense_pair_terms<true>(d, P, in, t0 * 32, sA, sB, aA, aB, cnt);
               else
-                dense_pair_terms<false>(d, P, in, jA, jB, sA, sB, aA, aB, cnt);
+                dense_pair_terms<false>(d, P, in, t0 * 32, sA, sB, aA, aB, cnt);
               acc_sig[q][tid] = (acc_sig[q][tid] + sA) + sB;  // tile order
               acc_arr[q][tid] = (acc_arr[q][tid] + aA) + aB;
               acc_cnt[q][tid] += cnt;
             }
-            tstep = 2 * NWT;
             continue;
           }
-          DiffW X;
-          long long tq = kProfItems ? clock64() : 0;
-          const double* stg = nullptr;
-          if (stage_on) {
-            if (tile + NWT < tile_end) {
-              stage_issue(tile + NWT, sbuf ^ 1);
-              cp_async_wait<1>();
-            } else {
-              cp_async_wait<0>();
-            }
-            stg = stg_w + sbuf * kStageRows * 32;
-          }
-          // tiles where the region's diff has no effective window (e.g. only
-          // arrival moves at other stations were accepted) stay so until the
-          // next accept: remembered per tile, the pair walk is skipped
-          if (np_now == 0 || (tw_fresh && tile_nw[tile] == 0)) {
-            X.nwmax = 0;
-          } else {
-            diff_windows<GEN>(d, tile * 32 + lane, np_now, pold, pnew, X, stg);
-            if (tw_ok && any_dense && lane == 0) tile_nw[tile] = (unsigned char)min(X.nwmax, 255);
-          }
-          if (kProfItems) {
-            __syncwarp();
-            const long long now = clock64();
-            if (lane == 0) {
-              atomicAdd(&s_tprof[0][5], (unsigned long long)(now - tq));
-              atomicAdd(&s_tprof[1][5], 1ull);
-            }
-            tq = now;
-          }
+          const int t1 = min(t0 + 2, tile_end);
 #pragma unroll 1
-          for (int q = 0; q < m; ++q) {
-            const Prop& P = prop[buf][q];
-            if (P.skip) continue;
-            if (MODE == 0 && P.type == 3 && tile != 0) continue;
-            PassIn in;
-            in.src = P.na == 0 ? SRC_NONE
-                               : (MODE == 1 ? SRC_ROWS : (P.type == 0 ? SRC_BIRTH : SRC_SHIFT));
-            in.rows[0] = pa.tape_arr + (MODE == 1 ? P.tape_off : 0);
-            in.rows[1] = in.rows[0] + d.S;
-            in.seed = sp.seed;
-            in.sweep = (uint32_t)pa.epoch;
-            in.region = (uint32_t)region;
-            in.step = (uint32_t)(pa.step_base + i0 + q);
-            in.wlo = win_lo;
-            in.whi = win_hi;
-            double sig = 0.0, arr = 0.0;
-            int cnt = 0;
-            const double* stg_r =
-                (stg && q < kStageRows - 5 && s_stage_slot[warp][5 + q] >= 0)
-                    ? stg + (5 + q) * 32
-                    : nullptr;
-            Win dw;
-            dw.lo = -1;
-            score_item<MODE, YT, GEN>(d, P, in, tile, np_now, pold, pnew, X, true, Ts, sig, arr,
-                                      cnt, stg, stg_r, tbuf_on ? &dw : nullptr);
-            if (tbuf_on && dw.lo >= 0) {  // (uniform) a dense band over cached terms
-              const int len = dw.hi - dw.lo;
-              const int j = tile * 32 + lane;
-              if (__all_sync(0xffffffffu, len <= kTermRows)) {
-                if (pend_q >= 0) drain();
-                const double* src = (P.na ? d.tpos : d.tneg) + yix(d.rows, dw.lo, j);
-#pragma unroll
-                for (int k = 0; k < kTermRows; ++k)
-                  if (k < len) cp_async8(tb + k * 32, src + k * 32);
-                cp_async_commit();
-                pend_q = q;
-                pend_len = len;
-              } else if (P.na) {
-                band1_terms<1>(d, j, dw, sig);
-              } else {
-                band1_terms<-1>(d, j, dw, sig);
-              }
+          for (int tile = t0; tile < t1; ++tile) {
+            DiffW X;
+            long long tq = kProfItems ? clock64() : 0;
+            // tiles where the region's diff has no effective window (e.g. only
+            // arrival moves at other stations were accepted) stay so until the
+            // next accept: remembered per tile, the pair walk is skipped
+            if (np_now == 0 || (tw_fresh && tile_nw[tile] == 0)) {
+              X.nwmax = 0;
+            } else {
+              diff_windows<GEN>(d, tile * 32 + lane, np_now, pold, pnew, X);
+              if (tw_ok && any_dense && lane == 0)
+                tile_nw[tile] = (unsigned char)min(X.nwmax, 255);
             }
-            // per-lane partial sums; the warp reduces them once per round
-            acc_sig[q][tid] += sig;
-            acc_arr[q][tid] += arr;
-            acc_cnt[q][tid] += cnt;
             if (kProfItems) {
+              __syncwarp();
               const long long now = clock64();
               if (lane == 0) {
-                atomicAdd(&s_tprof[0][P.type], (unsigned long long)(now - tq));
-                atomicAdd(&s_tprof[1][P.type], 1ull);
+                atomicAdd(&s_tprof[0][5], (unsigned long long)(now - tq));
+                atomicAdd(&s_tprof[1][5], 1ull);
               }
               tq = now;
             }
+#pragma unroll 1
+            for (int q = 0; q < m; ++q) {
+              const Prop& P = prop[buf][q];
+              if (P.skip) continue;
+              if (MODE == 0 && P.type == 3 && tile != 0) continue;
+              PassIn in;
+              in.src = P.na == 0 ? SRC_NONE
+                                 : (MODE == 1 ? SRC_ROWS : (P.type == 0 ? SRC_BIRTH : SRC_SHIFT));
+              in.rows[0] = pa.tape_arr + (MODE == 1 ? P.tape_off : 0);
+              in.rows[1] = in.rows[0] + d.S;
+              in.seed = sp.seed;
+              in.sweep = (uint32_t)pa.epoch;
+              in.region = (uint32_t)region;
+              in.step = (uint32_t)(pa.step_base + i0 + q);
+              in.wlo = win_lo;
+              in.whi = win_hi;
+              double sig = 0.0, arr = 0.0;
+              int cnt = 0;
+              score_item<MODE, YT, GEN>(d, P, in, tile, np_now, pold, pnew, X, true, Ts, sig, arr,
+                                        cnt);
+              // per-lane partial sums; the warp reduces them once per round
+              acc_sig[q][tid] += sig;
+              acc_arr[q][tid] += arr;
+              acc_cnt[q][tid] += cnt;
+              if (kProfItems) {
+                const long long now = clock64();
+                if (lane == 0) {
+                  atomicAdd(&s_tprof[0][P.type], (unsigned long long)(now - tq));
+                  atomicAdd(&s_tprof[1][P.type], 1ull);
+                }
+                tq = now;
+              }
+            }
           }
         }
-        if (pend_q >= 0) drain();
         for (int q = 0; q < m; ++q) {
           const double sg = warp_sum(acc_sig[q][tid]);
           const double ar = warp_sum(acc_arr[q][tid]);

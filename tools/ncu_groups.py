@@ -4,20 +4,66 @@
 import csv
 import sys
 
-G = [("kernels.cuh", 307, 334, "band1_terms (cached terms)"),
-     ("kernels.cuh", 239, 299, "band1 (dense band, own diff)"), ("kernels.cuh", 151, 222, "band"),
-     ("kernels.cuh", 341, 414, "edges"), ("kernels.cuh", 418, 452, "band_generic"),
-     ("kernels.cuh", 453, 586, "diff windows"), ("kernels.cuh", 587, 771, "station_item setup"),
-     ("kernels.cuh", 772, 804, "arrival_item"), ("kernels.cuh", 805, 840, "score_item dispatch"),
-     ("kernels.cuh", 1, 150, "kernels.cuh helpers (term, warp_sum, cp.async)"),
-     ("seis_philox.h", 1, 400, "philox + Box-Muller"), ("engine.cuh", 278, 287, "make_win"),
-     ("engine.cuh", 296, 299, "inw"), ("engine.cuh", 288, 295, "yix/pix"),
-     ("engine.cuh", 306, 313, "arrival_mean / div_v"), ("engine.cuh", 314, 336, "ver_arr / arr_of"),
-     ("engine.cuh", 337, 350, "arr_logpdf"), ("phase.cuh", 485, 640, "tile-major loop"),
-     ("phase.cuh", 641, 713, "proposal-major loop"), ("phase.cuh", 16, 205, "gen_proposal"),
-     ("phase.cuh", 206, 412, "k_phase prologue"), ("phase.cuh", 413, 484, "round head"),
-     ("phase.cuh", 714, 1015, "decision"), ("phase.cuh", 1016, 1102, "write-back"),
-     ("phase.cuh", 1103, 1200, "phase outputs")]
+import os
+import re
+
+CSRC = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "paper_1612_00595_b200", "csrc")
+# (file, first line of the region as a regex, label): a region runs to the next marker of its file
+MARKS = [
+    ("kernels.cuh", r"^struct Y2;", "kernels.cuh helpers (term, warp_sum)"),
+    ("kernels.cuh", r"void band\(const Dev", "band (generic rows)"),
+    ("kernels.cuh", r"void band1\(const Dev", "band1 (dense band, own diff)"),
+    ("kernels.cuh", r"void band1_terms\(", "band1_terms (cached terms)"),
+    ("kernels.cuh", r"void dense_pair_terms\(", "dense_pair_terms (tile pairs, cached terms)"),
+    ("kernels.cuh", r"void edges\(const Dev", "edges"),
+    ("kernels.cuh", r"void band_generic\(", "band_generic"),
+    ("kernels.cuh", r"^struct DiffW", "diff windows"),
+    ("kernels.cuh", r"void station_item\(", "station_item setup"),
+    ("kernels.cuh", r"void arrival_item\(", "arrival_item"),
+    ("kernels.cuh", r"void score_item\(", "score_item dispatch"),
+    ("engine.cuh", r"Win make_win\(", "make_win"),
+    ("engine.cuh", r"size_t yix\(", "yix/pix"),
+    ("engine.cuh", r"int inw\(", "inw"),
+    ("engine.cuh", r"double div_v\(", "arrival_mean / div_v"),
+    ("engine.cuh", r"double gen_arrival\(", "ver_arr / arr_of"),
+    ("engine.cuh", r"double arr_logpdf\(", "arr_logpdf"),
+    ("phase.cuh", r"^__device__ void gen_proposal", "gen_proposal"),
+    ("phase.cuh", r"k_phase\(const Dev d", "k_phase prologue"),
+    ("phase.cuh", r"for \(int i0 = 0; i0 < \(int\)sp.k; \+\+round\)", "round head"),
+    ("phase.cuh", r"if constexpr \(TM\) \{", "tile-major loop"),
+    ("phase.cuh", r"int cur_q = -1;", "proposal-major loop"),
+    ("phase.cuh", r"// S2: partial sums ready", "decision"),
+    ("phase.cuh", r"// S3: decision", "write-back"),
+    ("phase.cuh", r"// ---- phase outputs", "phase outputs"),
+]
+
+
+def build_groups():
+    out = []
+    by_file = {}
+    for f, rx, label in MARKS:
+        by_file.setdefault(f, []).append((rx, label))
+    for f, marks in by_file.items():
+        path = os.path.join(CSRC, f)
+        if not os.path.exists(path):
+            continue
+        lines = open(path).read().split("\n")
+        starts = []
+        for rx, label in marks:
+            for i, line in enumerate(lines, 1):
+                if re.search(rx, line):
+                    starts.append((i, label))
+                    break
+        starts.sort()
+        for k, (ln, label) in enumerate(starts):
+            # a function's template / comment header sits just above its first line
+            hi = starts[k + 1][0] - 1 if k + 1 < len(starts) else len(lines)
+            out.append((f, ln, hi, label))
+    out.append(("seis_philox.h", 1, 100000, "philox + Box-Muller"))
+    return out
+
+
+G = build_groups()
 rows = list(csv.reader(open(sys.argv[1])))
 f, hdr = None, None
 acc = {g[3]: [0, 0] for g in G}
