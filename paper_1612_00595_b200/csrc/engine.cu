@@ -719,9 +719,20 @@ static_assert(kPhaseSmemTM + 48 * 1024 <= 227 * 1024, "k_phase shared memory");
 // the diff-window cache, so its launches leave that shared memory to L1: the
 // band rows a warp's proposals share on a tile stay resident between them.
 // SEIS_SMEM_FULL=1 keeps the full allocation (A/B).
+// The item order of a launch: tile-major (rounds that end at their first
+// scored proposal, tile pairs on cached terms) from kTileMajorTiles station
+// tiles on; below that the proposal-major pass with speculative rounds spreads
+// the few (proposal, tile) items over the warps better. SEIS_TM_MIN_TILES
+// overrides the threshold (A/B).
+constexpr int kTileMajorTiles = SEIS_TM_TILES;
+inline bool tile_major(const Dev& d) {
+  static const int min_tiles =
+      getenv("SEIS_TM_MIN_TILES") ? atoi(getenv("SEIS_TM_MIN_TILES")) : kTileMajorTiles;
+  return (d.S_pad + 31) / 32 >= min_tiles;
+}
 inline int phase_smem(const Dev& d) {
   static const bool full = getenv("SEIS_SMEM_FULL") && atoi(getenv("SEIS_SMEM_FULL")) == 1;
-  const bool dcache = (d.S_pad + 31) / 32 < 4 * NW && d.S_pad <= kDiffCache && d.n < 65535;
+  const bool dcache = d.dcache_on != 0;
   // tile-major: + one flag byte per station tile
   return (dcache || full) ? kPhaseSmem
                           : kPhaseSmemTile + std::min(kTileFlags, (d.S_pad / 32 + 15) & ~15);
@@ -996,9 +1007,6 @@ int refresh_terms(seis_engine* e) {
   return 1;
 }
 
-// the item order of a launch: tile-major from 4 station tiles per warp on
-inline bool tile_major(const Dev& d) { return (d.S_pad + 31) / 32 >= 4 * NW; }
-
 template <typename YT, int MODE, bool TM>
 void launch_phase_tm(seis_engine* e, int ncr, const Samp& sp, const PhaseArgs& pa, int stamp) {
   const bool rows_only = MODE == 0 && !pa.serial && !e->compact && !e->gen_present;
@@ -1232,6 +1240,7 @@ int seis_engine_create(const seis_model_cfg* cfg, const double* stations, int64_
     d.gv = e->gv;
     d.gv_free = e->gv_free;
     d.gv_cap = e->gv_cap;
+    d.dcache_on = (!tile_major(d) && d.S_pad <= kDiffCache && d.n < 65535) ? 1 : 0;
     set_phase_attrs<float, 0>();
     set_phase_attrs<float, 1>();
     set_phase_attrs<double, 0>();

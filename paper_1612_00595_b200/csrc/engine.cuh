@@ -76,6 +76,9 @@ __host__ __device__ __forceinline__ size_t diff_off(const Ovf& o, int n_slots, i
 #define SEIS_TBL 512
 #endif
 constexpr int TBL = SEIS_TBL;    // coverage counts whose {dL, dI} rows live in smem
+#ifndef SEIS_TM_TILES
+#define SEIS_TM_TILES (4 * NW)
+#endif
 constexpr int kDiffCache = 2048;  // stations whose round diff windows k_phase caches in smem
 constexpr int kTileFlags = 24576;  // station tiles whose diff flags the tile-major pass keeps
 #ifndef SEIS_PAIR
@@ -154,6 +157,7 @@ struct Dev {
   int logi_n;
   int pool_cap;
   int gv_cap;
+  int dcache_on;  // proposal-major launches keep the round's diff windows in shared memory
 };
 
 struct Samp {

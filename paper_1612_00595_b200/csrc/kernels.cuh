@@ -623,7 +623,7 @@ __device__ __forceinline__ void diff_station(const Dev& d, int j, int np, const 
 // the same condition k_phase builds it; the overflow windows follow the
 // cache in dynamic shared memory
 __device__ __forceinline__ bool diff_cache_active(const Dev& d, int np) {
-  return np > 0 && (d.S_pad + 31) / 32 < 4 * (NT / 32) && d.S_pad <= kDiffCache && d.n < 65535;
+  return np > 0 && d.dcache_on != 0;
 }
 __device__ __forceinline__ const DiffS4x* diff_cache_overflow() {
   extern __shared__ double s_dyn_diff[];

@@ -429,7 +429,7 @@ __global__ void __launch_bounds__(NTT, MINB)
     // the round's diff windows per station (proposal-major pass): rebuilt only
     // after an accept changed the region's diff, alongside generation
     const bool use_dcache =
-        !TM && !kBig && (d.S_pad + 31) / 32 < 4 * NWT && d.S_pad <= kDiffCache && d.n < 65535;
+        !TM && !kBig && d.dcache_on != 0;
     const bool dc_build = use_dcache && s_np > 0 && s_dc_dirty;
     const bool tw_dirty = s_tw_dirty != 0;  // per-tile diff flags of the tile-major pass
     if (warp < m && lane == 0 && !(MODE == 0 && s_specok)) {  // one lane per warp: move types do not diverge
