@@ -40,16 +40,16 @@ NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", 
 MAXOWN, SERIAL_CAP = 64, 1024  # engine.cuh (checked by a static_assert in phase_inst.cu)
 
 
-def phase_variants(fast: bool):
+def phase_variants(fast: bool, maxown: int = MAXOWN):
     """(YT, MODE, CAP, GEN, TM) of every k_phase instantiation engine.cu launches"""
     out = []
     for yt in ("float",) if fast else ("float", "double"):
         for tm in (1, 0):
-            out.append((yt, 0, MAXOWN, 0, tm))
+            out.append((yt, 0, maxown, 0, tm))
             if fast:
                 continue
             for mode in (0, 1):
-                out.append((yt, mode, MAXOWN, 1, tm))
+                out.append((yt, mode, maxown, 1, tm))
                 out.append((yt, mode, SERIAL_CAP, 1, tm))
     return out
 
@@ -92,7 +92,11 @@ def build(force: bool = False, verbose: bool = False, defs=(), fast: bool = Fals
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
         jobs.append((obj, [nvcc(), *NVCC_FLAGS, *defs, *inc, "-c", src, "-o", obj],
                      [src] + HEADERS))
-    for yt, mode, cap, gen, tm in phase_variants(fast):
+    maxown = MAXOWN
+    for d_ in defs:  # -DSEIS_MAXOWN=N (A/B builds) changes the region chains' capacity
+        if d_.startswith("-DSEIS_MAXOWN="):
+            maxown = int(d_.split("=")[1])
+    for yt, mode, cap, gen, tm in phase_variants(fast, maxown):
         obj = os.path.join(objdir, f"phase_{yt}_m{mode}_c{cap}_g{gen}_t{tm}.o")
         inst = [f"-DINST_YT={yt}", f"-DINST_MODE={mode}", f"-DINST_CAP={cap}",
                 f"-DINST_GEN={gen}", f"-DINST_TM={tm}"]

@@ -40,7 +40,10 @@ constexpr bool kProfItems = SEIS_PROF_ITEMS;
 #define SEIS_MINB 1  // k_phase CTAs per SM the register budget is cut for
 #endif
 constexpr int NW = NT / 32;
-constexpr int MAXOWN = 64;       // events a region may hold during a phase
+#ifndef SEIS_MAXOWN
+#define SEIS_MAXOWN 64
+#endif
+constexpr int MAXOWN = SEIS_MAXOWN;  // events a region may hold during a phase (build.py passes the same)
 constexpr int kMaxEvents = 1 << 22;  // event_capacity bound (table sizes; counts stay uint16)
 constexpr int MAXDIFF = 2 * MAXOWN;  // diff pairs a region may hold
 constexpr int MAXDOUT = 3 * MAXOWN;  // diff pairs + recycled slots per region

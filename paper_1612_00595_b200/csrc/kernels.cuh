@@ -340,7 +340,13 @@ template <bool BIRTH>
 __device__ __forceinline__ void dense_pair_terms(const Dev& d, const Prop& P, const PassIn& in,
                                                  int j0, double& sigA, double& sigB,
                                                  double& arrA, double& arrB, int& cnt) {
-  constexpr int H = SEIS_BAND_RU / 2;
+#ifndef SEIS_PAIR_H
+#define SEIS_PAIR_H SEIS_BAND_RU  // rows per tile and batch: both windows' 40 rows in flight at once
+                                  // (10 rows per tile and batch: -2.6 %, 5: the same)
+#endif
+  constexpr int H = SEIS_PAIR_H;
+  constexpr int NB = SEIS_BAND_RU / H;
+  static_assert(NB * H == SEIS_BAND_RU, "batches cover the window");
   const int lane = threadIdx.x & 31;
   const int jA = j0 + lane, jB = jA + 32;
   const bool vA = jA < d.S, vB = jB < d.S;
@@ -371,12 +377,12 @@ __device__ __forceinline__ void dense_pair_terms(const Dev& d, const Prop& P, co
   arrB = BIRTH ? lB : 0.0 - lB;
   const int lenA = WA.hi - WA.lo, lenB = WB.hi - WB.lo;
   cnt += lenA + lenB;
-  if (__all_sync(0xffffffffu, lenA == 2 * H && lenB == 2 * H)) {
+  if (__all_sync(0xffffffffu, lenA == NB * H && lenB == NB * H)) {
     const double* __restrict__ tA = (BIRTH ? d.tpos : d.tneg) + yix(d.rows, WA.lo, jA);
     const double* __restrict__ tB = (BIRTH ? d.tpos : d.tneg) + yix(d.rows, WB.lo, jB);
     double a = 0.0, b = 0.0;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < NB; ++h) {
       double v[2 * H];
 #pragma unroll
       for (int k = 0; k < H; ++k) {
