@@ -1684,19 +1684,23 @@ int seis_log_joint(seis_engine* e, double* out) {
 // constraint, chunks of record_every steps.
 // Speculative proposals per round (1..MSPEC); SEIS_SPEC overrides the
 // default depth for A/B measurements.
-static int spec_depth() {
+static int spec_depth(const seis_engine* e) {
   const char* v = getenv("SEIS_SPEC");
-  const int m = v ? atoi(v) : kSpecDefault;
+  // proposals generated per round: 3 scored speculatively (proposal-major), 4
+  // of which a tile-major round scores a prefix (first_scored)
+  const int m = v ? atoi(v) : (tile_major(e->d) ? MSPEC : kSpecDefault);
   return m < 1 ? 1 : (m > MSPEC ? MSPEC : m);
 }
-// Rounds that stop at their first scored proposal: the default of tile-major
-// launches (config[2]: 3.70 M -> proposals/s with three proposals scored per
-// round, measured against SEIS_FIRST=0); SEIS_FIRST overrides (A/B).
+// Rounds that stop at their first scored proposal, births and deaths taking
+// the next one along: the default of tile-major launches (config[2], one
+// B200: three proposals scored per round 3.70 M proposals/s, rounds ending at
+// the first scored one 3.88 M; with tile pairs: 4.34 M, births / deaths taking
+// one more along 4.57 M, as many as the batch of four holds 4.66 M);
+// SEIS_FIRST = 0 / 1 / 2 / 3 overrides (A/B).
 static int first_scored(const seis_engine* e) {
-  if (const char* v = getenv("SEIS_FIRST")) return atoi(v) != 0;
-  return tile_major(e->d) ? 1 : 0;
+  if (const char* v = getenv("SEIS_FIRST")) return atoi(v);
+  return tile_major(e->d) ? 3 : 0;
 }
-
 static int run_driver(seis_engine* e, const seis_sampler_cfg* sc, int32_t mode,
                       const seis_tape_step* tape, int64_t n_tape, const double* tape_arr,
                       int64_t n_tape_arr, seis_step_out* step_out, int64_t row_cap,
@@ -1757,7 +1761,7 @@ static int run_driver(seis_engine* e, const seis_sampler_cfg* sc, int32_t mode,
     sp.step_joint = sc->step_joint;
     sp.joint_t_sd = sc->step_joint / e->cfg.v;
     sp.ncol = ncol;
-    sp.mspec = spec_depth();
+    sp.mspec = spec_depth(e);
     sp.first_scored = first_scored(e);
     const int bcap = (int)sc->n_regions + 4;
     // the timed region starts before the partition kernel: everything the run
@@ -2207,7 +2211,7 @@ extern "C" int seis_run_naive(seis_engine* e, const seis_sampler_cfg* sc, int32_
     sp.step_joint = sc->step_joint;
     sp.joint_t_sd = sc->step_joint / e->cfg.v;
     sp.ncol = 1;
-    sp.mspec = spec_depth();
+    sp.mspec = spec_depth(e);
     sp.first_scored = first_scored(e);
     // every region of the one launch may outgrow MAXOWN events (long chains
     // from the empty start): an overflow area each, up to 32768 regions

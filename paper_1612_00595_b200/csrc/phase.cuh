@@ -459,12 +459,24 @@ __global__ void __launch_bounds__(NTT, MINB)
     __syncthreads();  // S1: proposals (and diff windows) ready
     // first_scored: the round ends with its first proposal that needs scoring
     // (the skipped ones before it are rejected for free, the ones after it
-    // are regenerated): no proposal is ever scored and then discarded, while
-    // generation stays parallel. Pays where a round's items are long
-    // (tile-major launches); speculation pays where they are short.
+    // are regenerated), except that births and deaths, which are rarely
+    // accepted, take the batch's next scored proposal along (2: one more, 3:
+    // as long as they are births or deaths). Almost nothing scored is
+    // discarded (config[2]: 1 % of the steps), generation stays parallel, and
+    // a round's fixed cost (barriers, decision) is shared where that is
+    // safe. Pays where a round's items are long (tile-major launches);
+    // plain speculation pays where they are short.
     if (sp.first_scored) {
       int f = 0;
       while (f < m - 1 && prop[buf][f].skip) ++f;
+      // first_scored = 2: a birth or death (rarely accepted) takes the next
+      // scored proposal of the batch along
+      int more = sp.first_scored - 1;  // 2: one more, 3: as long as they are births / deaths
+      while (more > 0 && f < m - 1 && !prop[buf][f].skip && prop[buf][f].type <= 1) {
+        ++f;
+        while (f < m - 1 && prop[buf][f].skip) ++f;
+        if (sp.first_scored == 2) --more;
+      }
       m = f + 1;
     }
     if (tid == 0) {

@@ -567,7 +567,8 @@ def test_tile_major_fast_paths_equal_the_direct_paths(E, oc, monkeypatch, toggle
     """The tile-major pass's shortcuts must not change a result: the per-sample
     term cache (k_terms, summed by band1_terms / dense_pair_terms instead of
     the direct band; SEIS_TERMS=0 disables it) and rounds that end at their
-    first scored proposal (SEIS_FIRST=0: three proposals scored per round).
+    first scored proposal, births and deaths taking the next ones along
+    (SEIS_FIRST=0: three proposals scored per round).
     With the shortcut off and on: every delta and decision bit-identical
     (same operations in the same order), the final hypothesis identical, and
     both equal to the oracle (density.hpp:214-305, samplers.hpp:115-138)."""
@@ -576,11 +577,17 @@ def test_tile_major_fast_paths_equal_the_direct_paths(E, oc, monkeypatch, toggle
     w32 = O.World(m, w.events, w.signals.astype(np.float32).astype(np.float64))
     s = O.Sampler(steps_per_epoch=20, epochs=2, n_regions=12, seed=33, dynamic=1, rng_mode=1)
     outs = []
-    for val in ("0", "1"):
+    # SEIS_FIRST: 0 = three proposals scored per round, 1 = rounds end at the
+    # first scored one, 2 / 3 = births and deaths take one more / as many as
+    # the batch holds along (3 is the tile-major default)
+    for val in ("0", "1") if toggle == "SEIS_TERMS" else ("0", "1", "2", "3"):
         monkeypatch.setenv(toggle, val)
         tr, ro = _prod_vs_oracle(E, oc, m, w32, s, init=w.events, dtype=np.float32)
         outs.append(tr)
-    a, b = outs
+    a, b = outs[0], outs[-1]
+    for o in outs[1:]:
+        assert np.array_equal(a.step_out["accepted"], o.step_out["accepted"])
+        assert np.array_equal(a.final.arrivals, o.final.arrivals)
     assert np.array_equal(a.step_out["accepted"], b.step_out["accepted"])
     if toggle == "SEIS_TERMS":  # same operations in the same order
         assert np.array_equal(a.step_out["delta"], b.step_out["delta"])
