@@ -1684,22 +1684,28 @@ int seis_log_joint(seis_engine* e, double* out) {
 // constraint, chunks of record_every steps.
 // Speculative proposals per round (1..MSPEC); SEIS_SPEC overrides the
 // default depth for A/B measurements.
+// Rounds that score a prefix of their batch (first_scored) from 16 station
+// tiles on; below that (config[0]: 4 tiles, rounds of a few microseconds)
+// plain speculation over three proposals is faster (1.80 M against 1.48 M
+// proposals/s at config[0]; config[1], 50 tiles: 9.74 M against 10.05 M).
+static bool round_prefix(const seis_engine* e) { return (e->S_pad + 31) / 32 >= 16; }
 static int spec_depth(const seis_engine* e) {
   const char* v = getenv("SEIS_SPEC");
   // proposals generated per round: 3 scored speculatively (proposal-major), 4
   // of which a tile-major round scores a prefix (first_scored)
-  const int m = v ? atoi(v) : (tile_major(e->d) ? MSPEC : kSpecDefault);
+  const int m = v ? atoi(v) : (round_prefix(e) ? MSPEC : kSpecDefault);
   return m < 1 ? 1 : (m > MSPEC ? MSPEC : m);
 }
 // Rounds that stop at their first scored proposal, births and deaths taking
-// the next one along: the default of tile-major launches (config[2], one
+// the next one along (unless the chain accepts them often, phase.cuh s_bd_hot):
+// the default from 16 station tiles on (config[2], one
 // B200: three proposals scored per round 3.70 M proposals/s, rounds ending at
 // the first scored one 3.88 M; with tile pairs: 4.34 M, births / deaths taking
 // one more along 4.57 M, as many as the batch of four holds 4.66 M);
 // SEIS_FIRST = 0 / 1 / 2 / 3 overrides (A/B).
 static int first_scored(const seis_engine* e) {
   if (const char* v = getenv("SEIS_FIRST")) return atoi(v);
-  return tile_major(e->d) ? 3 : 0;
+  return round_prefix(e) ? 3 : 0;
 }
 static int run_driver(seis_engine* e, const seis_sampler_cfg* sc, int32_t mode,
                       const seis_tape_step* tape, int64_t n_tape, const double* tape_arr,

@@ -223,6 +223,7 @@ __global__ void __launch_bounds__(NTT, MINB)
   __shared__ int red_cnt[NWT][MSPEC];
   __shared__ int s_w[NWT];
   __shared__ int s_nown, s_np, s_abort, s_tmp, s_adv, s_accq, s_dc_dirty, s_tw_dirty;
+  __shared__ int s_bd_hot, s_bd_scored, s_bd_acc;  // this chain's scored / accepted births + deaths
   __shared__ int s_specok;  // this round's proposals were generated during the last decision
   __shared__ unsigned long long s_births;
   __shared__ double s_delta[MSPEC], s_logr[MSPEC], s_prior[2];
@@ -286,6 +287,9 @@ __global__ void __launch_bounds__(NTT, MINB)
     s_dc_dirty = 1;
     s_tw_dirty = 1;
     s_specok = 0;
+    s_bd_hot = 0;
+    s_bd_scored = 0;
+    s_bd_acc = 0;
   }
   if (tid < 16) s_tprof[tid >> 3][tid & 7] = 0ull;  // kernels.cuh
   __syncthreads();
@@ -470,8 +474,11 @@ __global__ void __launch_bounds__(NTT, MINB)
       int f = 0;
       while (f < m - 1 && prop[buf][f].skip) ++f;
       // first_scored = 2: a birth or death (rarely accepted) takes the next
-      // scored proposal of the batch along
-      int more = sp.first_scored - 1;  // 2: one more, 3: as long as they are births / deaths
+      // scored proposal of the batch along. Not where this chain does accept
+      // them often (s_bd_hot: more than one in eight of its scored births /
+      // deaths this phase, e.g. configs 3 / 4, whose hypothesis swings by
+      // 400 k events per phase): there the round ends at its first scored one.
+      int more = s_bd_hot ? 0 : sp.first_scored - 1;  // 2: one more, 3: while births / deaths
       while (more > 0 && f < m - 1 && !prop[buf][f].skip && prop[buf][f].type <= 1) {
         ++f;
         while (f < m - 1 && prop[buf][f].skip) ++f;
@@ -713,21 +720,23 @@ __global__ void __launch_bounds__(NTT, MINB)
       // parallel lanes (delta_log_joint density.hpp:223-240; log_accept_ratio
       // and mh_step proposals.hpp:255-291). Lanes 8q..8q+7 reduce proposal q's
       // per-warp partials (fixed order, deterministic).
-      static_assert(MSPEC * 8 <= 32, "reduction layout");
-      const int q = lane >> 3, g = lane & 7;
+      // (kLPQ lanes per proposal: 8 with up to four proposals per round)
+      constexpr int kLPQ = MSPEC <= 4 ? 8 : (MSPEC <= 8 ? 4 : 2);
+      static_assert(MSPEC * kLPQ <= 32 && MSPEC <= 16, "reduction layout");
+      const int q = lane / kLPQ, g = lane % kLPQ;
       double sig = 0.0, A = 0.0;
       int c = 0;
       if (q < m)
-        for (int w = g; w < NWT; w += 8) {
+        for (int w = g; w < NWT; w += kLPQ) {
           sig += red_sig[w][q];
           A += red_arr[w][q];
           c += red_cnt[w][q];
         }
 #pragma unroll
-      for (int o = 4; o; o >>= 1) {
-        sig += __shfl_down_sync(0xffffffffu, sig, o, 8);
-        A += __shfl_down_sync(0xffffffffu, A, o, 8);
-        c += __shfl_down_sync(0xffffffffu, c, o, 8);
+      for (int o = kLPQ / 2; o; o >>= 1) {
+        sig += __shfl_down_sync(0xffffffffu, sig, o, kLPQ);
+        A += __shfl_down_sync(0xffffffffu, A, o, kLPQ);
+        c += __shfl_down_sync(0xffffffffu, c, o, kLPQ);
       }
       Prop& P = prop[buf][q < m ? q : 0];
       if (g == 0 && q < m && !P.skip) {
@@ -797,6 +806,7 @@ __global__ void __launch_bounds__(NTT, MINB)
           }
           continue;
         }
+        if (P.type <= 1) ++s_bd_scored;
         n_changed += (unsigned long long)s_cnt[q];
         n_arr += (P.type == 3) ? 2ull : (unsigned long long)d.S * (P.nr + P.na);
         const double delta = s_delta[q], log_r = s_logr[q];
@@ -895,6 +905,7 @@ __global__ void __launch_bounds__(NTT, MINB)
         }
         P.accept = 1;
         ++n_acc;
+        if (P.type <= 1) ++s_bd_acc;
         if (P.type == 0) ++births;
         // retire removed versions; deaths of this-phase versions free slots
         for (int r = 0; r < P.nr; ++r) {
@@ -978,6 +989,7 @@ __global__ void __launch_bounds__(NTT, MINB)
           if (at == (int)sp.k) break;
         }
       }
+      s_bd_hot = (s_bd_scored >= 4 && 8 * s_bd_acc > s_bd_scored) ? 1 : 0;
       s_adv = adv;
       s_accq = accq;
       s_specok = (MODE == 0 && accq < 0 && m_next > 0) ? 1 : 0;
